@@ -1,0 +1,180 @@
+/*
+ * mact_cuda.h — C ABI of libmact_cuda.so, the B200 (sm_100a) implementation of
+ * the MACT per-pixel colour-transform path (arXiv 1009.0854).
+ *
+ * The reference (`mact` 0.1.0, pure Python/numpy, /root/reference/pkg/src/mact)
+ * has no native FFI; its plugin seam is a Python callable
+ * `pixels (...,3) -> (...,3) float` (harness.py:71-74, :77-78).  Each entry point
+ * below replaces one such reference function and is bound from the Python
+ * mirror package `paper_1009_0854_b200` through ctypes (INTEGRATION.md shows
+ * the binding a maintainer would add to `mact` itself).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Unless stated otherwise pointers are DEVICE
+ *    pointers owned by the caller; the library allocates nothing on the hot
+ *    path.  `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *  - Calls are stream-ordered and asynchronous.
+ *  - Pixels are interleaved RGB, C order, `n` pixels (the reference's (...,3)
+ *    layout, harness.py:35-46).  Outputs are fp32 (the reference returns fp64,
+ *    exact.py:48-49; fp32 is the documented deviation, within the north-star
+ *    tolerance) — interleaved (N,3) or planar (3,N).
+ *  - Return status: MACT_OK, MACT_EBADARG (-> ValueError in Python),
+ *    MACT_EUNKNOWN_APPROX (-> UnknownApproximant), MACT_ECUDA (-> MactError);
+ *    `mact_last_error()` returns a thread-local message for the last failure.
+ */
+#ifndef MACT_CUDA_H
+#define MACT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  MACT_OK = 0,
+  MACT_EBADARG = 1,
+  MACT_EUNKNOWN_APPROX = 2,
+  MACT_ECUDA = 3
+};
+
+enum { MACT_SPACE_LAB = 0, MACT_SPACE_HSI = 1, MACT_SPACE_SCT = 2 };
+enum { MACT_LAYOUT_INTERLEAVED = 0, MACT_LAYOUT_PLANAR = 1 };
+enum { MACT_DTYPE_U8 = 0, MACT_DTYPE_F32 = 1, MACT_DTYPE_F64 = 2 };
+enum {
+  MACT_LUT_TRILINEAR = 0,
+  MACT_LUT_PRISM = 1,
+  MACT_LUT_PYRAMIDAL = 2,
+  MACT_LUT_TETRAHEDRAL = 3
+};
+enum { MACT_METRIC_DISTANCE = 0, MACT_METRIC_COMPONENT = 1 };
+enum { MACT_CAND_FAST = 0, MACT_CAND_LUT = 1, MACT_CAND_ARRAY = 2 };
+
+#define MACT_MAX_COEFFS 8
+
+/* Coefficient sets resolved from a MactConfig (fast.py:46-78).  Polynomials
+ * are ascending a_0..a_deg, evaluated by Horner highest-first
+ * (approximants.py:55-71).  Passed BY VALUE to every kernel as a
+ * __grid_constant__ parameter: no mutable device globals, so concurrent
+ * configurations on different streams are safe. */
+typedef struct MactCoeffs {
+  int32_t cbrt_num_deg, cbrt_den_deg;  /* CIELAB rational (n, m)      approximants.py:179-213 */
+  int32_t hsi_deg;                     /* atan(sqrt3 x) refit degree  fast.py:38-43          */
+  int32_t asin_deg, acos_deg, atan_deg;/* SCT (n_asin, m_acos, r_atan) fast.py:67-75         */
+  double cbrt_num[MACT_MAX_COEFFS];
+  double cbrt_den[MACT_MAX_COEFFS];
+  double atan_sqrt3[MACT_MAX_COEFFS];
+  double asin_half[MACT_MAX_COEFFS];   /* approximants.py:231-238 */
+  double acos_half[MACT_MAX_COEFFS];   /* approximants.py:240-247 */
+  double atan_f[MACT_MAX_COEFFS];      /* approximants.py:249-256 */
+  double atan_g[MACT_MAX_COEFFS];      /* approximants.py:258-265 */
+} MactCoeffs;
+
+/* Per-shard error-statistic partial (harness.py:63-74 semantics):
+ * sum of the metric (fp64), number of scored pixels, max value, GLOBAL index
+ * of the first pixel attaining it (index_base + local index), and the number
+ * of pixels excluded because the exact component is undefined (NaN). */
+typedef struct MactErrStats {
+  double sum;
+  double max;
+  uint64_t count;
+  uint64_t argmax;
+  uint64_t nan_count;
+  uint64_t _pad;
+} MactErrStats;
+
+/* Candidate description for the fused error reduction. */
+typedef struct MactErrSpec {
+  int32_t space;        /* MACT_SPACE_*                                      */
+  int32_t metric;       /* MACT_METRIC_DISTANCE (harness DISTANCES) or COMPONENT */
+  int32_t candidate;    /* MACT_CAND_FAST / _LUT / _ARRAY                      */
+  int32_t lut_grid_n;   /* for MACT_CAND_LUT                                   */
+  int32_t lut_method;   /* MACT_LUT_*                                          */
+  int32_t cand_dtype;   /* MACT_CAND_ARRAY: MACT_DTYPE_F32 / _F64, interleaved */
+  const float* lut_lattice;   /* (n^3, 3) fp32, r-major                        */
+  const void* cand_array;     /* (n, 3) candidate outputs                      */
+  const void* ref_array;      /* optional (n,3) reference outputs, NULL = exact on device */
+  int32_t ref_dtype;
+  int32_t _pad;
+} MactErrSpec;
+
+/* ---- MACT fast transforms (K1-K3) -------------------------------------- */
+/* replaces mact.fast.rgb_to_lab_fast (fast.py:86-107); in_dtype U8 takes the
+ * 256-entry gamma table path (fast.py:92-95), F32 the analytic path (:96-99). */
+int mact_lab_fast(const void* rgb, int in_dtype, float* out, int64_t n,
+                  const MactCoeffs* c, int layout, void* stream);
+/* replaces mact.fast.rgb_to_hsi_fast (fast.py:125-148) */
+int mact_hsi_fast(const void* rgb, int in_dtype, float* out, int64_t n,
+                  const MactCoeffs* c, int layout, void* stream);
+/* replaces mact.fast.rgb_to_sct_fast (fast.py:188-203) */
+int mact_sct_fast(const void* rgb, int in_dtype, float* out, int64_t n,
+                  const MactCoeffs* c, int layout, void* stream);
+/* all three from one read of the pixels (BASELINE config 5); any output may be NULL */
+int mact_all_fast(const uint8_t* rgb, float* lab, float* hsi, float* sct, int64_t n,
+                  const MactCoeffs* c, int layout, void* stream);
+
+/* ---- exact transforms, fp64 ground truth (K5) --------------------------- */
+/* replaces mact.exact.rgb_to_{lab,hsi,sct}_exact (exact.py:86-92, :119-137,
+ * :140-149); in_dtype U8/F32/F64, out_dtype F32/F64, interleaved. */
+int mact_exact(int space, const void* rgb, int in_dtype, void* out, int out_dtype,
+               int64_t n, void* stream);
+/* replaces mact.exact.sct_to_rgb (exact.py:152-160), fp64 in/out */
+int mact_sct_to_rgb(const double* sct, double* rgb, int64_t n, void* stream);
+/* replaces mact.exact.{lab,hsi}_distance / sct_distance_indirect (exact.py:163-190);
+ * x, y interleaved (n,3) of dtype F32/F64 each; out fp64 (n). */
+int mact_distance(int space, const void* x, int x_dtype, const void* y, int y_dtype,
+                  double* out, int64_t n, void* stream);
+
+/* ---- 3D LUT (K4) --------------------------------------------------------- */
+/* replaces mact.lut.build_lut (lut.py:82-95): lattice values at k*255/(n-1),
+ * NaN -> 0; writes fp64 (n^3,3) and/or fp32 (n^3,3), either may be NULL. */
+int mact_lut_build(int space, int grid_n, double* lattice_f64, float* lattice_f32,
+                   void* stream);
+/* replaces mact.lut.interpolate(lut, pixels, method, "standard") (lut.py:231-246,
+ * :341-350) for the linear (CIELAB) destination; in_dtype U8. */
+int mact_lut_interp(const float* lattice, int grid_n, int method, const uint8_t* rgb,
+                    float* out, int64_t n, int layout, void* stream);
+/* replaces mact.lut.node_weights (lut.py:115-199): flat node indices (n,k)
+ * and weights (n,k), k = 8/6/5/4; indices bit-exact with the reference. */
+int mact_lut_nodes(int grid_n, int method, const uint8_t* rgb, int64_t n,
+                   int32_t* nodes, float* weights, void* stream);
+
+/* ---- error reduction (K6) ------------------------------------------------ */
+/* Fused candidate + exact + metric + reduction over pixels rgb[0..n)
+ * (harness.measure_error semantics, harness.py:71-122; per-component abs error
+ * of SURVEY A21).  Writes 1 (DISTANCE) or 3 (COMPONENT) MactErrStats to
+ * `out` (device).  `workspace` must hold mact_err_workspace_bytes() bytes.
+ * `rgb` may be NULL with `cube_start` >= 0: pixels are then generated on
+ * device as the R-major cube enumeration index cube_start + i (harness.py:35-46). */
+size_t mact_err_workspace_bytes(void);
+int mact_err_reduce(const MactErrSpec* spec, const MactCoeffs* c, const uint8_t* rgb,
+                    int64_t cube_start, int64_t n, int64_t index_base, MactErrStats* out,
+                    void* workspace, void* stream);
+
+/* ---- pixel generators ---------------------------------------------------- */
+/* harness.cube_chunk (harness.py:35-46) on device: rgb[i] = cube pixel start+i */
+int mact_cube_fill(uint8_t* rgb, int64_t start, int64_t n, void* stream);
+
+/* ---- host streaming executor (end-to-end, HOST buffers) ------------------ */
+/* Runs a fast transform over HOST buffers: chunked H2D -> kernel -> D2H on
+ * `nstreams` CUDA streams so both copy engines and the SMs overlap.  Host
+ * buffers should be pinned (cudaHostAlloc / registered); pageable buffers are
+ * staged through pinned bounce buffers.  op = MACT_SPACE_* (fast transform). */
+typedef struct MactHostCtx MactHostCtx;
+int mact_host_ctx_create(int device, int64_t chunk_px, int nstreams, MactHostCtx** ctx);
+int mact_host_ctx_destroy(MactHostCtx* ctx);
+int mact_transform_host(MactHostCtx* ctx, int op, const uint8_t* host_rgb, float* host_out,
+                        int64_t n, const MactCoeffs* c, int layout);
+
+/* ---- misc ----------------------------------------------------------------- */
+const char* mact_last_error(void);
+int mact_version(void);
+/* number of kernel launches issued by this thread since the last reset */
+uint64_t mact_launch_count(void);
+void mact_launch_count_reset(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MACT_CUDA_H */

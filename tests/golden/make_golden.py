@@ -1,0 +1,229 @@
+"""Generate the golden fixtures under tests/golden/ from the REAL reference.
+
+Run in the build container, where /root/reference exists:
+
+    MACT_THREADS=8 python tests/golden/make_golden.py
+
+It imports ``mact`` 0.1.0 from /root/reference/pkg/src (read-only, never
+copied) and records its outputs on deterministic pixel sets, plus the
+full-cube / per-config error figures of SURVEY.md §8c-d.  The fixtures pin
+``oracle/mact_oracle.py`` (tests/test_oracle_golden.py); the oracle in turn is
+the checker for the CUDA path.  Nothing on the GPU box reads /root/reference.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+OUT = Path(__file__).resolve().parent
+
+
+def probe_pixels() -> dict:
+    """Deterministic pixel sets covering the edge cases of SURVEY.md §4.4."""
+    from mact import exact
+
+    sets = {}
+    sets["kat"] = np.array([
+        (255, 0, 0), (37, 201, 88), (0, 0, 1), (128, 128, 128), (100, 100, 100),
+        (0, 255, 0), (0, 0, 255), (0, 0, 0), (255, 255, 255), (20, 7, 13),
+        (2, 8, 47), (34, 1, 24), (209, 229, 179), (0, 1, 0), (255, 254, 242),
+        (200, 100, 100), (1, 0, 0), (255, 255, 0), (0, 255, 255), (255, 0, 255),
+    ], dtype=np.uint8)
+    v = np.arange(256, dtype=np.uint8)
+    sets["grays"] = np.stack([v, v, v], -1)
+    z = np.zeros(256, np.uint8)
+    sets["rg_zero"] = np.stack([z, z, v], -1)
+    rng = np.random.default_rng(20261019)
+    # HSI case 4: r > b, g == b
+    r = rng.integers(1, 256, 256)
+    k = (rng.random(256) * r).astype(np.int64)
+    sets["hsi_case4"] = np.stack([r, k, k], -1).astype(np.uint8)
+    # pixels whose X/Xw, Y/Yw or Z/Zw sit closest to the 0.008856 knee
+    idx = np.arange(1 << 24, dtype=np.uint32)
+    cube = np.stack([idx >> 16, (idx >> 8) & 255, idx & 255], -1).astype(np.uint8)
+    gt = exact.inverse_gamma(np.arange(256) / 255.0)
+    m = exact.RGB_TO_XYZ_MATRIX
+    white = (exact.WHITE_X, exact.WHITE_Y, exact.WHITE_Z)
+    knee = []
+    for row in range(3):
+        t = (m[row, 0] * gt[cube[:, 0]] + m[row, 1] * gt[cube[:, 1]]
+             + m[row, 2] * gt[cube[:, 2]]) / white[row]
+        near = np.argsort(np.abs(t - exact.LAB_KNEE))[:96]
+        knee.append(cube[near])
+    sets["knee"] = np.concatenate(knee)
+    # lattice-relevant channel values (faces p=255, near-boundary residues)
+    vals = np.array([0, 1, 8, 15, 16, 32, 127, 128, 223, 247, 254, 255], np.uint8)
+    g3 = np.stack(np.meshgrid(vals, vals, vals, indexing="ij"), -1).reshape(-1, 3)
+    sets["lattice_grid"] = g3
+    # two equal channels (simplex tie rules)
+    a = rng.integers(0, 256, (512,))
+    b = rng.integers(0, 256, (512,))
+    perm = rng.integers(0, 3, (512,))
+    ties = np.stack([a, a, b], -1)
+    ties[perm == 1] = ties[perm == 1][:, [0, 2, 1]]
+    ties[perm == 2] = ties[perm == 2][:, [2, 0, 1]]
+    sets["ties"] = ties.astype(np.uint8)
+    sets["random"] = rng.integers(0, 256, (2048, 3), dtype=np.uint8)
+    return sets
+
+
+def main() -> None:
+    sys.path.insert(0, str(REF))
+    os.environ.setdefault("MACT_THREADS", str(os.cpu_count() or 1))
+    from mact import exact, fast, harness, lut
+    from mact.fast import MactConfig
+
+    t0 = time.time()
+    sets = probe_pixels()
+    names = list(sets)
+    probe = np.concatenate([sets[k] for k in names])
+    offsets = np.cumsum([0] + [len(sets[k]) for k in names]).tolist()
+    small = np.concatenate([sets["kat"], sets["grays"], sets["rg_zero"], sets["ties"][:256],
+                            sets["lattice_grid"][::2], sets["random"][:256]])
+
+    arrays = {"probe": probe, "small": small}
+    cfg = fast.DEFAULT_CONFIG
+    arrays["lab_fast"] = fast.rgb_to_lab_fast(probe, cfg)
+    arrays["hsi_fast"] = fast.rgb_to_hsi_fast(probe, cfg)
+    arrays["sct_fast"] = fast.rgb_to_sct_fast(probe, cfg)
+    arrays["lab_exact"] = exact.rgb_to_lab_exact(probe)
+    arrays["hsi_exact"] = exact.rgb_to_hsi_exact(probe)
+    arrays["hsi_arccos"] = exact.rgb_to_hsi_arccos(probe)
+    arrays["sct_exact"] = exact.rgb_to_sct_exact(probe)
+    arrays["lab_dist"] = exact.lab_distance(arrays["lab_fast"], arrays["lab_exact"])
+    arrays["hsi_dist"] = exact.hsi_distance(arrays["hsi_fast"], arrays["hsi_exact"])
+    arrays["sct_dist"] = exact.sct_distance_indirect(arrays["sct_fast"], arrays["sct_exact"])
+    arrays["sct_to_rgb"] = exact.sct_to_rgb(arrays["sct_exact"])
+    # float-input fast path (analytic gamma, fast.py:96-99)
+    arrays["lab_fast_float"] = fast.rgb_to_lab_fast(small.astype(np.float64) + 0.25, cfg)
+    arrays["small_float"] = small.astype(np.float64) + 0.25
+    # other degree selections on the small set
+    for n, m in [(2, 2), (2, 3), (3, 2), (2, 4), (3, 3), (4, 2), (3, 4), (4, 3)]:
+        arrays[f"lab_fast_{n}{m}"] = fast.rgb_to_lab_fast(small, MactConfig(cielab_degrees=(n, m)))
+    for n in (2, 3, 4):
+        arrays[f"hsi_fast_{n}"] = fast.rgb_to_hsi_fast(small, MactConfig(hsi_degree=n))
+    for d in [(4, 4, 4), (4, 5, 4), (5, 4, 4), (5, 5, 4), (4, 4, 5), (4, 5, 5), (5, 4, 5)]:
+        arrays["sct_fast_" + "".join(map(str, d))] = fast.rgb_to_sct_fast(
+            small, MactConfig(sct_degrees=d))
+    # LUTs
+    for space in ("lab", "hsi", "sct"):
+        for n in (9, 17, 33):
+            L = lut.build_lut(space, n)
+            vals = L.values
+            if n == 33:
+                pick = np.random.default_rng(n).integers(0, n ** 3, 1024)
+                arrays[f"lut_{space}_{n}_sample_idx"] = pick
+                arrays[f"lut_{space}_{n}_sample"] = vals.reshape(-1, 3)[pick]
+                arrays[f"lut_{space}_{n}_sum"] = np.array([vals.sum(axis=(0, 1, 2))])
+            else:
+                arrays[f"lut_{space}_{n}"] = vals
+            for method in lut.METHODS:
+                if space == "lab":
+                    nodes, w = lut.node_weights(L, small, method)
+                    arrays[f"nodes_{n}_{method}"] = nodes.astype(np.int32)
+                    arrays[f"weights_{n}_{method}"] = w
+                    arrays[f"interp_lab_{n}_{method}"] = lut.interpolate(L, small, method)
+                    arrays[f"interp_lab_{n}_{method}_caching"] = lut.interpolate(
+                        lut.build_cache(L), small, method, "caching")
+                else:
+                    arrays[f"interp_{space}_{n}_{method}"] = lut.interpolate(L, small, method)
+    arrays["probe_offsets"] = np.array(offsets)
+    np.savez_compressed(OUT / "reference_outputs.npz", **arrays)
+    if "--arrays-only" in sys.argv:
+        print(f"arrays written in {time.time() - t0:.1f}s")
+        return
+
+    refit = {str(n): list(fast._atan_unit_interval(n).form.coeffs) for n in (2, 3, 4, 5)}
+    refit_eps = {str(n): float(fast._atan_unit_interval(n).eps_max) for n in (2, 3, 4, 5)}
+
+    # ------------------------------------------------------------ figures
+    def stats(s):
+        return {"avg": s.avg, "max": s.max, "count": s.count, "argmax_pixel": list(s.argmax_pixel)}
+
+    fig = {}
+    cube = {}
+    for n, m in [(2, 2), (2, 3), (3, 2), (2, 4), (3, 3), (4, 2), (3, 4), (4, 3), (4, 4)]:
+        c = MactConfig(cielab_degrees=(n, m))
+        cube[f"lab_{n}{m}"] = stats(harness.measure_error(
+            "lab", lambda p, c=c: fast.rgb_to_lab_fast(p, c), exact.rgb_to_lab_exact))
+    for n in (2, 3, 4, 5):
+        c = MactConfig(hsi_degree=n)
+        cube[f"hsi_{n}"] = stats(harness.measure_error(
+            "hsi", lambda p, c=c: fast.rgb_to_hsi_fast(p, c), exact.rgb_to_hsi_exact))
+    for d in [(4, 4, 4), (4, 5, 4), (5, 4, 4), (5, 5, 4), (4, 4, 5), (4, 5, 5), (5, 4, 5), (5, 5, 5)]:
+        c = MactConfig(sct_degrees=d)
+        cube["sct_" + "".join(map(str, d))] = stats(harness.measure_error(
+            "sct", lambda p, c=c: fast.rgb_to_sct_fast(p, c), exact.rgb_to_sct_exact))
+    for n in (9, 17, 33):
+        L = lut.build_lut("lab", n)
+        for method in lut.METHODS:
+            cube[f"lut_lab_{n}_{method}"] = stats(harness.measure_error(
+                "lab", lambda p, L=L, mm=method: lut.interpolate(L, p, mm), exact.rgb_to_lab_exact))
+    fig["cube"] = cube
+
+    # per-config figures
+    c1 = np.random.default_rng(0).integers(0, 256, size=(512, 512, 3), dtype=np.uint8)
+    fig["c1_lab"] = stats(harness.measure_error(
+        "lab", fast.rgb_to_lab_fast, exact.rgb_to_lab_exact, population=c1.reshape(-1, 3)))
+    c3 = np.random.default_rng(0).integers(0, 256, size=(4096, 4096, 3), dtype=np.uint8)
+    c3f = c3.reshape(-1, 3)
+    chunks = [c3f[s:s + (1 << 20)] for s in range(0, c3f.shape[0], 1 << 20)]
+    fig["c3_lab"] = stats(harness.measure_error("lab", fast.rgb_to_lab_fast,
+                                                exact.rgb_to_lab_exact, population=chunks))
+    c3lut = {}
+    for n in (17, 33):
+        L = lut.build_lut("lab", n)
+        for method in lut.METHODS:
+            c3lut[f"{n}_{method}"] = stats(harness.measure_error(
+                "lab", lambda p, L=L, mm=method: lut.interpolate(L, p, mm),
+                exact.rgb_to_lab_exact, population=chunks))
+    fig["c3_lut"] = c3lut
+    # checksum of the C1/C3 inputs so the fixtures prove the generator call
+    fig["c1_sum"] = int(c1.astype(np.int64).sum())
+    fig["c3_sum"] = int(c3.astype(np.int64).sum())
+
+    # A21 per-component absolute error over the cube (C2)
+    comp = {}
+    for space in ("hsi", "sct"):
+        acc = [{"sum": 0.0, "count": 0, "max": -1.0, "argmax": -1, "nan": 0} for _ in range(3)]
+        fsums = [[], [], []]
+        for start in range(0, 1 << 24, 1 << 20):
+            p = harness.cube_chunk(start, 1 << 20)
+            f = fast.rgb_to_hsi_fast(p) if space == "hsi" else fast.rgb_to_sct_fast(p)
+            e = exact.rgb_to_hsi_exact(p) if space == "hsi" else exact.rgb_to_sct_exact(p)
+            for c in range(3):
+                d = np.abs(f[:, c] - e[:, c])
+                if space == "hsi" and c == 0:
+                    d = np.minimum(d, 2 * np.pi - d)
+                nan = np.isnan(e[:, c]) | np.isnan(f[:, c])
+                dv = np.where(nan, -np.inf, d)
+                j = int(np.argmax(dv))
+                fsums[c].append(float(np.sum(d[~nan])))
+                acc[c]["count"] += int((~nan).sum())
+                acc[c]["nan"] += int(nan.sum())
+                if dv[j] > acc[c]["max"]:
+                    acc[c]["max"] = float(dv[j])
+                    acc[c]["argmax"] = start + j
+        import math
+        for c in range(3):
+            acc[c]["sum"] = math.fsum(fsums[c])
+            acc[c]["mean"] = acc[c]["sum"] / max(acc[c]["count"], 1)
+            a = acc[c]["argmax"]
+            acc[c]["argmax_pixel"] = [a >> 16, (a >> 8) & 255, a & 255]
+        comp[space] = acc
+    fig["c2_component"] = comp
+
+    (OUT / "figures.json").write_text(json.dumps(fig, indent=1))
+    (OUT / "hsi_refit.json").write_text(json.dumps({"coeffs": refit, "eps": refit_eps}, indent=1))
+    print(f"golden fixtures written in {time.time() - t0:.1f}s")
+
+
+if __name__ == "__main__":
+    main()
