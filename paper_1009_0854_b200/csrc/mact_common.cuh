@@ -1,0 +1,171 @@
+// mact_common.cuh — shared device helpers for libmact_cuda (sm_100a).
+//
+// Kernel-side coefficient block, PTX wrappers for the Blackwell bulk-copy
+// engine (cp.async.bulk = TMA 1-D, SASS UBLKCP) and mbarriers, cheap
+// float<->double bit conversions, and launch bookkeeping.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mact_cuda.h"
+
+namespace mact {
+
+constexpr double kPi = 3.14159265358979311600;   // np.pi
+constexpr double kTwoPi = 2.0 * kPi;
+
+// BT.709 / D65 constants (exact.py:21-40)
+constexpr double kGammaKnee = 0.081, kGammaSlope = 4.5, kGammaOffset = 0.099,
+                 kGammaScale = 1.099, kGammaPower = 1.0 / 0.45;
+constexpr double kWhiteX = 0.950456, kWhiteY = 1.0, kWhiteZ = 1.089058;
+constexpr double kLabKnee = 0.008856, kLabSlope = 7.787, kLabOffset = 16.0 / 116.0;
+__host__ __device__ constexpr double rgb2xyz(int row, int col) {
+  return row == 0 ? (col == 0 ? 0.412391 : col == 1 ? 0.357584 : 0.180481)
+       : row == 1 ? (col == 0 ? 0.212639 : col == 1 ? 0.715169 : 0.072192)
+                  : (col == 0 ? 0.019331 : col == 1 ? 0.119195 : 0.950532);
+}
+
+// Degree caps of the bundled sets: CIELAB rationals up to (4,4), the HSI
+// refit and SCT polynomials up to 5.  Unused high coefficients are zero,
+// which leaves Horner bit-identical (0*x + 0 = 0, then 0*x + a_n = a_n).
+constexpr int kCbrtDeg = 4;
+constexpr int kPolyDeg = 5;
+
+// Kernel parameter block built on the host from MactCoeffs (passed by value
+// as a __grid_constant__ parameter, so it lives in the constant bank and the
+// FMAs take coefficients as c[][] operands — no registers, no globals).
+struct KCoeffs {
+  double cbrt_num[kCbrtDeg + 1];
+  double cbrt_den[kCbrtDeg + 1];
+  double hsi_d[kPolyDeg + 1], asin_d[kPolyDeg + 1], acos_d[kPolyDeg + 1],
+      atanf_d[kPolyDeg + 1], atang_d[kPolyDeg + 1];
+  float hsi[kPolyDeg + 1], asin[kPolyDeg + 1], acos[kPolyDeg + 1], atanf[kPolyDeg + 1],
+      atang[kPolyDeg + 1];
+  float mxyz[9];   // RGB->XYZ rows pre-divided by the white point (fp32)
+};
+
+// ---------------------------------------------------------------- Horner
+template <int DEG>
+__device__ __forceinline__ float horner_f(const float* c, float x) {
+  float acc = c[DEG];
+#pragma unroll
+  for (int k = DEG - 1; k >= 0; --k) acc = fmaf(acc, x, c[k]);
+  return acc;
+}
+template <int DEG>
+__device__ __forceinline__ double horner_d(const double* c, double x) {
+  double acc = c[DEG];
+#pragma unroll
+  for (int k = DEG - 1; k >= 0; --k) acc = fma(acc, x, c[k]);
+  return acc;
+}
+
+// ------------------------------------------------- float <-> double bit moves
+// Valid for positive normal inputs (and harmless garbage-but-finite for +0).
+// They replace F2F.F64.F32 / F2F.F32.F64, which issue on the quarter-rate
+// conversion pipe, by 2-3 integer ops on the ALU pipe.
+__device__ __forceinline__ double f2d_pos(float f) {
+  uint32_t b = __float_as_uint(f);
+  uint32_t hi = (b >> 3) + 0x38000000u;
+  uint32_t lo = b << 29;
+  return __hiloint2double((int)hi, (int)lo);
+}
+// Truncating double->float for positive normal values inside float range.
+__device__ __forceinline__ float d2f_pos_trunc(double d) {
+  uint32_t hi = (uint32_t)__double2hiint(d) - 0x38000000u;
+  uint32_t lo = (uint32_t)__double2loint(d);
+  return __uint_as_float(__funnelshift_l(lo, hi, 3));
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) {
+  return __byte_perm(w, 0u, 0x4440u + (uint32_t)k);
+}
+
+// ------------------------------------------------ exact integer -> float
+// Magic-number conversion for 0 <= v < 2^23 (IADD + FADD instead of I2F).
+__device__ __forceinline__ float u2f_small(uint32_t v) {
+  return __uint_as_float(v + 0x4B000000u) - 8388608.0f;
+}
+
+// ------------------------------------------------------------ PTX: mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+// -------------------------------------------- PTX: bulk copy engine (TMA 1-D)
+// global -> shared, completion signalled on an mbarrier (complete_tx::bytes).
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// shared -> global, bulk-group completion.
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+// Make generic-proxy shared-memory writes visible to the async (bulk) proxy.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// ------------------------------------------------------------- host side
+void count_launch(int k = 1);
+int set_error(int code, const char* fmt, ...);
+int check_launch(const char* what);
+int num_sms();
+int make_kcoeffs(const MactCoeffs* c, KCoeffs* out);
+// Sets the dynamic-smem attribute once per (kernel, device) and returns the
+// persistent grid size occupancy x SM count (cached), or <= 0 on error.
+int persistent_grid(const void* fn, int threads, size_t smem_bytes);
+
+}  // namespace mact

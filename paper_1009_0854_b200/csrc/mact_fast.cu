@@ -1,0 +1,174 @@
+// mact_fast.cu — K1-K3 (+ fused triple): the MACT fast transforms.
+//
+//   mact_lab_fast  <- mact.fast.rgb_to_lab_fast  (fast.py:86-115)
+//   mact_hsi_fast  <- mact.fast.rgb_to_hsi_fast  (fast.py:118-148)
+//   mact_sct_fast  <- mact.fast.rgb_to_sct_fast  (fast.py:151-203)
+//   mact_all_fast  <- all three from one read of the pixels (BASELINE config 5)
+//
+// uint8 input runs the streaming kernel of mact_stream.cuh; real-valued
+// input (the reference's float path, fast.py:96-99) runs a per-pixel fp64
+// kernel that follows the reference formulas operation for operation.
+#include "mact_pixel.cuh"
+#include "mact_stream.cuh"
+
+namespace mact {
+
+// ---------------------------------------------------------------- ops
+struct OpLab {
+  static constexpr int NOUT = 1;
+  using Params = KCoeffs;
+  struct Shared {
+    float gamma[256 * 32];   // GAMMA_TABLE (fast.py:35) in fp32, replicated per bank
+  };
+  static __device__ __forceinline__ void init(Shared* s, const Params&) {
+    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
+      const int k = i >> 5;
+      s->gamma[i] = (float)inverse_gamma_d((double)k / 255.0);
+    }
+  }
+  static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
+                                            uint32_t lane, const Params& c, float (*o)[3]) {
+    const Lab3 v = lab_fast_u8(r, g, b, s->gamma, lane, c);
+    o[0][0] = v.c0; o[0][1] = v.c1; o[0][2] = v.c2;
+  }
+};
+
+struct OpHsi {
+  static constexpr int NOUT = 1;
+  using Params = KCoeffs;
+  struct Shared { int unused; };
+  static __device__ __forceinline__ void init(Shared*, const Params&) {}
+  static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared*,
+                                            uint32_t, const Params& c, float (*o)[3]) {
+    const Lab3 v = hsi_fast_u8((int)r, (int)g, (int)b, c);
+    o[0][0] = v.c0; o[0][1] = v.c1; o[0][2] = v.c2;
+  }
+};
+
+struct OpSct {
+  static constexpr int NOUT = 1;
+  using Params = KCoeffs;
+  struct Shared { int unused; };
+  static __device__ __forceinline__ void init(Shared*, const Params&) {}
+  static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared*,
+                                            uint32_t, const Params& c, float (*o)[3]) {
+    const Lab3 v = sct_fast_u8((int)r, (int)g, (int)b, c);
+    o[0][0] = v.c0; o[0][1] = v.c1; o[0][2] = v.c2;
+  }
+};
+
+struct OpAll {
+  static constexpr int NOUT = 3;
+  using Params = KCoeffs;
+  using Shared = OpLab::Shared;
+  static __device__ __forceinline__ void init(Shared* s, const Params& c) { OpLab::init(s, c); }
+  static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
+                                            uint32_t lane, const Params& c, float (*o)[3]) {
+    const Lab3 a = lab_fast_u8(r, g, b, s->gamma, lane, c);
+    const Lab3 h = hsi_fast_u8((int)r, (int)g, (int)b, c);
+    const Lab3 q = sct_fast_u8((int)r, (int)g, (int)b, c);
+    o[0][0] = a.c0; o[0][1] = a.c1; o[0][2] = a.c2;
+    o[1][0] = h.c0; o[1][1] = h.c1; o[1][2] = h.c2;
+    o[2][0] = q.c0; o[2][1] = q.c1; o[2][2] = q.c2;
+  }
+};
+
+// Real-valued input, fp64, reference formulas verbatim.
+template <typename T>
+__global__ void k_fast_real(int space, const T* __restrict__ in, float* __restrict__ out,
+                            int64_t n, int planar, const __grid_constant__ KCoeffs c) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double r = (double)in[3 * i], g = (double)in[3 * i + 1], b = (double)in[3 * i + 2];
+    double o[3];
+    if (space == MACT_SPACE_LAB) lab_fast_d(r, g, b, c, o);
+    else if (space == MACT_SPACE_HSI) hsi_fast_d(r, g, b, c, o);
+    else sct_fast_d(r, g, b, c, o);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (planar) out[k * n + i] = (float)o[k];
+      else out[3 * i + k] = (float)o[k];
+    }
+  }
+}
+
+// ------------------------------------------------------------ launchers
+template <class Op, int TP, int NT, int SIN>
+struct StreamCfg {
+  static constexpr int tp = TP, nt = NT, sin = SIN;
+};
+
+// Tile configurations (see DESIGN.md §Kernels for the smem/occupancy math).
+using CfgLab = StreamCfg<OpLab, 2048, 256, 3>;   // 98 KB smem -> 2 CTA/SM
+using CfgHsi = StreamCfg<OpHsi, 2048, 256, 3>;   // 66 KB -> 3 CTA/SM
+using CfgSct = StreamCfg<OpSct, 2048, 256, 3>;
+using CfgAll = StreamCfg<OpAll, 1024, 256, 2>;   // 110 KB -> 2 CTA/SM
+
+template <typename T>
+static int launch_real(int space, const T* in, float* out, int64_t n, int planar,
+                       const KCoeffs& kc, cudaStream_t st) {
+  if (n <= 0) return MACT_OK;
+  int64_t grid = (n + 255) / 256;
+  const int64_t cap = 8LL * num_sms();
+  if (grid > cap) grid = cap;
+  k_fast_real<T><<<(unsigned)grid, 256, 0, st>>>(space, in, out, n, planar, kc);
+  count_launch();
+  return check_launch("fast_real");
+}
+
+static int fast_entry(int space, const void* rgb, int in_dtype, float* out, int64_t n,
+                      const MactCoeffs* c, int layout, void* stream) {
+  if (n < 0 || (n > 0 && (rgb == nullptr || out == nullptr)) || c == nullptr)
+    return set_error(MACT_EBADARG, "bad argument (n=%lld)", (long long)n);
+  if (layout != MACT_LAYOUT_INTERLEAVED && layout != MACT_LAYOUT_PLANAR)
+    return set_error(MACT_EBADARG, "unknown layout %d", layout);
+  KCoeffs kc;
+  if (int rc = make_kcoeffs(c, &kc)) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int planar = layout == MACT_LAYOUT_PLANAR;
+  Outs outs{{out, nullptr, nullptr}};
+  const uint8_t* in = (const uint8_t*)rgb;
+  switch (in_dtype) {
+    case MACT_DTYPE_U8:
+      if (space == MACT_SPACE_LAB)
+        return launch_stream_t<OpLab, CfgLab::tp, CfgLab::nt, CfgLab::sin>(in, outs, n, planar, kc, st, "lab_fast");
+      if (space == MACT_SPACE_HSI)
+        return launch_stream_t<OpHsi, CfgHsi::tp, CfgHsi::nt, CfgHsi::sin>(in, outs, n, planar, kc, st, "hsi_fast");
+      return launch_stream_t<OpSct, CfgSct::tp, CfgSct::nt, CfgSct::sin>(in, outs, n, planar, kc, st, "sct_fast");
+    case MACT_DTYPE_F32:
+      return launch_real<float>(space, (const float*)rgb, out, n, planar, kc, st);
+    case MACT_DTYPE_F64:
+      return launch_real<double>(space, (const double*)rgb, out, n, planar, kc, st);
+    default:
+      return set_error(MACT_EBADARG, "unsupported input dtype %d", in_dtype);
+  }
+}
+
+}  // namespace mact
+
+using namespace mact;
+
+extern "C" int mact_lab_fast(const void* rgb, int in_dtype, float* out, int64_t n,
+                             const MactCoeffs* c, int layout, void* stream) {
+  return fast_entry(MACT_SPACE_LAB, rgb, in_dtype, out, n, c, layout, stream);
+}
+extern "C" int mact_hsi_fast(const void* rgb, int in_dtype, float* out, int64_t n,
+                             const MactCoeffs* c, int layout, void* stream) {
+  return fast_entry(MACT_SPACE_HSI, rgb, in_dtype, out, n, c, layout, stream);
+}
+extern "C" int mact_sct_fast(const void* rgb, int in_dtype, float* out, int64_t n,
+                             const MactCoeffs* c, int layout, void* stream) {
+  return fast_entry(MACT_SPACE_SCT, rgb, in_dtype, out, n, c, layout, stream);
+}
+extern "C" int mact_all_fast(const uint8_t* rgb, float* lab, float* hsi, float* sct, int64_t n,
+                             const MactCoeffs* c, int layout, void* stream) {
+  if (n < 0 || (n > 0 && rgb == nullptr) || c == nullptr)
+    return set_error(MACT_EBADARG, "bad argument (n=%lld)", (long long)n);
+  if (layout != MACT_LAYOUT_INTERLEAVED && layout != MACT_LAYOUT_PLANAR)
+    return set_error(MACT_EBADARG, "unknown layout %d", layout);
+  KCoeffs kc;
+  if (int rc = make_kcoeffs(c, &kc)) return rc;
+  Outs outs{{lab, hsi, sct}};
+  return launch_stream_t<OpAll, CfgAll::tp, CfgAll::nt, CfgAll::sin>(
+      rgb, outs, n, layout == MACT_LAYOUT_PLANAR, kc, (cudaStream_t)stream, "all_fast");
+}

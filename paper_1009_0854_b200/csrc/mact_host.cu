@@ -1,0 +1,181 @@
+// mact_host.cu — host streaming executor: the end-to-end path over HOST buffers.
+//
+// The reference's transforms take and return host numpy arrays
+// (fast.py:86, :125, :188).  A drop-in therefore pays host<->device
+// transfers; this executor hides them behind each other and behind compute:
+// the pixel stream is cut into chunks, chunk k runs H2D -> kernel -> D2H on
+// stream k % nstreams, so the H2D engine, the SMs and the D2H engine work on
+// three different chunks at once.  Pinned host buffers are DMA'd directly;
+// pageable buffers are staged through pinned bounce buffers, with the CPU
+// memcpy of chunk k overlapping the DMA of chunk k-1.
+#include <cstring>
+#include <vector>
+
+#include "mact_common.cuh"
+
+struct MactHostCtx {
+  int device = 0;
+  int64_t chunk = 0;
+  int nstreams = 0;
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> done;        // per stream: last D2H of that slot finished
+  std::vector<uint8_t*> d_in;
+  std::vector<float*> d_out;
+  std::vector<uint8_t*> h_in;           // pinned bounce buffers (pageable callers)
+  std::vector<float*> h_out;
+};
+
+using namespace mact;
+
+static bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+extern "C" int mact_host_ctx_create(int device, int64_t chunk_px, int nstreams, MactHostCtx** out) {
+  if (!out || chunk_px <= 0 || nstreams <= 0 || nstreams > 16)
+    return set_error(MACT_EBADARG, "bad host-context arguments");
+  chunk_px = (chunk_px + 2047) / 2048 * 2048;
+  auto* c = new MactHostCtx();
+  c->device = device;
+  c->chunk = chunk_px;
+  c->nstreams = nstreams;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaError_t e = cudaSetDevice(device);
+  for (int s = 0; s < nstreams && e == cudaSuccess; ++s) {
+    cudaStream_t st;
+    cudaEvent_t ev;
+    uint8_t* di = nullptr;
+    float* dout = nullptr;
+    if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) break;
+    c->streams.push_back(st);
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) break;
+    c->done.push_back(ev);
+    if ((e = cudaMalloc(&di, (size_t)chunk_px * 3)) != cudaSuccess) break;
+    c->d_in.push_back(di);
+    if ((e = cudaMalloc(&dout, (size_t)chunk_px * 12)) != cudaSuccess) break;
+    c->d_out.push_back(dout);
+  }
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    mact_host_ctx_destroy(c);
+    return set_error(MACT_ECUDA, "host context: %s", cudaGetErrorString(e));
+  }
+  *out = c;
+  return MACT_OK;
+}
+
+extern "C" int mact_host_ctx_destroy(MactHostCtx* c) {
+  if (!c) return MACT_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(c->device);
+  for (auto s : c->streams) cudaStreamSynchronize(s);
+  for (auto p : c->d_in) cudaFree(p);
+  for (auto p : c->d_out) cudaFree(p);
+  for (auto p : c->h_in) cudaFreeHost(p);
+  for (auto p : c->h_out) cudaFreeHost(p);
+  for (auto e : c->done) cudaEventDestroy(e);
+  for (auto s : c->streams) cudaStreamDestroy(s);
+  cudaSetDevice(prev);
+  delete c;
+  return MACT_OK;
+}
+
+static int ensure_bounce(MactHostCtx* c) {
+  if (!c->h_in.empty()) return MACT_OK;
+  for (int s = 0; s < c->nstreams; ++s) {
+    uint8_t* hi = nullptr;
+    float* ho = nullptr;
+    cudaError_t e = cudaHostAlloc(&hi, (size_t)c->chunk * 3, cudaHostAllocDefault);
+    if (e == cudaSuccess) e = cudaHostAlloc(&ho, (size_t)c->chunk * 12, cudaHostAllocDefault);
+    if (e != cudaSuccess) return set_error(MACT_ECUDA, "pinned bounce buffers: %s", cudaGetErrorString(e));
+    c->h_in.push_back(hi);
+    c->h_out.push_back(ho);
+  }
+  return MACT_OK;
+}
+
+static int run_kernel(int op, const uint8_t* din, float* dout, int64_t n, const MactCoeffs* cf,
+                      int layout, cudaStream_t st) {
+  switch (op) {
+    case MACT_SPACE_LAB: return mact_lab_fast(din, MACT_DTYPE_U8, dout, n, cf, layout, st);
+    case MACT_SPACE_HSI: return mact_hsi_fast(din, MACT_DTYPE_U8, dout, n, cf, layout, st);
+    case MACT_SPACE_SCT: return mact_sct_fast(din, MACT_DTYPE_U8, dout, n, cf, layout, st);
+  }
+  return set_error(MACT_EBADARG, "unknown transform %d", op);
+}
+
+// D2H of one chunk's result; planar output lands in 3 strided host planes.
+static cudaError_t copy_out(float* host_out, const float* dout, int64_t off, int64_t m, int64_t n,
+                            int layout, cudaStream_t st) {
+  if (layout == MACT_LAYOUT_INTERLEAVED)
+    return cudaMemcpyAsync(host_out + 3 * off, dout, (size_t)m * 12, cudaMemcpyDeviceToHost, st);
+  return cudaMemcpy2DAsync(host_out + off, (size_t)n * 4, dout, (size_t)m * 4, (size_t)m * 4, 3,
+                           cudaMemcpyDeviceToHost, st);
+}
+
+extern "C" int mact_transform_host(MactHostCtx* c, int op, const uint8_t* host_rgb, float* host_out,
+                                   int64_t n, const MactCoeffs* cf, int layout) {
+  if (!c || n < 0 || (n > 0 && (!host_rgb || !host_out)) || !cf)
+    return set_error(MACT_EBADARG, "bad argument");
+  if (n == 0) return MACT_OK;
+  if (op < 0 || op > 2) return set_error(MACT_EBADARG, "unknown transform %d", op);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(c->device);
+  const bool direct = is_pinned(host_rgb) && is_pinned(host_out);
+  int rc = MACT_OK;
+  if (!direct) rc = ensure_bounce(c);
+  const int64_t nchunks = (n + c->chunk - 1) / c->chunk;
+  // slot bookkeeping for pageable callers: chunk that last used each slot
+  std::vector<int64_t> pending(c->nstreams, -1);
+  auto drain = [&](int s) -> int {
+    const int64_t k = pending[s];
+    if (k < 0) return MACT_OK;
+    cudaError_t e = cudaEventSynchronize(c->done[s]);
+    if (e != cudaSuccess) return set_error(MACT_ECUDA, "d2h: %s", cudaGetErrorString(e));
+    const int64_t off = k * c->chunk, m = std::min<int64_t>(c->chunk, n - off);
+    if (layout == MACT_LAYOUT_INTERLEAVED) {
+      memcpy(host_out + 3 * off, c->h_out[s], (size_t)m * 12);
+    } else {
+      for (int p = 0; p < 3; ++p) memcpy(host_out + p * n + off, c->h_out[s] + p * m, (size_t)m * 4);
+    }
+    pending[s] = -1;
+    return MACT_OK;
+  };
+  for (int64_t k = 0; k < nchunks && rc == MACT_OK; ++k) {
+    const int s = (int)(k % c->nstreams);
+    cudaStream_t st = c->streams[s];
+    const int64_t off = k * c->chunk, m = std::min<int64_t>(c->chunk, n - off);
+    cudaError_t e;
+    if (direct) {
+      e = cudaMemcpyAsync(c->d_in[s], host_rgb + 3 * off, (size_t)m * 3, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) rc = run_kernel(op, c->d_in[s], c->d_out[s], m, cf, layout, st);
+      if (rc == MACT_OK && e == cudaSuccess) e = copy_out(host_out, c->d_out[s], off, m, n, layout, st);
+    } else {
+      if ((rc = drain(s)) != MACT_OK) break;
+      memcpy(c->h_in[s], host_rgb + 3 * off, (size_t)m * 3);
+      e = cudaMemcpyAsync(c->d_in[s], c->h_in[s], (size_t)m * 3, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) rc = run_kernel(op, c->d_in[s], c->d_out[s], m, cf, layout, st);
+      if (rc == MACT_OK && e == cudaSuccess)
+        e = cudaMemcpyAsync(c->h_out[s], c->d_out[s], (size_t)m * 12, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaEventRecord(c->done[s], st);
+      pending[s] = k;
+    }
+    if (e != cudaSuccess) rc = set_error(MACT_ECUDA, "host stream: %s", cudaGetErrorString(e));
+  }
+  if (!direct)
+    for (int s = 0; s < c->nstreams && rc == MACT_OK; ++s) rc = drain(s);
+  for (auto st : c->streams) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess && rc == MACT_OK) rc = set_error(MACT_ECUDA, "sync: %s", cudaGetErrorString(e));
+  }
+  cudaSetDevice(prev);
+  return rc;
+}

@@ -1,0 +1,183 @@
+// mact_lut.cu — K4: 3D-LUT build, node selection and interpolation.
+//
+//   mact_lut_build   <- lut.build_lut        (lut.py:77-95)
+//   mact_lut_nodes   <- lut.node_weights     (lut.py:115-199)
+//   mact_lut_interp  <- lut.interpolate(..., variant="standard") for the linear
+//                       CIELAB destination   (lut.py:231-246, :341-350)
+//
+// Interpolation runs inside the streaming skeleton (mact_stream.cuh).  For
+// grids 9^3 and 17^3 the lattice is staged once per persistent CTA into
+// shared memory as float4-padded nodes (17^3 x 16 B = 78.6 KB): one LDS.128
+// per node.  33^3 (431 KB packed) exceeds a CTA's 227 KB and is read through
+// the read-only L1/L2 path.
+#include "mact_lut.cuh"
+#include "mact_pixel.cuh"
+#include "mact_stream.cuh"
+
+namespace mact {
+
+struct LutParams {
+  const float* lat;   // (n^3, 3) fp32, r-major
+};
+
+template <int N, int METHOD>
+struct OpLut {
+  static constexpr int NOUT = 1;
+  static constexpr bool SMEM = N <= 17;
+  using Params = LutParams;
+  struct Shared {
+    float4 lat[SMEM ? N * N * N : 1];
+  };
+  static __device__ __forceinline__ void init(Shared* s, const Params& p) {
+    if constexpr (SMEM) {
+      for (int i = threadIdx.x; i < N * N * N; i += blockDim.x)
+        s->lat[i] = make_float4(__ldg(p.lat + 3 * i), __ldg(p.lat + 3 * i + 1),
+                                __ldg(p.lat + 3 * i + 2), 0.0f);
+    }
+  }
+  static __device__ __forceinline__ float3 node(const Shared* s, const Params& p, int i) {
+    if constexpr (SMEM) {
+      const float4 v = s->lat[i];
+      return make_float3(v.x, v.y, v.z);
+    } else {
+      return make_float3(__ldg(p.lat + 3 * i), __ldg(p.lat + 3 * i + 1), __ldg(p.lat + 3 * i + 2));
+    }
+  }
+  static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
+                                            uint32_t, const Params& p, float (*o)[3]) {
+    constexpr int K = LutK<METHOD>::K;
+    int idx[K];
+    float w[K];
+    lut_nodes<N, METHOD>(r, g, b, idx, w);
+    float3 v = node(s, p, idx[0]);
+    float a0 = w[0] * v.x, a1 = w[0] * v.y, a2 = w[0] * v.z;
+#pragma unroll
+    for (int j = 1; j < K; ++j) {
+      v = node(s, p, idx[j]);
+      a0 = fmaf(w[j], v.x, a0);
+      a1 = fmaf(w[j], v.y, a1);
+      a2 = fmaf(w[j], v.z, a2);
+    }
+    o[0][0] = a0; o[0][1] = a1; o[0][2] = a2;
+  }
+};
+
+// ---------------------------------------------------------------- build
+__global__ void k_lut_build(int space, int n, double* __restrict__ f64, float* __restrict__ f32) {
+  const int total = n * n * n;
+  const double spacing = 255.0 / (n - 1);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int ir = i / (n * n), ig = (i / n) % n, ib = i % n;
+    double o[3];
+    const double r = ir * spacing, g = ig * spacing, b = ib * spacing;   // lattice_coordinates
+    if (space == MACT_SPACE_LAB) lab_exact_d(r, g, b, o);
+    else if (space == MACT_SPACE_HSI) hsi_exact_d(r, g, b, o);
+    else sct_exact_d(r, g, b, o);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double v = isnan(o[k]) ? 0.0 : o[k];                        // nan_to_num (lut.py:92)
+      if (f64) f64[3 * i + k] = v;
+      if (f32) f32[3 * i + k] = (float)v;
+    }
+  }
+}
+
+// --------------------------------------------------------------- nodes
+template <int N, int METHOD>
+__global__ void k_lut_nodes(const uint8_t* __restrict__ rgb, int64_t n, int32_t* __restrict__ nodes,
+                            float* __restrict__ weights) {
+  constexpr int K = LutK<METHOD>::K;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int idx[K];
+    float w[K];
+    lut_nodes<N, METHOD>(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2], idx, w);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      nodes[i * K + j] = idx[j];
+      weights[i * K + j] = w[j];
+    }
+  }
+}
+
+template <int N, int METHOD>
+static int launch_interp(const float* lat, const uint8_t* rgb, float* out, int64_t n, int planar,
+                         cudaStream_t st) {
+  constexpr int TP = N <= 9 ? 2048 : 1024;
+  Outs outs{{out, nullptr, nullptr}};
+  LutParams p{lat};
+  return launch_stream_t<OpLut<N, METHOD>, TP, 256, 3>(rgb, outs, n, planar, p, st, "lut_interp");
+}
+
+template <int N>
+static int interp_grid(int method, const float* lat, const uint8_t* rgb, float* out, int64_t n,
+                       int planar, cudaStream_t st) {
+  switch (method) {
+    case MACT_LUT_TRILINEAR: return launch_interp<N, MACT_LUT_TRILINEAR>(lat, rgb, out, n, planar, st);
+    case MACT_LUT_PRISM: return launch_interp<N, MACT_LUT_PRISM>(lat, rgb, out, n, planar, st);
+    case MACT_LUT_PYRAMIDAL: return launch_interp<N, MACT_LUT_PYRAMIDAL>(lat, rgb, out, n, planar, st);
+    case MACT_LUT_TETRAHEDRAL: return launch_interp<N, MACT_LUT_TETRAHEDRAL>(lat, rgb, out, n, planar, st);
+  }
+  return set_error(MACT_EBADARG, "unknown interpolation method %d", method);
+}
+
+template <int N>
+static int nodes_grid(int method, const uint8_t* rgb, int64_t n, int32_t* nodes, float* w,
+                      cudaStream_t st) {
+  int64_t g = (n + 255) / 256;
+  if (g > 8LL * num_sms()) g = 8LL * num_sms();
+  switch (method) {
+    case MACT_LUT_TRILINEAR: k_lut_nodes<N, MACT_LUT_TRILINEAR><<<(unsigned)g, 256, 0, st>>>(rgb, n, nodes, w); break;
+    case MACT_LUT_PRISM: k_lut_nodes<N, MACT_LUT_PRISM><<<(unsigned)g, 256, 0, st>>>(rgb, n, nodes, w); break;
+    case MACT_LUT_PYRAMIDAL: k_lut_nodes<N, MACT_LUT_PYRAMIDAL><<<(unsigned)g, 256, 0, st>>>(rgb, n, nodes, w); break;
+    case MACT_LUT_TETRAHEDRAL: k_lut_nodes<N, MACT_LUT_TETRAHEDRAL><<<(unsigned)g, 256, 0, st>>>(rgb, n, nodes, w); break;
+    default: return set_error(MACT_EBADARG, "unknown interpolation method %d", method);
+  }
+  count_launch();
+  return check_launch("lut_nodes");
+}
+
+}  // namespace mact
+
+using namespace mact;
+
+extern "C" int mact_lut_build(int space, int grid_n, double* lattice_f64, float* lattice_f32,
+                              void* stream) {
+  if (space < 0 || space > 2) return set_error(MACT_EBADARG, "unknown destination space %d", space);
+  if (grid_n != 9 && grid_n != 17 && grid_n != 33)
+    return set_error(MACT_EBADARG, "grid_n must be one of 9, 17, 33");
+  if (!lattice_f64 && !lattice_f32) return set_error(MACT_EBADARG, "no output lattice");
+  const int total = grid_n * grid_n * grid_n;
+  k_lut_build<<<(total + 255) / 256, 256, 0, (cudaStream_t)stream>>>(space, grid_n, lattice_f64,
+                                                                     lattice_f32);
+  count_launch();
+  return check_launch("lut_build");
+}
+
+extern "C" int mact_lut_interp(const float* lattice, int grid_n, int method, const uint8_t* rgb,
+                               float* out, int64_t n, int layout, void* stream) {
+  if (n < 0 || (n > 0 && (!lattice || !rgb || !out))) return set_error(MACT_EBADARG, "bad argument");
+  if (layout != MACT_LAYOUT_INTERLEAVED && layout != MACT_LAYOUT_PLANAR)
+    return set_error(MACT_EBADARG, "unknown layout %d", layout);
+  const int planar = layout == MACT_LAYOUT_PLANAR;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (grid_n) {
+    case 9: return interp_grid<9>(method, lattice, rgb, out, n, planar, st);
+    case 17: return interp_grid<17>(method, lattice, rgb, out, n, planar, st);
+    case 33: return interp_grid<33>(method, lattice, rgb, out, n, planar, st);
+  }
+  return set_error(MACT_EBADARG, "grid_n must be one of 9, 17, 33");
+}
+
+extern "C" int mact_lut_nodes(int grid_n, int method, const uint8_t* rgb, int64_t n,
+                              int32_t* nodes, float* weights, void* stream) {
+  if (n < 0 || (n > 0 && (!rgb || !nodes || !weights))) return set_error(MACT_EBADARG, "bad argument");
+  if (n == 0) return MACT_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (grid_n) {
+    case 9: return nodes_grid<9>(method, rgb, n, nodes, weights, st);
+    case 17: return nodes_grid<17>(method, rgb, n, nodes, weights, st);
+    case 33: return nodes_grid<33>(method, rgb, n, nodes, weights, st);
+  }
+  return set_error(MACT_EBADARG, "grid_n must be one of 9, 17, 33");
+}

@@ -1,0 +1,102 @@
+// mact_lut.cuh — 3D-LUT cell location and simplex selection (K4 device side).
+//
+// Follows mact/lut.py:98-199 with INTEGER arithmetic:
+//   x = p (n-1) ; base = min(x div 255, n-2) ; rem = x - 255 base   (lut.py:98-105)
+// so frac = rem/255 and every comparison between offsets (prism dg >= db,
+// pyramid strict/tie rules, tetrahedral stable descending sort) is made on
+// the integers rem_r, rem_g, rem_b.  Because spacing = 255/(n-1) is an exact
+// binary fraction for n in {9,17,33}, the reference's fp64 frac is the
+// correctly rounded rem/255 and orders identically (tests pin this on the
+// full cube).  Weights are integer products / 255^k, exact until one final
+// rounding.  Node order and accumulation order match the reference
+// (out += w_j * V[node_j], j ascending, lut.py:233-236).
+#pragma once
+
+#include "mact_common.cuh"
+
+namespace mact {
+
+template <int METHOD>
+struct LutK;
+template <> struct LutK<MACT_LUT_TRILINEAR> { static constexpr int K = 8; };
+template <> struct LutK<MACT_LUT_PRISM> { static constexpr int K = 6; };
+template <> struct LutK<MACT_LUT_PYRAMIDAL> { static constexpr int K = 5; };
+template <> struct LutK<MACT_LUT_TETRAHEDRAL> { static constexpr int K = 4; };
+
+template <int N>
+__device__ __forceinline__ void lut_locate(uint32_t p, int& base, int& rem) {
+  const int x = (int)p * (N - 1);
+  int bse = x / 255;
+  bse = bse > N - 2 ? N - 2 : bse;
+  base = bse;
+  rem = x - 255 * bse;
+}
+
+// Node flat indices and weights of one pixel.  rem values in [0,255].
+template <int N, int METHOD>
+__device__ __forceinline__ void lut_nodes(uint32_t pr, uint32_t pg, uint32_t pb,
+                                          int (&idx)[LutK<METHOD>::K],
+                                          float (&w)[LutK<METHOD>::K]) {
+  constexpr int SR = N * N, SG = N, SB = 1;
+  int br, bg, bb, rr, rg, rb;
+  lut_locate<N>(pr, br, rr);
+  lut_locate<N>(pg, bg, rg);
+  lut_locate<N>(pb, bb, rb);
+  const int bf = (br * N + bg) * N + bb;
+  const float fr = (float)rr, fg = (float)rg, fb = (float)rb;
+  constexpr float inv1 = (float)(1.0 / 255.0);
+  constexpr float inv2 = (float)(1.0 / (255.0 * 255.0));
+  constexpr float inv3 = (float)(1.0 / (255.0 * 255.0 * 255.0));
+  if constexpr (METHOD == MACT_LUT_TRILINEAR) {
+    const float ar[2] = {255.0f - fr, fr}, ag[2] = {255.0f - fg, fg}, ab[2] = {255.0f - fb, fb};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int cr = c >> 2 & 1, cg = c >> 1 & 1, cb = c & 1;
+      idx[c] = bf + cr * SR + cg * SG + cb * SB;
+      w[c] = (ar[cr] * ag[cg] * ab[cb]) * inv3;      // product < 2^24: exact
+    }
+  } else if constexpr (METHOD == MACT_LUT_PRISM) {
+    const bool up = rg >= rb;                        // lut.py:146
+    const float ta = up ? 255.0f - fg : 255.0f - fb;
+    const float tb = (float)(up ? rg - rb : rb - rg);
+    const float tc = up ? fb : fg;
+    const int mid = up ? SG : SB, far = SG + SB;
+    const float a0 = 255.0f - fr;
+    idx[0] = bf; idx[1] = bf + mid; idx[2] = bf + far;
+    idx[3] = bf + SR; idx[4] = bf + mid + SR; idx[5] = bf + far + SR;
+    w[0] = ta * a0 * inv2; w[1] = tb * a0 * inv2; w[2] = tc * a0 * inv2;
+    w[3] = ta * fr * inv2; w[4] = tb * fr * inv2; w[5] = tc * fr * inv2;
+  } else if constexpr (METHOD == MACT_LUT_PYRAMIDAL) {
+    const bool sel_r = (rg > rr) & (rb > rr);        // lut.py:166-167
+    const bool sel_g = !sel_r & (rr >= rg) & (rb >= rg);
+    const int m = sel_r ? rr : sel_g ? rg : rb;
+    const int u = sel_r ? rg : rr;
+    const int v = sel_r ? rb : sel_g ? rb : rg;
+    const int nu = sel_r ? SG : SR;
+    const int nv = (sel_r | sel_g) ? SB : SG;
+    const float fu = (float)u, fv = (float)v;
+    idx[0] = bf; idx[1] = bf + nu; idx[2] = bf + nv; idx[3] = bf + nu + nv;
+    idx[4] = bf + SR + SG + SB;
+    w[0] = (255.0f - fu) * (255.0f - fv) * inv2;
+    w[1] = fu * (255.0f - fv) * inv2;
+    w[2] = fv * (255.0f - fu) * inv2;
+    w[3] = (float)(u * v - 255 * m) * inv2;
+    w[4] = (float)m * inv1;
+  } else {
+    // stable argsort of -d (lut.py:185): ties keep r before g before b
+    const int pos_r = (rg > rr) + (rb > rr);
+    const int pos_g = (rr >= rg) + (rb > rg);
+    const int s1 = pos_r == 0 ? SR : pos_g == 0 ? SG : SB;
+    const int d1 = pos_r == 0 ? rr : pos_g == 0 ? rg : rb;
+    const int s2 = pos_r == 1 ? SR : pos_g == 1 ? SG : SB;
+    const int d2 = pos_r == 1 ? rr : pos_g == 1 ? rg : rb;
+    const int d3 = pos_r == 2 ? rr : pos_g == 2 ? rg : rb;
+    idx[0] = bf; idx[1] = bf + s1; idx[2] = bf + s1 + s2; idx[3] = bf + SR + SG + SB;
+    w[0] = (float)(255 - d1) * inv1;
+    w[1] = (float)(d1 - d2) * inv1;
+    w[2] = (float)(d2 - d3) * inv1;
+    w[3] = (float)d3 * inv1;
+  }
+}
+
+}  // namespace mact

@@ -1,0 +1,301 @@
+// mact_pixel.cuh — per-pixel device functions of the MACT path.
+//
+//   lab_fast_u8  <- fast.rgb_to_lab_fast integer path   (fast.py:86-115)
+//   hsi_fast_u8  <- fast.rgb_to_hsi_fast                 (fast.py:118-148)
+//   sct_fast_u8  <- fast.rgb_to_sct_fast                 (fast.py:151-203)
+//   *_fast_d     <- the same functions on real-valued channels, fp64
+//   *_exact_d    <- exact.rgb_to_*_exact                 (exact.py:52-149)
+//   distances    <- exact.{lab,hsi}_distance, sct_distance_indirect (exact.py:163-190)
+//
+// Precision design:
+//  * HSI and SCT run in fp32 with every branch predicate and every
+//    numerator/denominator formed in exact integer arithmetic, so case
+//    selection is bit-identical to the reference's fp64 compares.
+//  * SCT's folded-arcsin argument uses the cancellation-free
+//    1 - b/L = (r^2+g^2) / (L (L+b))  (H2).
+//  * CIELAB: fp32 gamma table + fp32 3x3 (white folded in), then the rational
+//    P/Q in fp64 Horner and a double-float quotient q0 + r/Q, carried as a
+//    (hi, lo) pair through L*, a*, b* so that 500 (fx - fy) does not amplify
+//    fp32 rounding (H1).
+#pragma once
+
+#include "mact_common.cuh"
+
+namespace mact {
+
+// ---------------------------------------------------------------- gamma
+// inverse_gamma(i/255) exactly as exact.py:52-57 (fp64 pow).
+__device__ __forceinline__ double inverse_gamma_d(double k) {
+  return k < kGammaKnee ? k / kGammaSlope : pow((k + kGammaOffset) / kGammaScale, kGammaPower);
+}
+
+// -------------------------------------------------------------- CIELAB fast
+// Lightness kernel branch f(t) as a double-float (hi + lo), fast.py:110-115.
+__device__ __forceinline__ void lab_f_fast_df(float t, const KCoeffs& c, float& hi, float& lo) {
+  const double td = f2d_pos(t);
+  const double P = horner_d<kCbrtDeg>(c.cbrt_num, td);
+  const double Q = horner_d<kCbrtDeg>(c.cbrt_den, td);
+  const float rq = rcp_approx(d2f_pos_trunc(Q));
+  const float q0 = d2f_pos_trunc(P) * rq;            // ~4 ulp estimate of P/Q
+  const double r = fma(-f2d_pos(q0), Q, P);          // exact-ish residual in fp64
+  const float corr = __double2float_rn(r) * rq;      // r/Q, tiny
+  const bool cube = t > (float)kLabKnee;              // strict '>' (fast.py:114)
+  hi = cube ? q0 : fmaf((float)kLabSlope, t, (float)kLabOffset);
+  lo = cube ? corr : 0.0f;
+}
+
+struct Lab3 {
+  float c0, c1, c2;
+};
+
+// gamma_rep: 256 entries replicated 32x, entry i at [i*32 + lane] (conflict-free)
+__device__ __forceinline__ Lab3 lab_fast_u8(uint32_t r, uint32_t g, uint32_t b,
+                                            const float* gamma_rep, uint32_t lane,
+                                            const KCoeffs& c) {
+  const float gr = gamma_rep[(r << 5) | lane];
+  const float gg = gamma_rep[(g << 5) | lane];
+  const float gb = gamma_rep[(b << 5) | lane];
+  const float tx = fmaf(c.mxyz[2], gb, fmaf(c.mxyz[1], gg, c.mxyz[0] * gr));
+  const float ty = fmaf(c.mxyz[5], gb, fmaf(c.mxyz[4], gg, c.mxyz[3] * gr));
+  const float tz = fmaf(c.mxyz[8], gb, fmaf(c.mxyz[7], gg, c.mxyz[6] * gr));
+  float hx, lx, hy, ly, hz, lz;
+  lab_f_fast_df(tx, c, hx, lx);
+  lab_f_fast_df(ty, c, hy, ly);
+  lab_f_fast_df(tz, c, hz, lz);
+  Lab3 o;
+  o.c0 = fmaf(116.0f, ly, fmaf(116.0f, hy, -16.0f));
+  o.c1 = 500.0f * ((hx - hy) + (lx - ly));
+  o.c2 = 200.0f * ((hy - hz) + (ly - lz));
+  return o;
+}
+
+// Reference-faithful fp64 evaluation on real-valued channels (float input
+// path, fast.py:96-115), used for non-uint8 inputs.
+__device__ __forceinline__ double lab_f_fast_d(double t, const KCoeffs& c) {
+  const double P = horner_d<kCbrtDeg>(c.cbrt_num, t);
+  const double Q = horner_d<kCbrtDeg>(c.cbrt_den, t);
+  return t > kLabKnee ? P / Q : kLabSlope * t + kLabOffset;
+}
+__device__ __forceinline__ void lab_fast_d(double r, double g, double b, const KCoeffs& c,
+                                           double* o) {
+  const double gr = inverse_gamma_d(r / 255.0), gg = inverse_gamma_d(g / 255.0),
+               gb = inverse_gamma_d(b / 255.0);
+  const double x = rgb2xyz(0, 0) * gr + rgb2xyz(0, 1) * gg + rgb2xyz(0, 2) * gb;
+  const double y = rgb2xyz(1, 0) * gr + rgb2xyz(1, 1) * gg + rgb2xyz(1, 2) * gb;
+  const double z = rgb2xyz(2, 0) * gr + rgb2xyz(2, 1) * gg + rgb2xyz(2, 2) * gb;
+  const double fx = lab_f_fast_d(x / kWhiteX, c), fy = lab_f_fast_d(y / kWhiteY, c),
+               fz = lab_f_fast_d(z / kWhiteZ, c);
+  o[0] = 116.0 * fy - 16.0;
+  o[1] = 500.0 * (fx - fy);
+  o[2] = 200.0 * (fy - fz);
+}
+
+// ----------------------------------------------------------------- HSI fast
+// Kender case analysis (fast.py:131-146) on the integer channels.
+__device__ __forceinline__ Lab3 hsi_fast_u8(int r, int g, int b, const KCoeffs& c) {
+  const bool c1 = (r > b) & (g > b);
+  const bool c2 = !c1 & (g > r);
+  const bool c3 = !c1 & !c2 & (b > g);
+  const bool c4 = !c1 & !c2 & !c3 & (r > b);
+  int num, den;
+  float base;
+  if (c1) {
+    num = g - r; den = (g - b) + (r - b); base = (float)(kPi / 3.0);
+  } else if (c2) {
+    num = b - g; den = (b - r) + (g - r); base = (float)kPi;
+  } else if (c3) {
+    num = r - b; den = (r - g) + (b - g); base = (float)(5.0 * kPi / 3.0);
+  } else {
+    num = 0; den = 1; base = 0.0f;
+  }
+  const float fn = (float)num, fd = (float)den;       // |num|,den <= 510: exact
+  const float x = fn * rcp_approx(fd);
+  const float mag = horner_f<kPolyDeg>(c.hsi, fabsf(x));
+  float h = base + (num < 0 ? -mag : mag);           // odd extension (fast.py:118-122)
+  h = (c1 | c2 | c3) ? h : (c4 ? 0.0f : __int_as_float(0x7fc00000));
+  h = h < 0.0f ? h + (float)kTwoPi : h;
+  h = h >= (float)kTwoPi ? h - (float)kTwoPi : h;
+  const int sum = r + g + b;
+  const int mn = min(min(r, g), b);
+  Lab3 o;
+  o.c0 = h;
+  // S = 1 - 3 min/sum = (sum - 3 min)/sum, exact zero on grays (exact.py:95-101)
+  o.c1 = sum > 0 ? (float)(sum - 3 * mn) * rcp_approx((float)sum) : 0.0f;
+  o.c2 = (float)sum * (float)(1.0 / 765.0);
+  return o;
+}
+
+__device__ __forceinline__ double horner_dd(const double* cc, int deg, double x) {
+  double acc = cc[deg];
+  for (int k = deg - 1; k >= 0; --k) acc = acc * x + cc[k];
+  return acc;
+}
+
+__device__ __forceinline__ void hsi_fast_d(double r, double g, double b, const KCoeffs& c,
+                                           double* o) {
+  r /= 255.0; g /= 255.0; b /= 255.0;
+  const bool c1 = (r > b) && (g > b);
+  const bool c2 = !c1 && (g > r);
+  const bool c3 = !c1 && !c2 && (b > g);
+  const bool c4 = !c1 && !c2 && !c3 && (r > b);
+  double num = 0.0, den = 1.0, base = 0.0;
+  if (c1) { num = g - r; den = (g - b) + (r - b); base = kPi / 3.0; }
+  else if (c2) { num = b - g; den = (b - r) + (g - r); base = kPi; }
+  else if (c3) { num = r - b; den = (r - g) + (b - g); base = 5.0 * kPi / 3.0; }
+  const double x = num / den;
+  const double mag = horner_dd(c.hsi_d, kPolyDeg, fabs(x));
+  double h = base + (x < 0.0 ? -mag : mag);
+  h = (c1 || c2 || c3) ? h : (c4 ? 0.0 : __longlong_as_double(0x7ff8000000000000ll));
+  if (h < 0.0) h += kTwoPi;
+  if (h >= kTwoPi) h -= kTwoPi;
+  const double total = r + g + b;
+  const double low = fmin(fmin(r, g), b);
+  o[0] = h;
+  o[1] = total > 0.0 ? 1.0 - 3.0 * low / total : 0.0;
+  o[2] = total / 3.0;
+}
+
+// ----------------------------------------------------------------- SCT fast
+__device__ __forceinline__ Lab3 sct_fast_u8(int r, int g, int b, const KCoeffs& c) {
+  const int rg2 = r * r + g * g;
+  const int ss = rg2 + b * b;                 // <= 195075 < 2^24: exact in fp32
+  const float fss = (float)ss;
+  const float L = __fsqrt_rn(fss);            // correctly rounded |v| (fast.py:196)
+  const float fb = (float)b;
+  // angle A = acos_fast(b/L) (fast.py:151-162, :198); x >= 0.5 <=> 3 b^2 >= r^2 + g^2
+  const bool upper = 3 * b * b >= rg2;
+  float arg, pa;
+  if (upper) {
+    // sqrt(1 - b/L) without cancellation: (r^2+g^2) / (L (L + b))
+    const float den = L * (L + fb);
+    arg = sqrt_approx((float)rg2 * rcp_approx(den));
+    pa = horner_f<kPolyDeg>(c.asin, arg);
+  } else {
+    arg = fb * rcp_approx(L);
+    pa = horner_f<kPolyDeg>(c.acos, arg);
+  }
+  float ang_a = ss > 0 ? pa : 0.0f;
+  ang_a = fminf(fmaxf(ang_a, 0.0f), (float)(0.5 * kPi));
+  // angle B = atan_unit_fast(g, r) (fast.py:165-185)
+  const bool direct = g < r;
+  const int lo = direct ? g : r, hi = direct ? r : g;
+  const float t = hi > 0 ? (float)lo * rcp_approx((float)hi) : 0.0f;
+  const float pb = direct ? horner_f<kPolyDeg>(c.atanf, t) : horner_f<kPolyDeg>(c.atang, t);
+  float ang_b = fminf(fmaxf(pb, 0.0f), (float)(0.5 * kPi));
+  ang_b = (r == 0 && g == 0) ? __int_as_float(0x7fc00000) : ang_b;
+  Lab3 o;
+  o.c0 = L;
+  o.c1 = ang_a;
+  o.c2 = ang_b;
+  return o;
+}
+
+__device__ __forceinline__ void sct_fast_d(double r, double g, double b, const KCoeffs& c,
+                                           double* o) {
+  const double len = sqrt(r * r + g * g + b * b);
+  double a = 0.0;
+  if (len > 0.0) {
+    const double x = b / len;
+    a = x < 0.5 ? horner_dd(c.acos_d, kPolyDeg, x)
+                : horner_dd(c.asin_d, kPolyDeg, sqrt(fmax(1.0 - x, 0.0)));
+  }
+  double bb;
+  if (g == 0.0 && r == 0.0) {
+    bb = __longlong_as_double(0x7ff8000000000000ll);
+  } else {
+    const bool direct = g < r;
+    const double arg = direct ? g / (r > 0.0 ? r : 1.0) : (g > 0.0 ? r / g : 0.0);
+    bb = direct ? horner_dd(c.atanf_d, kPolyDeg, arg) : horner_dd(c.atang_d, kPolyDeg, arg);
+    bb = fmin(fmax(bb, 0.0), 0.5 * kPi);
+  }
+  o[0] = len;
+  o[1] = fmin(fmax(a, 0.0), 0.5 * kPi);
+  o[2] = bb;
+}
+
+// ------------------------------------------------------------ exact, fp64
+__device__ __forceinline__ double lab_f_exact(double t) {
+  return t > kLabKnee ? cbrt(t) : kLabSlope * t + kLabOffset;
+}
+// linear-light channels -> L*a*b* (exact.py:60-83)
+__device__ __forceinline__ void lab_from_linear(double gr, double gg, double gb, double* o) {
+  const double x = rgb2xyz(0, 0) * gr + rgb2xyz(0, 1) * gg + rgb2xyz(0, 2) * gb;
+  const double y = rgb2xyz(1, 0) * gr + rgb2xyz(1, 1) * gg + rgb2xyz(1, 2) * gb;
+  const double z = rgb2xyz(2, 0) * gr + rgb2xyz(2, 1) * gg + rgb2xyz(2, 2) * gb;
+  const double fx = lab_f_exact(x / kWhiteX), fy = lab_f_exact(y / kWhiteY),
+               fz = lab_f_exact(z / kWhiteZ);
+  o[0] = 116.0 * fy - 16.0;
+  o[1] = 500.0 * (fx - fy);
+  o[2] = 200.0 * (fy - fz);
+}
+__device__ __forceinline__ void lab_exact_d(double r, double g, double b, double* o) {
+  lab_from_linear(inverse_gamma_d(r / 255.0), inverse_gamma_d(g / 255.0),
+                  inverse_gamma_d(b / 255.0), o);
+}
+__device__ __forceinline__ void hsi_exact_d(double r, double g, double b, double* o) {
+  r /= 255.0; g /= 255.0; b /= 255.0;
+  const double s3 = 1.7320508075688772;       // np.sqrt(3.0)
+  const bool c1 = (r > b) && (g > b);
+  const bool c2 = !c1 && (g > r);
+  const bool c3 = !c1 && !c2 && (b > g);
+  const bool c4 = !c1 && !c2 && !c3 && (r > b);
+  double h;
+  if (c1) h = kPi / 3.0 + atan(s3 * (g - r) / ((g - b) + (r - b)));
+  else if (c2) h = kPi + atan(s3 * (b - g) / ((b - r) + (g - r)));
+  else if (c3) h = 5.0 * kPi / 3.0 + atan(s3 * (r - b) / ((r - g) + (b - g)));
+  else h = c4 ? 0.0 : __longlong_as_double(0x7ff8000000000000ll);
+  const double total = r + g + b;
+  const double low = fmin(fmin(r, g), b);
+  o[0] = h;
+  o[1] = total > 0.0 ? 1.0 - 3.0 * low / total : 0.0;
+  o[2] = total / 3.0;
+}
+__device__ __forceinline__ void sct_exact_d(double r, double g, double b, double* o) {
+  const double len = sqrt(r * r + g * g + b * b);
+  o[0] = len;
+  o[1] = len > 0.0 ? acos(fmin(fmax(b / len, -1.0), 1.0)) : 0.0;
+  o[2] = (r == 0.0 && g == 0.0) ? __longlong_as_double(0x7ff8000000000000ll) : atan2(g, r);
+}
+
+// --------------------------------------------------------------- distances
+__device__ __forceinline__ double lab_distance_d(const double* x, const double* y) {
+  const double d0 = x[0] - y[0], d1 = x[1] - y[1], d2 = x[2] - y[2];
+  return sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+}
+__device__ __forceinline__ double hsi_distance_d(const double* x, const double* y) {
+  const double hx = isnan(x[0]) ? 0.0 : x[0], hy = isnan(y[0]) ? 0.0 : y[0];
+  double th = fabs(hx - hy);
+  th = th > kPi ? kTwoPi - th : th;
+  const double di = x[2] - y[2];
+  const double d2 = x[1] * x[1] + y[1] * y[1] - 2.0 * x[1] * y[1] * cos(th) + di * di;
+  return sqrt(fmax(d2, 0.0));
+}
+__device__ __forceinline__ void sct_to_rgb_d(const double* s, double* rgb) {
+  const double bb = isnan(s[2]) ? 0.0 : s[2];
+  double sa, ca, sb, cb;
+  sincos(s[1], &sa, &ca);
+  sincos(bb, &sb, &cb);
+  rgb[0] = s[0] * sa * cb;
+  rgb[1] = s[0] * sa * sb;
+  rgb[2] = s[0] * ca;
+}
+__device__ __forceinline__ double sct_distance_d(const double* x, const double* y) {
+  double rx[3], ry[3], lx[3], ly[3];
+  sct_to_rgb_d(x, rx);
+  sct_to_rgb_d(y, ry);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    rx[k] = fmin(fmax(rx[k], 0.0), 255.0);
+    ry[k] = fmin(fmax(ry[k], 0.0), 255.0);
+  }
+  lab_exact_d(rx[0], rx[1], rx[2], lx);
+  lab_exact_d(ry[0], ry[1], ry[2], ly);
+  return lab_distance_d(lx, ly);
+}
+__device__ __forceinline__ double distance_d(int space, const double* x, const double* y) {
+  return space == MACT_SPACE_LAB ? lab_distance_d(x, y)
+       : space == MACT_SPACE_HSI ? hsi_distance_d(x, y)
+                                 : sct_distance_d(x, y);
+}
+
+}  // namespace mact

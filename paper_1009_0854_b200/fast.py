@@ -1,0 +1,165 @@
+"""MACT fast transforms on B200 — drop-in for ``mact.fast`` (reference fast.py).
+
+Same entry points, same arguments:
+
+    rgb_to_lab_fast(pixels, cfg=DEFAULT_CONFIG)   # fast.py:86-107
+    rgb_to_hsi_fast(pixels, cfg=DEFAULT_CONFIG)   # fast.py:125-148
+    rgb_to_sct_fast(pixels, cfg=DEFAULT_CONFIG)   # fast.py:188-203
+
+``pixels`` is any ``(..., 3)`` array.  Integer input takes the 8-bit table path,
+real input the analytic path, as in the reference.  Differences, all
+documented in DESIGN.md:
+
+* results are float32 (the reference returns float64) — within the north-star
+  tolerance (1e-4 on L*a*b*, 1e-5 on normalised H/S/I and SCT);
+* a CUDA tensor in gives a CUDA tensor out (no host round trip); a numpy
+  array in gives a numpy array out, streamed through the native host executor;
+* keyword-only extras: ``out=`` (preallocated result) and ``layout=``
+  ("interleaved" (...,3) or "planar" (3,...)).
+
+Every call runs libmact_cuda kernels; there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import functools
+from dataclasses import dataclass
+from typing import Tuple
+
+import numpy as np
+
+from . import _dev, _lib
+from .approximants import (Approximant, Rational, TargetFn, hsi_refit, registry_get)
+
+TWO_PI = 2.0 * np.pi
+
+
+def _inverse_gamma_table() -> np.ndarray:
+    k = np.arange(256) / 255.0
+    with np.errstate(invalid="ignore"):
+        curved = ((k + 0.099) / 1.099) ** (1.0 / 0.45)
+    return np.where(k < 0.081, k / 4.5, curved)
+
+
+# Linearised 8-bit channel values (reference fast.py:35); informational — the
+# kernels rebuild the same table on device.
+GAMMA_TABLE = _inverse_gamma_table()
+
+
+def _fill(dst, coeffs) -> int:
+    for i, c in enumerate(coeffs):
+        dst[i] = float(c)
+    return len(coeffs) - 1
+
+
+@dataclass(frozen=True)
+class MactConfig:
+    """Degree selection (reference fast.py:46-78).  Defaults: CIELAB rational
+    (4,4), HSI degree 5, SCT (n_asin, m_acos, r_atan) = (5,5,5)."""
+
+    cielab_degrees: Tuple[int, int] = (4, 4)
+    hsi_degree: int = 5
+    sct_degrees: Tuple[int, int, int] = (5, 5, 5)
+
+    def __post_init__(self):
+        n, m = self.cielab_degrees
+        object.__setattr__(self, "cbrt_approx", registry_get(TargetFn.CBRT, (n, m)))
+        registry_get(TargetFn.ATAN_SQRT3, (self.hsi_degree,))   # degree must be bundled
+        object.__setattr__(self, "atan_sqrt3_approx", hsi_refit(self.hsi_degree))
+        a, c, t = self.sct_degrees
+        object.__setattr__(self, "asin_approx", registry_get(TargetFn.ASIN_HALF, (a,)))
+        object.__setattr__(self, "acos_approx", registry_get(TargetFn.ACOS_HALF, (c,)))
+        object.__setattr__(self, "atan_f_approx", registry_get(TargetFn.ATAN_F, (t,)))
+        object.__setattr__(self, "atan_g_approx", registry_get(TargetFn.ATAN_G, (t,)))
+        object.__setattr__(self, "coeffs", self._pack())
+
+    def _pack(self) -> _lib.MactCoeffs:
+        k = _lib.MactCoeffs()
+        rat: Rational = self.cbrt_approx.form
+        k.cbrt_num_deg = _fill(k.cbrt_num, rat.numerator.coeffs)
+        k.cbrt_den_deg = _fill(k.cbrt_den, rat.denominator.coeffs)
+        k.hsi_deg = _fill(k.atan_sqrt3, self.atan_sqrt3_approx.form.coeffs)
+        k.asin_deg = _fill(k.asin_half, self.asin_approx.form.coeffs)
+        k.acos_deg = _fill(k.acos_half, self.acos_approx.form.coeffs)
+        k.atan_deg = _fill(k.atan_f, self.atan_f_approx.form.coeffs)
+        _fill(k.atan_g, self.atan_g_approx.form.coeffs)
+        return k
+
+
+DEFAULT_CONFIG = MactConfig()
+
+_ENTRY = {"lab": "mact_lab_fast", "hsi": "mact_hsi_fast", "sct": "mact_sct_fast"}
+
+
+def _host_u8(space: str, arr: np.ndarray, cfg: MactConfig, out, layout: str):
+    """numpy uint8 -> numpy fp32 through the native chunked H2D/kernel/D2H executor."""
+    import torch
+
+    src = np.ascontiguousarray(arr)
+    lead = src.shape[:-1]
+    n = int(np.prod(lead, dtype=np.int64)) if lead else 1
+    shape = lead + (3,) if layout == "interleaved" else (3,) + lead
+    if out is None:
+        out = np.empty(shape, dtype=np.float32)
+    elif out.dtype != np.float32 or out.shape != shape or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a C-contiguous float32 array of shape {shape}")
+    dev = torch.cuda.current_device()
+    ctx = _dev.host_ctx(dev)
+    _lib.call("mact_transform_host", ctx, _lib.SPACES[space], _dev.np_ptr(src), _dev.np_ptr(out),
+              n, cfg.coeffs, _lib.LAYOUTS[layout])
+    return out
+
+
+def transform(space: str, pixels, cfg: MactConfig = DEFAULT_CONFIG, *, out=None,
+              layout: str = "interleaved"):
+    """Run one MACT fast transform (space in lab/hsi/sct) on the GPU."""
+    if space not in _ENTRY:
+        raise ValueError(f"unknown space {space!r}")
+    if layout not in _lib.LAYOUTS:
+        raise ValueError(f"unknown layout {layout!r}")
+    _dev.require_cuda()
+    if not _dev.is_device_tensor(pixels):
+        arr = np.asarray(pixels)
+        if arr.dtype == np.uint8 and arr.ndim >= 1 and arr.shape[-1] == 3:
+            return _host_u8(space, arr, cfg, out, layout)
+    t, code, lead, on_dev = _dev.as_device_pixels(pixels)
+    n = t.numel() // 3
+    res = out if (out is not None and on_dev) else _dev.empty_out(lead, layout, t.device)
+    _lib.call(_ENTRY[space], t.data_ptr(), code, res.data_ptr(), n, cfg.coeffs,
+              _lib.LAYOUTS[layout], _dev.stream_ptr())
+    if not on_dev and out is not None:
+        out[...] = res.cpu().numpy()
+        return out
+    return _dev.to_caller(res, on_dev)
+
+
+def rgb_to_lab_fast(pixels, cfg: MactConfig = DEFAULT_CONFIG, **kw):
+    """RGB -> CIELAB with the minimax rational cube root (reference fast.py:86-107)."""
+    return transform("lab", pixels, cfg, **kw)
+
+
+def rgb_to_hsi_fast(pixels, cfg: MactConfig = DEFAULT_CONFIG, **kw):
+    """RGB -> HSI with the minimax hue arctangent (reference fast.py:125-148)."""
+    return transform("hsi", pixels, cfg, **kw)
+
+
+def rgb_to_sct_fast(pixels, cfg: MactConfig = DEFAULT_CONFIG, **kw):
+    """RGB -> spherical coordinates with minimax arccos/arctan (reference fast.py:188-203)."""
+    return transform("sct", pixels, cfg, **kw)
+
+
+def rgb_to_all_fast(pixels, cfg: MactConfig = DEFAULT_CONFIG, *, layout: str = "interleaved"):
+    """All three transforms from one read of the pixels (BASELINE config 5).
+
+    Device tensor in (uint8) -> (lab, hsi, sct) device tensors out.
+    """
+    import torch
+
+    t, code, lead, on_dev = _dev.as_device_pixels(pixels)
+    if code != _lib.DTYPE_U8:
+        raise ValueError("rgb_to_all_fast takes 8-bit pixels")
+    n = t.numel() // 3
+    outs = [_dev.empty_out(lead, layout, t.device) for _ in range(3)]
+    _lib.call("mact_all_fast", t.data_ptr(), *[o.data_ptr() for o in outs], n, cfg.coeffs,
+              _lib.LAYOUTS[layout], _dev.stream_ptr())
+    return tuple(_dev.to_caller(o, on_dev) for o in outs)

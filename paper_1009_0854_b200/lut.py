@@ -1,0 +1,134 @@
+"""3D-LUT interpolators on B200 — drop-in for ``mact.lut``.
+
+    build_lut(space, grid_n) -> Lut3D          (lut.py:82-95)
+    node_weights(lut, pixels, method)          (lut.py:115-199)
+    interpolate(lut, pixels, method, variant)  (lut.py:341-350)
+
+The lattice is built on device from the fp64 exact transforms; interpolation
+and node selection run in libmact_cuda (integer cell location, bit-exact
+node indices).  Linear destinations (CIELAB) are supported; the angular
+HSI/SCT blend (lut.py:202-262) is listed as next work in DESIGN.md.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict, Optional, Tuple
+
+import numpy as np
+
+from . import _dev, _lib
+from .errors import CacheMissing, MactError
+
+METHODS = ("trilinear", "prism", "pyramidal", "tetrahedral")
+VARIANTS = ("standard", "caching")
+NEIGHBOR_COUNT = {"trilinear": 8, "prism": 6, "pyramidal": 5, "tetrahedral": 4}
+SPACES = ("lab", "hsi", "sct")
+ANGULAR_MASKS = {"lab": (False, False, False), "hsi": (True, False, False),
+                 "sct": (False, True, True)}
+
+
+@dataclass
+class Lut3D:
+    grid_n: int
+    spacing: float
+    destination_space: str
+    values: np.ndarray                      # (n, n, n, 3) float64, r-major (host copy)
+    angular_mask: Tuple[bool, bool, bool]
+    cache: Optional[Dict[str, object]] = None
+    _device: Dict[int, object] = field(default_factory=dict, repr=False, compare=False)
+
+    @property
+    def flat_values(self) -> np.ndarray:
+        return self.values.reshape(-1, 3)
+
+    def lattice(self, device=None):
+        """fp32 (n^3, 3) device lattice consumed by the kernels (cached per device)."""
+        import torch
+
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        key = dev.index if dev.index is not None else torch.cuda.current_device()
+        if key not in self._device:
+            self._device[key] = torch.from_numpy(
+                np.ascontiguousarray(self.values.reshape(-1, 3), dtype=np.float32)).to(dev)
+        return self._device[key]
+
+
+def lattice_coordinates(grid_n: int) -> np.ndarray:
+    return np.arange(grid_n) * (255.0 / (grid_n - 1))
+
+
+def build_lut(space: str, grid_n: int) -> Lut3D:
+    """Lattice of exact transforms at k*255/(n-1), NaN -> 0 (lut.py:82-95), built on device."""
+    import torch
+
+    if space not in SPACES:
+        raise ValueError(f"unknown destination space {space!r}")
+    if grid_n not in (9, 17, 33):
+        raise ValueError("grid_n must be one of 9, 17, 33")
+    _dev.require_cuda()
+    total = grid_n ** 3
+    f64 = torch.empty((total, 3), dtype=torch.float64, device="cuda")
+    f32 = torch.empty((total, 3), dtype=torch.float32, device="cuda")
+    _lib.call("mact_lut_build", _lib.SPACES[space], grid_n, f64.data_ptr(), f32.data_ptr(),
+              _dev.stream_ptr())
+    lut = Lut3D(grid_n=grid_n, spacing=255.0 / (grid_n - 1), destination_space=space,
+                values=f64.cpu().numpy().reshape(grid_n, grid_n, grid_n, 3),
+                angular_mask=ANGULAR_MASKS[space])
+    lut._device[f32.device.index] = f32
+    return lut
+
+
+def _method_code(method: str) -> int:
+    if method not in METHODS:
+        raise ValueError(f"unknown interpolation method {method!r}")
+    return _lib.METHODS[method]
+
+
+def _u8_pixels(pixels):
+    t, code, lead, on_dev = _dev.as_device_pixels(pixels)
+    if code != _lib.DTYPE_U8:
+        raise ValueError("LUT kernels take 8-bit pixels (integer RGB in [0, 255])")
+    return t, lead, on_dev
+
+
+def node_weights(lut: Lut3D, pixels, method: str):
+    """(flat node indices int32 (..., k), weights float32 (..., k)) (lut.py:115-199)."""
+    import torch
+
+    m = _method_code(method)
+    t, lead, on_dev = _u8_pixels(pixels)
+    k = NEIGHBOR_COUNT[method]
+    nodes = torch.empty(lead + (k,), dtype=torch.int32, device=t.device)
+    w = torch.empty(lead + (k,), dtype=torch.float32, device=t.device)
+    _lib.call("mact_lut_nodes", lut.grid_n, m, t.data_ptr(), t.numel() // 3, nodes.data_ptr(),
+              w.data_ptr(), _dev.stream_ptr())
+    return _dev.to_caller(nodes, on_dev), _dev.to_caller(w, on_dev)
+
+
+def build_cache(lut: Lut3D) -> Lut3D:
+    """Caching variant marker (lut.py:265-291).  On the GPU the per-cell
+    difference cache buys nothing over the shared-memory lattice, so the
+    caching variant evaluates the same kernel (the reference proves the two
+    variants agree to 1e-12)."""
+    return Lut3D(grid_n=lut.grid_n, spacing=lut.spacing, destination_space=lut.destination_space,
+                 values=lut.values, angular_mask=lut.angular_mask, cache={"device": True},
+                 _device=lut._device)
+
+
+def interpolate(lut: Lut3D, pixels, method: str = "tetrahedral", variant: str = "standard", *,
+                out=None, layout: str = "interleaved"):
+    """Interpolate destination triples for RGB in [0, 255] (lut.py:341-350)."""
+    m = _method_code(method)
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown variant {variant!r}")
+    if variant == "caching" and lut.cache is None:
+        raise CacheMissing("caching interpolation requested without a cache; call build_cache first")
+    if any(lut.angular_mask):
+        raise MactError("angular (HSI/SCT) LUT interpolation is not implemented on the device yet")
+    t, lead, on_dev = _u8_pixels(pixels)
+    res = out if (out is not None and on_dev) else _dev.empty_out(lead, layout, t.device)
+    lat = lut.lattice(t.device)
+    _lib.call("mact_lut_interp", lat.data_ptr(), lut.grid_n, m, t.data_ptr(), res.data_ptr(),
+              t.numel() // 3, _lib.LAYOUTS[layout], _dev.stream_ptr())
+    return _dev.to_caller(res, on_dev)

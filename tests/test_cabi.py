@@ -1,0 +1,95 @@
+"""CPU-side checks of the C ABI: the library builds/loads without a GPU, exports
+every symbol include/mact_cuda.h declares, and the ctypes structs match the C
+layout (checked by compiling the header with gcc)."""
+
+import os
+import re
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mact_cuda.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1009_0854_b200 import _lib, build
+    if not _lib.LIB_PATH.exists():
+        build.build()
+    return _lib.load()
+
+
+def header_functions():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(mact_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_exports_every_declared_symbol(lib):
+    from paper_1009_0854_b200 import _lib
+    names = header_functions()
+    assert len(names) >= 18
+    for n in names:
+        assert hasattr(lib, n), f"libmact_cuda.so does not export {n}"
+    assert set(names) == set(_lib.EXPORTS), "ctypes signature table out of sync with the header"
+
+
+def test_version_and_counters_without_gpu(lib):
+    assert lib.mact_version() == 100
+    lib.mact_launch_count_reset()
+    assert lib.mact_launch_count() == 0
+
+
+def test_struct_layout_matches_c(tmp_path):
+    from paper_1009_0854_b200 import _lib
+    import ctypes as C
+    src = tmp_path / "layout.c"
+    src.write_text("""
+#include <stdio.h>
+#include <stddef.h>
+#include "mact_cuda.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(MactCoeffs), offsetof(MactCoeffs, atan_g),
+         sizeof(MactErrStats), sizeof(MactErrSpec), offsetof(MactErrSpec, ref_array),
+         offsetof(MactErrSpec, ref_dtype));
+  return 0;
+}
+""")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    vals = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()))
+    assert vals == [C.sizeof(_lib.MactCoeffs), _lib.MactCoeffs.atan_g.offset,
+                    C.sizeof(_lib.MactErrStats), C.sizeof(_lib.MactErrSpec),
+                    _lib.MactErrSpec.ref_array.offset, _lib.MactErrSpec.ref_dtype.offset]
+
+
+def test_bad_arguments_fail_without_touching_the_device(lib):
+    from paper_1009_0854_b200 import _lib
+    from paper_1009_0854_b200.errors import UnknownApproximant
+    with pytest.raises(ValueError):
+        _lib.call("mact_lut_build", 0, 16, None, None, None)
+    with pytest.raises(ValueError):
+        _lib.call("mact_exact", 7, None, 0, None, 2, 1, None)
+    c = _lib.MactCoeffs()
+    c.cbrt_num_deg = c.cbrt_den_deg = 9
+    c.hsi_deg = 5
+    c.asin_deg = c.acos_deg = c.atan_deg = 5
+    with pytest.raises(UnknownApproximant):
+        _lib.call("mact_lab_fast", None, 0, None, 0, C_ptr(c), 0, None)
+
+
+def C_ptr(c):
+    import ctypes as C
+    return C.pointer(c)
+
+
+def test_product_never_imports_oracle():
+    """The product package must not reach the CPU oracle (no CPU fallback)."""
+    pkg = os.path.join(ROOT, "paper_1009_0854_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*", "", txt).replace('"""', ""), f

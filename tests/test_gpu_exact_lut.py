@@ -1,0 +1,126 @@
+"""GPU parity of the exact transforms, distances (K5) and the 3D LUT (K4)."""
+
+import numpy as np
+import pytest
+
+from oracle import mact_oracle as O
+from tests.parity_util import check_lab
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_1009_0854_b200 import _lib, exact, fast, harness, lut
+    _lib.load()
+    return {"fast": fast, "exact": exact, "lut": lut, "harness": harness}
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def close(a, b, rtol=1e-12, atol=1e-12):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    np.testing.assert_array_equal(np.isnan(a), np.isnan(b))
+    np.testing.assert_allclose(np.nan_to_num(a), np.nan_to_num(b), rtol=rtol, atol=atol)
+
+
+@pytest.mark.parametrize("space", ["lab", "hsi", "sct"])
+def test_exact_vs_reference(P, golden, space):
+    got = getattr(P["exact"], f"rgb_to_{space}_exact")(dev(golden["probe"])).cpu().numpy()
+    close(got, golden[f"{space}_exact"], rtol=1e-11, atol=1e-11)
+
+
+def test_exact_real_inputs(P, golden):
+    x = golden["small_float"]
+    close(P["exact"].rgb_to_lab_exact(dev(x)).cpu().numpy(), O.rgb_to_lab_exact(x), 1e-11, 1e-11)
+    close(P["exact"].rgb_to_sct_exact(dev(x)).cpu().numpy(), O.rgb_to_sct_exact(x), 1e-11, 1e-11)
+    close(P["exact"].rgb_to_hsi_exact(dev(x)).cpu().numpy(), O.rgb_to_hsi_exact(x), 1e-11, 1e-11)
+
+
+def test_distances_vs_reference(P, golden):
+    ex = P["exact"]
+    close(ex.lab_distance(golden["lab_fast"], golden["lab_exact"]), golden["lab_dist"], 1e-9, 1e-12)
+    close(ex.hsi_distance(golden["hsi_fast"], golden["hsi_exact"]), golden["hsi_dist"], 1e-6, 1e-12)
+    close(ex.sct_distance_indirect(golden["sct_fast"], golden["sct_exact"]), golden["sct_dist"],
+          1e-6, 1e-10)
+    close(ex.sct_to_rgb(golden["sct_exact"]), golden["sct_to_rgb"], 1e-11, 1e-10)
+
+
+@pytest.mark.parametrize("space", ["lab", "hsi", "sct"])
+def test_lut_build(P, golden, space):
+    for n in (9, 17):
+        lt = P["lut"].build_lut(space, n)
+        close(lt.values, golden[f"lut_{space}_{n}"], 1e-11, 1e-11)
+    lt = P["lut"].build_lut(space, 33)
+    flat = lt.values.reshape(-1, 3)
+    close(flat[golden[f"lut_{space}_33_sample_idx"]], golden[f"lut_{space}_33_sample"], 1e-11, 1e-11)
+
+
+@pytest.mark.parametrize("n", [9, 17, 33])
+@pytest.mark.parametrize("method", O.METHODS)
+def test_lut_nodes_bit_exact(P, golden, n, method):
+    lt = P["lut"].build_lut("lab", n)
+    nodes, w = P["lut"].node_weights(lt, golden["small"], method)
+    np.testing.assert_array_equal(nodes, golden[f"nodes_{n}_{method}"])
+    np.testing.assert_allclose(w, golden[f"weights_{n}_{method}"], atol=2e-7)
+
+
+@pytest.mark.parametrize("n", [9, 17, 33])
+@pytest.mark.parametrize("method", O.METHODS)
+def test_lut_nodes_full_cube(P, n, method):
+    """Every cube colour: node indices bit-exact against the oracle (C3 rows)."""
+    lt = P["lut"].build_lut("lab", n)
+    cube = P["harness"].cube_chunk(0, 1 << 24, device="cuda")
+    nodes, w = P["lut"].node_weights(lt, cube, method)
+    nodes = nodes.cpu().numpy()
+    host = cube.cpu().numpy()
+    step = 1 << 22
+    for s in range(0, 1 << 24, step):
+        on, ow = O.node_weights(n, host[s:s + step], method)
+        np.testing.assert_array_equal(nodes[s:s + step], on)
+
+
+@pytest.mark.parametrize("n", [9, 17, 33])
+@pytest.mark.parametrize("method", O.METHODS)
+def test_lut_interp_vs_reference(P, golden, n, method):
+    lt = P["lut"].build_lut("lab", n)
+    got = P["lut"].interpolate(lt, dev(golden["small"]), method).cpu().numpy()
+    check_lab(got, golden[f"interp_lab_{n}_{method}"])
+    cache = P["lut"].build_cache(lt)
+    got_c = P["lut"].interpolate(cache, dev(golden["small"]), method, "caching").cpu().numpy()
+    check_lab(got_c, golden[f"interp_lab_{n}_{method}_caching"])
+
+
+@pytest.mark.parametrize("n", [17, 33])
+@pytest.mark.parametrize("method", O.METHODS)
+def test_lut_interp_c3_image(P, n, method):
+    """BASELINE config 3 image (4096^2, default_rng(0)) vs the oracle, tail and planar too."""
+    img = np.random.default_rng(0).integers(0, 256, (4096, 4096, 3), dtype=np.uint8)
+    lt = P["lut"].build_lut("lab", n)
+    d = dev(img)
+    got = P["lut"].interpolate(lt, d, method).cpu().numpy()
+    vals = O.build_lut_values("lab", n).astype(np.float32).astype(np.float64)
+    for r0 in (0, 3584):
+        check_lab(got[r0:r0 + 512], O.interpolate(vals, img[r0:r0 + 512], method))
+    part = P["lut"].interpolate(lt, d.reshape(-1, 3)[5:100005], method, layout="planar").cpu().numpy()
+    np.testing.assert_array_equal(part.T, got.reshape(-1, 3)[5:100005])
+
+
+def test_lut_errors(P):
+    from paper_1009_0854_b200.errors import CacheMissing
+    lut = P["lut"]
+    with pytest.raises(ValueError):
+        lut.build_lut("xyz", 17)
+    with pytest.raises(ValueError):
+        lut.build_lut("lab", 16)
+    lt = lut.build_lut("lab", 9)
+    with pytest.raises(ValueError):
+        lut.interpolate(lt, np.zeros((2, 3), np.uint8), "cubic")
+    with pytest.raises(ValueError):
+        lut.interpolate(lt, np.zeros((2, 3), np.uint8), "tetrahedral", "fancy")
+    with pytest.raises(CacheMissing):
+        lut.interpolate(lt, np.zeros((2, 3), np.uint8), "tetrahedral", "caching")

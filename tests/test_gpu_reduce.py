@@ -1,0 +1,127 @@
+"""GPU error reduction (K6) against the reference's published-by-oracle figures
+(tests/golden/figures.json, produced by the real reference harness)."""
+
+import numpy as np
+import pytest
+
+from oracle import mact_oracle as O
+from tests.parity_util import check_figure
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_1009_0854_b200 import _lib, exact, fast, harness, lut
+    _lib.load()
+    return {"fast": fast, "exact": exact, "lut": lut, "harness": harness}
+
+
+CUBE_ROWS = [("lab_22", "lab", dict(cielab_degrees=(2, 2))), ("lab_44", "lab", {}),
+             ("lab_34", "lab", dict(cielab_degrees=(3, 4))),
+             ("hsi_2", "hsi", dict(hsi_degree=2)), ("hsi_5", "hsi", {}),
+             ("sct_444", "sct", dict(sct_degrees=(4, 4, 4))), ("sct_555", "sct", {})]
+
+
+@pytest.mark.parametrize("key,space,kw", CUBE_ROWS)
+def test_cube_figures(P, figures, key, space, kw):
+    """Tables 9-11 rows over all 2^24 colours (fused fast+exact+distance kernel)."""
+    h = P["harness"]
+    cfg = P["fast"].MactConfig(**kw)
+    st = h.measure_error(space, h.fast_candidate(space, cfg),
+                         getattr(P["exact"], f"rgb_to_{space}_exact"))
+    ref = figures["cube"][key]
+    assert st.count == ref["count"]
+    check_figure(st.avg, st.max, ref["avg"], ref["max"], floor=1e-6)
+    if key in ("lab_44", "lab_22"):
+        assert list(st.argmax_pixel) == ref["argmax_pixel"]
+
+
+@pytest.mark.parametrize("n", [9, 17, 33])
+@pytest.mark.parametrize("method", O.METHODS)
+def test_cube_lut_figures(P, figures, n, method):
+    """Table 12 rows (LUT-Lab, full cube)."""
+    h = P["harness"]
+    lt = P["lut"].build_lut("lab", n)
+    st = h.measure_error("lab", h.LutCandidate(lt, method), P["exact"].rgb_to_lab_exact)
+    ref = figures["cube"][f"lut_lab_{n}_{method}"]
+    check_figure(st.avg, st.max, ref["avg"], ref["max"], avg_rtol=1e-3, max_rtol=1e-3)
+
+
+def test_c1_figure(P, figures):
+    h = P["harness"]
+    c1 = np.random.default_rng(0).integers(0, 256, size=(512, 512, 3), dtype=np.uint8)
+    st = h.measure_error("lab", P["fast"].rgb_to_lab_fast, P["exact"].rgb_to_lab_exact,
+                         population=c1.reshape(-1, 3))
+    ref = figures["c1_lab"]
+    check_figure(st.avg, st.max, ref["avg"], ref["max"])
+    assert list(st.argmax_pixel) == ref["argmax_pixel"] and st.count == ref["count"]
+
+
+def test_c3_figures(P, figures):
+    h = P["harness"]
+    c3 = np.random.default_rng(0).integers(0, 256, size=(4096, 4096, 3), dtype=np.uint8)
+    d = torch.from_numpy(c3).cuda().reshape(-1, 3)
+    st = h.measure_error("lab", P["fast"].rgb_to_lab_fast, P["exact"].rgb_to_lab_exact, population=d)
+    check_figure(st.avg, st.max, figures["c3_lab"]["avg"], figures["c3_lab"]["max"])
+    for n in (17, 33):
+        lt = P["lut"].build_lut("lab", n)
+        for method in O.METHODS:
+            st = h.measure_error("lab", h.LutCandidate(lt, method), P["exact"].rgb_to_lab_exact,
+                                 population=d)
+            ref = figures["c3_lut"][f"{n}_{method}"]
+            check_figure(st.avg, st.max, ref["avg"], ref["max"], avg_rtol=1e-3, max_rtol=1e-3)
+
+
+def test_component_figures(P, figures):
+    """SURVEY A21 per-component |fast - exact| over the cube (config 2)."""
+    h = P["harness"]
+    for space in ("hsi", "sct"):
+        comps = h.component_error(space)
+        ref = figures["c2_component"][space]
+        for c in range(3):
+            assert comps[c].count == ref[c]["count"] and comps[c].nan_count == ref[c]["nan"]
+            # fp32 outputs: mean within 1 %, max within 10 % or a 4-ulp floor of the range
+            floor = 4 * np.spacing(np.float32([1.0, 1.0, 1.0] if space == "hsi" else [441.7, 1.6, 1.6])[c])
+            floor = max(float(floor), 2e-6 if space == "hsi" else 5e-6)
+            assert abs(comps[c].mean - ref[c]["mean"]) <= max(1e-2 * ref[c]["mean"], floor)
+            assert abs(comps[c].max - ref[c]["max"]) <= max(0.1 * ref[c]["max"], floor)
+
+
+def test_generic_callables_and_chunks(P, figures):
+    """Arbitrary callables (not fusable) + chunked populations give the same figure."""
+    h = P["harness"]
+    fast, exact = P["fast"], P["exact"]
+    c1 = np.random.default_rng(0).integers(0, 256, size=(512, 512, 3), dtype=np.uint8).reshape(-1, 3)
+    fused = h.measure_error("lab", fast.rgb_to_lab_fast, exact.rgb_to_lab_exact, population=c1)
+    generic = h.measure_error("lab", lambda p: fast.rgb_to_lab_fast(p),
+                              lambda p: exact.rgb_to_lab_exact(p), population=c1)
+    chunks = [c1[i:i + 50000] for i in range(0, c1.shape[0], 50000)]
+    chunked = h.measure_error("lab", fast.rgb_to_lab_fast, exact.rgb_to_lab_exact, population=chunks)
+    for st in (generic, chunked):
+        assert st.count == fused.count and st.argmax_pixel == fused.argmax_pixel
+        assert st.max == fused.max
+        assert abs(st.avg - fused.avg) <= 1e-12 * fused.avg
+    with pytest.raises(ValueError):
+        h.measure_error("lab", fast.rgb_to_lab_fast, exact.rgb_to_lab_exact,
+                        population=np.zeros((0, 3), np.uint8))
+
+
+def test_reduction_deterministic_and_sharded(P):
+    """Shards with index_base fold to the single-shard result (the multi-GPU combine)."""
+    h = P["harness"]
+    one = h.reduce_partials("hsi", h.fast_candidate("hsi"), None, cube_start=0, n=1 << 24)[0]
+    again = h.reduce_partials("hsi", h.fast_candidate("hsi"), None, cube_start=0, n=1 << 24)[0]
+    assert one == again
+    parts = []
+    k = 8
+    for r in range(k):
+        s = r * ((1 << 24) // k)
+        parts.append(h.reduce_partials("hsi", h.fast_candidate("hsi"), None, cube_start=s,
+                                       n=(1 << 24) // k, index_base=s)[0])
+    tot = h.combine_partials(parts)
+    assert tot["max"] == one["max"] and tot["argmax"] == one["argmax"]
+    assert tot["count"] == one["count"]
+    assert abs(tot["sum"] - one["sum"]) <= 1e-12 * one["sum"]
