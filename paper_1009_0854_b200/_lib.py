@@ -15,7 +15,8 @@ from pathlib import Path
 from .errors import MactError, UnknownApproximant
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libmact_cuda.so"
+# MACT_LIB selects an alternative build (tuning variants); default: the in-tree library
+LIB_PATH = Path(os.environ["MACT_LIB"]) if os.environ.get("MACT_LIB") else _PKG / "libmact_cuda.so"
 
 MACT_OK, MACT_EBADARG, MACT_EUNKNOWN_APPROX, MACT_ECUDA = 0, 1, 2, 3
 SPACES = {"lab": 0, "hsi": 1, "sct": 2}

@@ -21,8 +21,12 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-BUILD = ROOT / "build" / "mact"
-LIB = PKG / "libmact_cuda.so"
+# Tuning builds: MACT_NVCC_DEFS="-DMACT_LAB_TP=2048 ..." MACT_LIB_TAG=v2 writes
+# libmact_cuda_v2.so (objects under build/mact_v2) without touching the default.
+_TAG = os.environ.get("MACT_LIB_TAG", "")
+BUILD = ROOT / "build" / ("mact" + (f"_{_TAG}" if _TAG else ""))
+LIB = PKG / ("libmact_cuda" + (f"_{_TAG}" if _TAG else "") + ".so")
+EXTRA = os.environ.get("MACT_NVCC_DEFS", "").split()
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2",
               "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"] + ARCH
@@ -53,7 +57,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     def compile_one(job):
         src, obj = job
-        cmd = [cc, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
+        cmd = [cc, *NVCC_FLAGS, *EXTRA, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -43,6 +43,14 @@ struct KCoeffs {
   float hsi[kPolyDeg + 1], asin[kPolyDeg + 1], acos[kPolyDeg + 1], atanf[kPolyDeg + 1],
       atang[kPolyDeg + 1];
   float mxyz[9];   // RGB->XYZ rows pre-divided by the white point (fp32)
+  // Monic form of a degree-(4,4) rational, used by the batched CIELAB path:
+  // P = p4 (t^4 + pm3 t^3 + ... + pm0), Q = q4 (t^4 + qm3 t^3 + ...),
+  // f = k P'/Q' with k = p4/q4 folded into the output constants.  The first
+  // Horner step becomes t + c3 (no constant pair to stage in registers).
+  int32_t monic44;                  // 1 when the configuration is (4,4)
+  double pm[4], qm[4];
+  double lin_s, lin_o;              // linear branch / k
+  double out_l, out_a, out_b;       // 116 k, 500 k, 200 k
 };
 
 // ---------------------------------------------------------------- Horner

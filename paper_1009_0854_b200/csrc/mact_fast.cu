@@ -21,15 +21,27 @@ struct OpLab {
     float gamma[256 * 32];   // GAMMA_TABLE (fast.py:35) in fp32, replicated per bank
   };
   static __device__ __forceinline__ void init(Shared* s, const Params&) {
-    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
-      const int k = i >> 5;
-      s->gamma[i] = (float)inverse_gamma_d((double)k / 255.0);
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) {   // 256 pow() per CTA, then replicate
+      const float v = (float)inverse_gamma_d((double)k / 255.0);
+#pragma unroll 8
+      for (int r = 0; r < 32; ++r) s->gamma[(k << 5) | ((r + k) & 31)] = v;
     }
   }
   static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
                                             uint32_t lane, const Params& c, float (*o)[3]) {
     const Lab3 v = lab_fast_u8(r, g, b, s->gamma, lane, c);
     o[0][0] = v.c0; o[0][1] = v.c1; o[0][2] = v.c2;
+  }
+  static __device__ __forceinline__ void px4(const uint32_t (&ch)[12], const Shared* s,
+                                             uint32_t lane, const Params& c, float (*o)[1][3]) {
+    if (c.monic44) {
+      float v[4][3];
+      lab_fast_u8x4(ch, s->gamma, lane, c, v);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { o[q][0][0] = v[q][0]; o[q][0][1] = v[q][1]; o[q][0][2] = v[q][2]; }
+    } else {
+      px4_each<OpLab>(ch, s, lane, c, o);
+    }
   }
 };
 
@@ -43,6 +55,10 @@ struct OpHsi {
     const Lab3 v = hsi_fast_u8((int)r, (int)g, (int)b, c);
     o[0][0] = v.c0; o[0][1] = v.c1; o[0][2] = v.c2;
   }
+  static __device__ __forceinline__ void px4(const uint32_t (&ch)[12], const Shared* s,
+                                             uint32_t lane, const Params& c, float (*o)[1][3]) {
+    px4_each<OpHsi>(ch, s, lane, c, o);
+  }
 };
 
 struct OpSct {
@@ -54,6 +70,10 @@ struct OpSct {
                                             uint32_t, const Params& c, float (*o)[3]) {
     const Lab3 v = sct_fast_u8((int)r, (int)g, (int)b, c);
     o[0][0] = v.c0; o[0][1] = v.c1; o[0][2] = v.c2;
+  }
+  static __device__ __forceinline__ void px4(const uint32_t (&ch)[12], const Shared* s,
+                                             uint32_t lane, const Params& c, float (*o)[1][3]) {
+    px4_each<OpSct>(ch, s, lane, c, o);
   }
 };
 
@@ -70,6 +90,23 @@ struct OpAll {
     o[0][0] = a.c0; o[0][1] = a.c1; o[0][2] = a.c2;
     o[1][0] = h.c0; o[1][1] = h.c1; o[1][2] = h.c2;
     o[2][0] = q.c0; o[2][1] = q.c1; o[2][2] = q.c2;
+  }
+  static __device__ __forceinline__ void px4(const uint32_t (&ch)[12], const Shared* s,
+                                             uint32_t lane, const Params& c, float (*o)[3][3]) {
+    if (c.monic44) {
+      float v[4][3];
+      lab_fast_u8x4(ch, s->gamma, lane, c, v);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        o[q][0][0] = v[q][0]; o[q][0][1] = v[q][1]; o[q][0][2] = v[q][2];
+        const Lab3 h = hsi_fast_u8((int)ch[3 * q], (int)ch[3 * q + 1], (int)ch[3 * q + 2], c);
+        const Lab3 z = sct_fast_u8((int)ch[3 * q], (int)ch[3 * q + 1], (int)ch[3 * q + 2], c);
+        o[q][1][0] = h.c0; o[q][1][1] = h.c1; o[q][1][2] = h.c2;
+        o[q][2][0] = z.c0; o[q][2][1] = z.c1; o[q][2][2] = z.c2;
+      }
+    } else {
+      px4_each<OpAll>(ch, s, lane, c, o);
+    }
   }
 };
 
@@ -93,16 +130,51 @@ __global__ void k_fast_real(int space, const T* __restrict__ in, float* __restri
 }
 
 // ------------------------------------------------------------ launchers
-template <class Op, int TP, int NT, int SIN>
-struct StreamCfg {
-  static constexpr int tp = TP, nt = NT, sin = SIN;
-};
-
-// Tile configurations (see DESIGN.md §Kernels for the smem/occupancy math).
-using CfgLab = StreamCfg<OpLab, 2048, 256, 3>;   // 98 KB smem -> 2 CTA/SM
-using CfgHsi = StreamCfg<OpHsi, 2048, 256, 3>;   // 66 KB -> 3 CTA/SM
-using CfgSct = StreamCfg<OpSct, 2048, 256, 3>;
-using CfgAll = StreamCfg<OpAll, 1024, 256, 2>;   // 110 KB -> 2 CTA/SM
+// Tile configurations <Op, NW compute warps, G groups/lane, SIN input stages,
+// NOB output buffers per warp> (DESIGN.md §Kernels has the smem/occupancy math).
+// Overridable at build time for tuning (MACT_NVCC_DEFS, see build.py).
+// CIELAB: 68 KB smem (32 KB bank-replicated gamma) -> 3 CTA/SM
+#ifndef MACT_LAB_NW
+#define MACT_LAB_NW 8
+#endif
+#ifndef MACT_LAB_G
+#define MACT_LAB_G 1
+#endif
+#ifndef MACT_LAB_SIN
+#define MACT_LAB_SIN 4
+#endif
+#ifndef MACT_LAB_NOB
+#define MACT_LAB_NOB 2
+#endif
+// HSI / SCT: 72 KB -> 3 CTA/SM
+#ifndef MACT_HS_NW
+#define MACT_HS_NW 8
+#endif
+#ifndef MACT_HS_G
+#define MACT_HS_G 2
+#endif
+#ifndef MACT_HS_SIN
+#define MACT_HS_SIN 4
+#endif
+#ifndef MACT_HS_NOB
+#define MACT_HS_NOB 2
+#endif
+// fused triple: 77 KB -> 2 CTA/SM
+#ifndef MACT_ALL_NW
+#define MACT_ALL_NW 8
+#endif
+#ifndef MACT_ALL_G
+#define MACT_ALL_G 1
+#endif
+#ifndef MACT_ALL_SIN
+#define MACT_ALL_SIN 4
+#endif
+#ifndef MACT_ALL_NOB
+#define MACT_ALL_NOB 1
+#endif
+#define MACT_LAB_CFG MACT_LAB_NW, MACT_LAB_G, MACT_LAB_SIN, MACT_LAB_NOB
+#define MACT_HS_CFG MACT_HS_NW, MACT_HS_G, MACT_HS_SIN, MACT_HS_NOB
+#define MACT_ALL_CFG MACT_ALL_NW, MACT_ALL_G, MACT_ALL_SIN, MACT_ALL_NOB
 
 template <typename T>
 static int launch_real(int space, const T* in, float* out, int64_t n, int planar,
@@ -131,10 +203,10 @@ static int fast_entry(int space, const void* rgb, int in_dtype, float* out, int6
   switch (in_dtype) {
     case MACT_DTYPE_U8:
       if (space == MACT_SPACE_LAB)
-        return launch_stream_t<OpLab, CfgLab::tp, CfgLab::nt, CfgLab::sin>(in, outs, n, planar, kc, st, "lab_fast");
+        return launch_stream_t<OpLab, MACT_LAB_CFG>(in, outs, n, planar, kc, st, "lab_fast");
       if (space == MACT_SPACE_HSI)
-        return launch_stream_t<OpHsi, CfgHsi::tp, CfgHsi::nt, CfgHsi::sin>(in, outs, n, planar, kc, st, "hsi_fast");
-      return launch_stream_t<OpSct, CfgSct::tp, CfgSct::nt, CfgSct::sin>(in, outs, n, planar, kc, st, "sct_fast");
+        return launch_stream_t<OpHsi, MACT_HS_CFG>(in, outs, n, planar, kc, st, "hsi_fast");
+      return launch_stream_t<OpSct, MACT_HS_CFG>(in, outs, n, planar, kc, st, "sct_fast");
     case MACT_DTYPE_F32:
       return launch_real<float>(space, (const float*)rgb, out, n, planar, kc, st);
     case MACT_DTYPE_F64:
@@ -169,6 +241,6 @@ extern "C" int mact_all_fast(const uint8_t* rgb, float* lab, float* hsi, float* 
   KCoeffs kc;
   if (int rc = make_kcoeffs(c, &kc)) return rc;
   Outs outs{{lab, hsi, sct}};
-  return launch_stream_t<OpAll, CfgAll::tp, CfgAll::nt, CfgAll::sin>(
+  return launch_stream_t<OpAll, MACT_ALL_CFG>(
       rgb, outs, n, layout == MACT_LAYOUT_PLANAR, kc, (cudaStream_t)stream, "all_fast");
 }

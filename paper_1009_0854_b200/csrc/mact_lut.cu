@@ -60,6 +60,10 @@ struct OpLut {
     }
     o[0][0] = a0; o[0][1] = a1; o[0][2] = a2;
   }
+  static __device__ __forceinline__ void px4(const uint32_t (&ch)[12], const Shared* s,
+                                             uint32_t lane, const Params& p, float (*o)[1][3]) {
+    px4_each<OpLut>(ch, s, lane, p, o);
+  }
 };
 
 // ---------------------------------------------------------------- build
@@ -103,10 +107,11 @@ __global__ void k_lut_nodes(const uint8_t* __restrict__ rgb, int64_t n, int32_t*
 template <int N, int METHOD>
 static int launch_interp(const float* lat, const uint8_t* rgb, float* out, int64_t n, int planar,
                          cudaStream_t st) {
-  constexpr int TP = N <= 9 ? 2048 : 1024;
   Outs outs{{out, nullptr, nullptr}};
   LutParams p{lat};
-  return launch_stream_t<OpLut<N, METHOD>, TP, 256, 3>(rgb, outs, n, planar, p, st, "lut_interp");
+  // 17^3 lattice = 78.6 KB of smem: 8 warps x G=1 + 4 stages -> 2 CTA/SM
+  return launch_stream_t<OpLut<N, METHOD>, 8, (N <= 9 ? 2 : 1), 4, 2>(rgb, outs, n, planar, p, st,
+                                                                      "lut_interp");
 }
 
 template <int N>

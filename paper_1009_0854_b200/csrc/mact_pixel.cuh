@@ -30,23 +30,51 @@ __device__ __forceinline__ double inverse_gamma_d(double k) {
 }
 
 // -------------------------------------------------------------- CIELAB fast
-// Lightness kernel branch f(t) as a double-float (hi + lo), fast.py:110-115.
-__device__ __forceinline__ void lab_f_fast_df(float t, const KCoeffs& c, float& hi, float& lo) {
-  const double td = f2d_pos(t);
+__device__ __forceinline__ double rcp_approx_d(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+
+// Lightness kernel f(t) (fast.py:110-115): t is the fp32 X/Xn, Y/Yn or Z/Zn.
+// The rational P/Q is evaluated in fp64 Horner (approximants.py:55-82) and
+// divided with MUFU.RCP64H + one Newton correction of the quotient
+// (q1 = q0 + (P - q0 Q) y0, relative error ~e0^2), all in fp64, so f keeps
+// ~1e-12 relative accuracy for the 500 (fx - fy) amplification (H1).
+__device__ __forceinline__ double lab_f_fast(float t, const KCoeffs& c) {
+  const double td = (double)t;                       // F2F on the XU pipe (1 issue slot)
   const double P = horner_d<kCbrtDeg>(c.cbrt_num, td);
   const double Q = horner_d<kCbrtDeg>(c.cbrt_den, td);
-  const float rq = rcp_approx(d2f_pos_trunc(Q));
-  const float q0 = d2f_pos_trunc(P) * rq;            // ~4 ulp estimate of P/Q
-  const double r = fma(-f2d_pos(q0), Q, P);          // exact-ish residual in fp64
-  const float corr = __double2float_rn(r) * rq;      // r/Q, tiny
-  const bool cube = t > (float)kLabKnee;              // strict '>' (fast.py:114)
-  hi = cube ? q0 : fmaf((float)kLabSlope, t, (float)kLabOffset);
-  lo = cube ? corr : 0.0f;
+  const double y0 = rcp_approx_d(Q);
+  const double q0 = P * y0;
+  double f = fma(fma(-q0, Q, P), y0, q0);
+  if (!(t > (float)kLabKnee)) f = fma(kLabSlope, td, kLabOffset);   // strict '>' (fast.py:114)
+  return f;
 }
 
 struct Lab3 {
   float c0, c1, c2;
 };
+
+// Batched 4-pixel CIELAB for the default (4,4) rational in monic form.
+// One warp vote decides whether any lane of the warp has a channel on the
+// linear branch (t <= knee: ~0.04-0.3 % of colours per channel); only then
+// is the linear value computed, so the common path has no selects.
+__device__ __forceinline__ double monic4(const double* cm, double t) {
+  double acc = t + cm[3];
+  acc = fma(acc, t, cm[2]);
+  acc = fma(acc, t, cm[1]);
+  return fma(acc, t, cm[0]);
+}
+__device__ __forceinline__ double lab_f_monic(float t, const KCoeffs& c) {
+  const double td = f2d_pos(t);
+  const double P = monic4(c.pm, td), Q = monic4(c.qm, td);
+  const double y0 = rcp_approx_d(Q);
+  const double q0 = P * y0;
+  const double f = fma(fma(-q0, Q, P), y0, q0);
+  return t > (float)kLabKnee ? f : fma(c.lin_s, (double)t, c.lin_o);
+}
+
 
 // gamma_rep: 256 entries replicated 32x, entry i at [i*32 + lane] (conflict-free)
 __device__ __forceinline__ Lab3 lab_fast_u8(uint32_t r, uint32_t g, uint32_t b,
@@ -58,15 +86,55 @@ __device__ __forceinline__ Lab3 lab_fast_u8(uint32_t r, uint32_t g, uint32_t b,
   const float tx = fmaf(c.mxyz[2], gb, fmaf(c.mxyz[1], gg, c.mxyz[0] * gr));
   const float ty = fmaf(c.mxyz[5], gb, fmaf(c.mxyz[4], gg, c.mxyz[3] * gr));
   const float tz = fmaf(c.mxyz[8], gb, fmaf(c.mxyz[7], gg, c.mxyz[6] * gr));
-  float hx, lx, hy, ly, hz, lz;
-  lab_f_fast_df(tx, c, hx, lx);
-  lab_f_fast_df(ty, c, hy, ly);
-  lab_f_fast_df(tz, c, hz, lz);
   Lab3 o;
-  o.c0 = fmaf(116.0f, ly, fmaf(116.0f, hy, -16.0f));
-  o.c1 = 500.0f * ((hx - hy) + (lx - ly));
-  o.c2 = 200.0f * ((hy - hz) + (ly - lz));
+  if (c.monic44) {   // same arithmetic as lab_fast_u8x4 (bit-identical tile/tail paths)
+    const double fx = lab_f_monic(tx, c), fy = lab_f_monic(ty, c), fz = lab_f_monic(tz, c);
+    o.c0 = (float)fma(c.out_l, fy, -16.0);
+    o.c1 = (float)(c.out_a * (fx - fy));
+    o.c2 = (float)(c.out_b * (fy - fz));
+    return o;
+  }
+  const double fx = lab_f_fast(tx, c), fy = lab_f_fast(ty, c), fz = lab_f_fast(tz, c);
+  o.c0 = (float)fma(116.0, fy, -16.0);
+  o.c1 = (float)(500.0 * (fx - fy));
+  o.c2 = (float)(200.0 * (fy - fz));
   return o;
+}
+
+__device__ __forceinline__ void lab_fast_u8x4(const uint32_t (&ch)[12], const float* gamma_rep,
+                                              uint32_t lane, const KCoeffs& c, float (*o)[3]) {
+  float t[12];
+  bool low = false;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const float gr = gamma_rep[(ch[3 * p] << 5) | lane];
+    const float gg = gamma_rep[(ch[3 * p + 1] << 5) | lane];
+    const float gb = gamma_rep[(ch[3 * p + 2] << 5) | lane];
+    t[3 * p] = fmaf(c.mxyz[2], gb, fmaf(c.mxyz[1], gg, c.mxyz[0] * gr));
+    t[3 * p + 1] = fmaf(c.mxyz[5], gb, fmaf(c.mxyz[4], gg, c.mxyz[3] * gr));
+    t[3 * p + 2] = fmaf(c.mxyz[8], gb, fmaf(c.mxyz[7], gg, c.mxyz[6] * gr));
+  }
+  double f[12];
+#pragma unroll
+  for (int j = 0; j < 12; ++j) {
+    low |= !(t[j] > (float)kLabKnee);
+    const double td = f2d_pos(t[j]);
+    const double P = monic4(c.pm, td), Q = monic4(c.qm, td);
+    const double y0 = rcp_approx_d(Q);
+    const double q0 = P * y0;
+    f[j] = fma(fma(-q0, Q, P), y0, q0);
+  }
+  if (__any_sync(0xffffffffu, low)) {
+#pragma unroll
+    for (int j = 0; j < 12; ++j)
+      if (!(t[j] > (float)kLabKnee)) f[j] = fma(c.lin_s, (double)t[j], c.lin_o);
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    o[p][0] = (float)fma(c.out_l, f[3 * p + 1], -16.0);
+    o[p][1] = (float)(c.out_a * (f[3 * p] - f[3 * p + 1]));
+    o[p][2] = (float)(c.out_b * (f[3 * p + 1] - f[3 * p + 2]));
+  }
 }
 
 // Reference-faithful fp64 evaluation on real-valued channels (float input

@@ -116,6 +116,20 @@ int make_kcoeffs(const MactCoeffs* c, KCoeffs* k) {
   const double white[3] = {kWhiteX, kWhiteY, kWhiteZ};
   for (int r = 0; r < 3; ++r)
     for (int col = 0; col < 3; ++col) k->mxyz[r * 3 + col] = (float)(rgb2xyz(r, col) / white[r]);
+  k->monic44 = (c->cbrt_num_deg == 4 && c->cbrt_den_deg == 4 && c->cbrt_num[4] != 0.0 &&
+                c->cbrt_den[4] != 0.0) ? 1 : 0;
+  if (k->monic44) {
+    const double p4 = c->cbrt_num[4], q4 = c->cbrt_den[4], kk = p4 / q4;
+    for (int i = 0; i < 4; ++i) {
+      k->pm[i] = c->cbrt_num[i] / p4;
+      k->qm[i] = c->cbrt_den[i] / q4;
+    }
+    k->lin_s = kLabSlope / kk;
+    k->lin_o = kLabOffset / kk;
+    k->out_l = 116.0 * kk;
+    k->out_a = 500.0 * kk;
+    k->out_b = 200.0 * kk;
+  }
   return MACT_OK;
 }
 

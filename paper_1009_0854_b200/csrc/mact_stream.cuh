@@ -1,21 +1,28 @@
-// mact_stream.cuh — persistent streaming skeleton shared by every per-pixel
-// kernel of the path (MACT transforms and LUT interpolators).
+// mact_stream.cuh — persistent, warp-specialised streaming skeleton shared by
+// every per-pixel kernel of the path (MACT transforms and LUT interpolators).
 //
 // Data layout in HBM: packed interleaved uint8 RGB in (3 B/px, the
 // reference's (...,3) C-order layout), fp32 out interleaved (N,3) or planar
 // (3,N).  The path is HBM-bound (15 B/px algorithmic traffic per transform),
-// so the kernel is built around the Blackwell bulk-copy engine:
+// so data moves with the Blackwell bulk-copy engine (cp.async.bulk, SASS
+// UBLKCP) and the SMs only compute:
 //
-//   * one CTA per SM slot, grid-stride over tiles of TP pixels;
-//   * thread 0 streams input tiles global->smem with cp.async.bulk into an
-//     SIN-deep mbarrier ring (3*TP bytes each, no register staging, no LSU
-//     instructions for the loads);
-//   * all threads read their 4-pixel groups from smem (3 x LDS.32, stride-3
-//     words: conflict-free), compute, and write fp32 results to one of two
-//     output staging buffers (STS.128, conflict-free);
-//   * thread 0 drains each output tile smem->global with cp.async.bulk
-//     bulk_group stores (12*TP bytes per output, 4*TP per plane), double
-//     buffered against compute with wait_group.read.
+//   * CTA = NW compute warps + 1 producer warp, persistent, grid-stride over
+//     tiles of TP = NW * 128 * G pixels;
+//   * producer (one lane): streams input tiles global->smem into an SIN-deep
+//     ring; full[s] completes on the transaction bytes, empty[s] collects one
+//     arrival per compute warp before stage s is refilled;
+//   * compute warp w owns the contiguous slice [w*WPX, (w+1)*WPX) of each tile
+//     (WPX = 128*G); lane l takes 4-pixel groups g*32 + l: 3 x LDS.32 at a
+//     stride of 3 words (conflict-free), results to the warp's own staging
+//     buffer with STS.128 (conflict-free), then lane 0 drains the slice with
+//     one bulk store per output array (WPX*12 B, or 3 planes of WPX*4 B).
+//     Output buffers are NOB-deep per warp and recycled with
+//     cp.async.bulk.wait_group.read — no CTA-wide barrier anywhere in the loop.
+//
+// WAR across proxies: a compute warp arrives on empty[s] only after its
+// results derived from stage s were written to smem and made visible to the
+// async proxy, so the producer's refill can never overtake a pending LDS.
 //
 // Tiles that are not whole (the tail) and unaligned buffers go through the
 // per-pixel generic kernel.
@@ -30,43 +37,62 @@ namespace mact {
 //   using Params;                           // __grid_constant__ parameter block
 //   struct Shared;                          // per-CTA shared state (tables)
 //   static __device__ void init(Shared*, const Params&);   // all threads, then __syncthreads
-//   static __device__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared*,
-//                             uint32_t lane, const Params&, float (*o)[3]);
+//   static __device__ void px(r, g, b, const Shared*, lane, const Params&, float (*o)[3]);
+//   static __device__ void px4(const uint32_t (&ch)[12], const Shared*, lane,
+//                              const Params&, float (*o)[NOUT][3]);   // warp-converged
 
 struct Outs {
   float* o[3];
 };
 
-template <class Op, int TP, int SIN>
-struct StreamSmem {
+// Default 4-pixel batch: four independent px() calls.
+template <class Op>
+__device__ __forceinline__ void px4_each(const uint32_t (&ch)[12], const typename Op::Shared* sh,
+                                         uint32_t lane, const typename Op::Params& p,
+                                         float (*o)[Op::NOUT][3]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Op::px(ch[3 * q], ch[3 * q + 1], ch[3 * q + 2], sh, lane, p, o[q]);
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <class Op, int NW, int G, int SIN, int NOB>
+struct WsLayout {
+  static constexpr int WPX = 128 * G;                 // pixels per warp slice
+  static constexpr int TP = NW * WPX;                 // pixels per tile
   static constexpr int IN_BYTES = TP * 3;
-  static constexpr int OUT_FLOATS = TP * 3;                    // per output triple-array
+  static constexpr int OUT_FLOATS = WPX * 3;          // one output array of one slice
   static constexpr size_t in_off = 0;
   static constexpr size_t out_off = (size_t)SIN * IN_BYTES;
-  static constexpr size_t bar_off = out_off + 2ull * Op::NOUT * OUT_FLOATS * 4;
-  static constexpr size_t sh_off = (bar_off + SIN * 8 + 127) / 128 * 128;
+  static constexpr size_t out_warp = (size_t)NOB * Op::NOUT * OUT_FLOATS * 4;
+  static constexpr size_t bar_off = out_off + NW * out_warp;
+  static constexpr size_t sh_off = (bar_off + 2 * SIN * 8 + 127) / 128 * 128;
   static constexpr size_t bytes = sh_off + sizeof(typename Op::Shared);
+  static constexpr int threads = 32 * (NW + 1);
 };
 
-template <class Op, int TP, int NT, int SIN>
-__global__ void __launch_bounds__(NT) k_stream(const uint8_t* __restrict__ in, Outs outs,
-                                                int64_t n, int64_t ntiles, int planar,
-                                                const __grid_constant__ typename Op::Params p) {
-  using L = StreamSmem<Op, TP, SIN>;
+template <class Op, int NW, int G, int SIN, int NOB>
+__global__ void __launch_bounds__(32 * (NW + 1)) k_ws(const uint8_t* __restrict__ in, Outs outs,
+                                                       int64_t n, int64_t ntiles, int planar,
+                                                       const __grid_constant__ typename Op::Params p) {
+  using L = WsLayout<Op, NW, G, SIN, NOB>;
   constexpr int NOUT = Op::NOUT;
-  constexpr int G = TP / (4 * NT);                 // 4-pixel groups per thread per tile
-  static_assert(TP % (4 * NT) == 0, "tile must split into 4-pixel groups");
-  static_assert((TP * 3) % 16 == 0, "bulk copies need 16-byte multiples");
+  static_assert((L::IN_BYTES % 16) == 0 && (L::OUT_FLOATS * 4) % 16 == 0, "bulk copies need 16 B");
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* in_s = smem + L::in_off;
-  float* out_s = reinterpret_cast<float*>(smem + L::out_off);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::bar_off);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::bar_off);
+  uint64_t* empty = full + SIN;
   auto* sh = reinterpret_cast<typename Op::Shared*>(smem + L::sh_off);
-  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
 #pragma unroll
-    for (int s = 0; s < SIN; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < SIN; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NW);
+    }
     fence_mbar_init();
   }
   Op::init(sh, p);
@@ -74,45 +100,41 @@ __global__ void __launch_bounds__(NT) k_stream(const uint8_t* __restrict__ in, O
 
   const int64_t first = blockIdx.x, stride = gridDim.x;
   const int64_t my_tiles = ntiles > first ? (ntiles - first + stride - 1) / stride : 0;
-  if (tid == 0) {
-    for (int s = 0; s < SIN && s < my_tiles; ++s) {
-      const int64_t t = first + s * stride;
-      mbar_arrive_expect_tx(&bars[s], L::IN_BYTES);
-      bulk_g2s(in_s + s * L::IN_BYTES, in + t * L::IN_BYTES, L::IN_BYTES, &bars[s]);
+
+  if (warp == NW) {                                       // ---- producer warp
+    if (lane == 0) {
+      for (int64_t i = 0; i < my_tiles; ++i) {
+        const int s = (int)(i % SIN);
+        if (i >= SIN) mbar_wait(&empty[s], (uint32_t)(((i / SIN) - 1) & 1));
+        mbar_arrive_expect_tx(&full[s], L::IN_BYTES);
+        bulk_g2s(in_s + (size_t)s * L::IN_BYTES, in + (first + i * stride) * L::IN_BYTES,
+                 L::IN_BYTES, &full[s]);
+      }
     }
+    return;
   }
 
+  // ---- compute warps
+  float* out_w = reinterpret_cast<float*>(smem + L::out_off + warp * L::out_warp);
   for (int64_t i = 0; i < my_tiles; ++i) {
     const int64_t t = first + i * stride;
     const int s = (int)(i % SIN);
-    mbar_wait(&bars[s], (uint32_t)((i / SIN) & 1));
-    const uint32_t* wsrc = reinterpret_cast<const uint32_t*>(in_s + s * L::IN_BYTES);
-    uint32_t w[G][3];
+    const int ob = NOB == 1 ? 0 : (int)(i % NOB);
+    float* ob_s = out_w + (size_t)ob * NOUT * L::OUT_FLOATS;
+    if (lane == 0) bulk_wait_read<NOB - 1>();             // this buffer's last store has read it
+    __syncwarp();
+    mbar_wait(&full[s], (uint32_t)((i / SIN) & 1));
+    const uint32_t* wsrc =
+        reinterpret_cast<const uint32_t*>(in_s + (size_t)s * L::IN_BYTES) + warp * (L::WPX / 4) * 3;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const int q = (g * NT + (int)tid) * 3;
-      w[g][0] = wsrc[q];
-      w[g][1] = wsrc[q + 1];
-      w[g][2] = wsrc[q + 2];
-    }
-    const int ob = (int)(i & 1);
-    if (tid == 0) bulk_wait_read<1>();            // tile i-2's stores have read buffer ob
-    __syncthreads();                              // input stage s consumed; buffer ob free
-    if (tid == 0 && i + SIN < my_tiles) {
-      const int64_t tn = first + (i + SIN) * stride;
-      mbar_arrive_expect_tx(&bars[s], L::IN_BYTES);
-      bulk_g2s(in_s + s * L::IN_BYTES, in + tn * L::IN_BYTES, L::IN_BYTES, &bars[s]);
-    }
-    float* ob_s = out_s + (size_t)ob * NOUT * L::OUT_FLOATS;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const uint32_t w0 = w[g][0], w1 = w[g][1], w2 = w[g][2];
+      const int grp = g * 32 + (int)lane;                 // 4-pixel group inside the warp slice
+      const uint32_t w0 = wsrc[3 * grp], w1 = wsrc[3 * grp + 1], w2 = wsrc[3 * grp + 2];
+      const uint32_t ch[12] = {byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), byte_of(w0, 3),
+                               byte_of(w1, 0), byte_of(w1, 1), byte_of(w1, 2), byte_of(w1, 3),
+                               byte_of(w2, 0), byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3)};
       float o[4][NOUT][3];
-      Op::px(byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), sh, lane, p, o[0]);
-      Op::px(byte_of(w0, 3), byte_of(w1, 0), byte_of(w1, 1), sh, lane, p, o[1]);
-      Op::px(byte_of(w1, 2), byte_of(w1, 3), byte_of(w2, 0), sh, lane, p, o[2]);
-      Op::px(byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3), sh, lane, p, o[3]);
-      const int grp = g * NT + (int)tid;          // 4-pixel group index inside the tile
+      Op::px4(ch, sh, lane, p, o);
 #pragma unroll
       for (int k = 0; k < NOUT; ++k) {
         float* base = ob_s + k * L::OUT_FLOATS;
@@ -124,30 +146,32 @@ __global__ void __launch_bounds__(NT) k_stream(const uint8_t* __restrict__ in, O
         } else {
 #pragma unroll
           for (int c = 0; c < 3; ++c)
-            *reinterpret_cast<float4*>(base + c * TP + grp * 4) =
+            *reinterpret_cast<float4*>(base + c * L::WPX + grp * 4) =
                 make_float4(o[0][k][c], o[1][k][c], o[2][k][c], o[3][k][c]);
         }
       }
     }
     fence_proxy_async_smem();
-    __syncthreads();
-    if (tid == 0) {
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t px0 = t * L::TP + (int64_t)warp * L::WPX;
 #pragma unroll
       for (int k = 0; k < NOUT; ++k) {
         float* dst = outs.o[k];
         if (dst == nullptr) continue;
         const float* src = ob_s + k * L::OUT_FLOATS;
         if (!planar) {
-          bulk_s2g(dst + t * (int64_t)TP * 3, src, TP * 12);
+          bulk_s2g(dst + px0 * 3, src, L::WPX * 12);
         } else {
 #pragma unroll
-          for (int c = 0; c < 3; ++c) bulk_s2g(dst + c * n + t * (int64_t)TP, src + c * TP, TP * 4);
+          for (int c = 0; c < 3; ++c) bulk_s2g(dst + c * n + px0, src + c * L::WPX, L::WPX * 4);
         }
       }
       bulk_commit();
+      mbar_arrive(&empty[s]);                             // stage s fully consumed by this warp
     }
   }
-  if (tid == 0) bulk_wait<0>();
+  if (lane == 0) bulk_wait<0>();
 }
 
 // Per-pixel fallback for the tail tile and unaligned buffers.
@@ -178,37 +202,34 @@ __global__ void __launch_bounds__(NT) k_generic(const uint8_t* __restrict__ in, 
   }
 }
 
-// Host launcher: persistent bulk-copy kernel over whole tiles, generic kernel
-// for the tail (or everything, when a buffer is not 16-byte aligned).
-template <class Op, int TP, int NT, int SIN>
+// Host launcher: whole tiles on k_ws, the remainder (or everything, when a
+// buffer is not 16-byte aligned) on k_generic.
+template <class Op, int NW, int G, int SIN, int NOB>
 inline int launch_stream_t(const uint8_t* in, Outs outs, int64_t n, int planar,
-                         const typename Op::Params& p, cudaStream_t st, const char* name) {
+                           const typename Op::Params& p, cudaStream_t st, const char* name) {
   if (n <= 0) return MACT_OK;
-  using L = StreamSmem<Op, TP, SIN>;
+  using L = WsLayout<Op, NW, G, SIN, NOB>;
   bool aligned = ((uintptr_t)in % 16) == 0;
-  for (int k = 0; k < Op::NOUT; ++k) {
+  for (int k = 0; k < Op::NOUT; ++k)
     if (outs.o[k] && ((uintptr_t)outs.o[k] % 16) != 0) aligned = false;
-  }
   if (planar && (n % 4) != 0) aligned = false;
-  int64_t ntiles = aligned ? n / TP : 0;
+  const int64_t ntiles = aligned ? n / L::TP : 0;
   if (ntiles > 0) {
-    auto kfn = k_stream<Op, TP, NT, SIN>;
-    int64_t grid = persistent_grid((const void*)kfn, NT, L::bytes);
+    auto kfn = k_ws<Op, NW, G, SIN, NOB>;
+    int64_t grid = persistent_grid((const void*)kfn, L::threads, L::bytes);
     if (grid <= 0) return MACT_ECUDA;
     if (grid > ntiles) grid = ntiles;
-    kfn<<<(unsigned)grid, NT, L::bytes, st>>>(in, outs, n, ntiles, planar, p);
+    kfn<<<(unsigned)grid, L::threads, L::bytes, st>>>(in, outs, n, ntiles, planar, p);
     count_launch();
-    int rc2 = check_launch(name);
-    if (rc2) return rc2;
+    if (int rc = check_launch(name)) return rc;
   }
-  const int64_t done = ntiles * TP;
+  const int64_t done = ntiles * L::TP;
   if (done < n) {
-    const int64_t rem = n - done;
     auto kfn = k_generic<Op, 256>;
     const size_t sb = sizeof(typename Op::Shared);
     const int64_t cap = persistent_grid((const void*)kfn, 256, sb);
     if (cap <= 0) return MACT_ECUDA;
-    int64_t grid = (rem + 255) / 256;
+    int64_t grid = (n - done + 255) / 256;
     if (grid > cap) grid = cap;
     kfn<<<(unsigned)grid, 256, sb, st>>>(in, outs, done, n, planar, p);
     count_launch();
