@@ -92,7 +92,7 @@ typedef struct MactErrSpec {
   int32_t lut_grid_n;   /* for MACT_CAND_LUT                                   */
   int32_t lut_method;   /* MACT_LUT_*                                          */
   int32_t cand_dtype;   /* MACT_CAND_ARRAY: MACT_DTYPE_F32 / _F64, interleaved */
-  const float* lut_lattice;   /* (n^3, 3) fp32, r-major                        */
+  const float* lut_lattice;   /* (n^3, 4) fp32 device lattice, r-major          */
   const void* cand_array;     /* (n, 3) candidate outputs                      */
   const void* ref_array;      /* optional (n,3) reference outputs, NULL = exact on device */
   int32_t ref_dtype;
@@ -128,11 +128,14 @@ int mact_distance(int space, const void* x, int x_dtype, const void* y, int y_dt
 
 /* ---- 3D LUT (K4) --------------------------------------------------------- */
 /* replaces mact.lut.build_lut (lut.py:82-95): lattice values at k*255/(n-1),
- * NaN -> 0; writes fp64 (n^3,3) and/or fp32 (n^3,3), either may be NULL. */
+ * NaN -> 0; writes fp64 (n^3,3) and/or the fp32 DEVICE LATTICE (n^3,4):
+ * node = (c0, c1, c2, 0), 16-byte aligned (one 16-B load per node).  Either
+ * output may be NULL. */
 int mact_lut_build(int space, int grid_n, double* lattice_f64, float* lattice_f32,
                    void* stream);
 /* replaces mact.lut.interpolate(lut, pixels, method, "standard") (lut.py:231-246,
- * :341-350) for the linear (CIELAB) destination; in_dtype U8. */
+ * :341-350) for the linear (CIELAB) destination; `lattice` is the (n^3,4)
+ * device lattice of mact_lut_build; pixels uint8. */
 int mact_lut_interp(const float* lattice, int grid_n, int method, const uint8_t* rgb,
                     float* out, int64_t n, int layout, void* stream);
 /* replaces mact.lut.node_weights (lut.py:115-199): flat node indices (n,k)
@@ -166,6 +169,12 @@ int mact_host_ctx_create(int device, int64_t chunk_px, int nstreams, MactHostCtx
 int mact_host_ctx_destroy(MactHostCtx* ctx);
 int mact_transform_host(MactHostCtx* ctx, int op, const uint8_t* host_rgb, float* host_out,
                         int64_t n, const MactCoeffs* c, int layout);
+
+/* ---- calibration ---------------------------------------------------------- */
+/* out = (r, g, b) as fp32 through the same streaming kernel: the achievable
+ * bandwidth of the 3 B in / 12 B out pattern with no arithmetic (not a
+ * reference function; bench.py reports it next to the HBM roofline). */
+int mact_probe_expand(const uint8_t* rgb, float* out, int64_t n, void* stream);
 
 /* ---- misc ----------------------------------------------------------------- */
 const char* mact_last_error(void);

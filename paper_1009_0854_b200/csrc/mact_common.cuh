@@ -96,6 +96,15 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+// Byte k of w as an exact float (one PRMT builds 2^23 + byte, one FADD removes 2^23).
+__device__ __forceinline__ float fbyte(uint32_t w, int k) {
+  return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u | (uint32_t)k)) - 8388608.0f;
+}
 __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) {
   return __byte_perm(w, 0u, 0x4440u + (uint32_t)k);
 }
@@ -121,16 +130,19 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+// Blocking wait on an mbarrier phase.  The suspend-time hint lets the
+// hardware park the warp until the phase completes (instead of returning
+// false after a short internal timeout and spinning through YIELD/BRA).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(addr),
-      "r"(parity)
+      "r"(parity), "r"(0x100000u)
       : "memory");
 }
 

@@ -14,6 +14,9 @@
 namespace mact {
 
 // ---------------------------------------------------------------- ops
+// px(): one pixel (tail / unaligned kernel); px4w(): the 4 pixels packed in
+// three input words (streaming kernel, warp-converged).  Both run the same
+// arithmetic, so tile and tail results are bit-identical.
 struct OpLab {
   static constexpr int NOUT = 1;
   using Params = KCoeffs;
@@ -32,50 +35,83 @@ struct OpLab {
     const Lab3 v = lab_fast_u8(r, g, b, s->gamma, lane, c);
     o[0][0] = v.c0; o[0][1] = v.c1; o[0][2] = v.c2;
   }
-  static __device__ __forceinline__ void px4(const uint32_t (&ch)[12], const Shared* s,
-                                             uint32_t lane, const Params& c, float (*o)[1][3]) {
+  static __device__ __forceinline__ void px4w(uint32_t w0, uint32_t w1, uint32_t w2,
+                                              const Shared* s, uint32_t lane, const Params& c,
+                                              float (*o)[1][3]) {
+    const uint32_t ch[12] = {byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), byte_of(w0, 3),
+                             byte_of(w1, 0), byte_of(w1, 1), byte_of(w1, 2), byte_of(w1, 3),
+                             byte_of(w2, 0), byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3)};
+#ifdef MACT_LAB_MONIC_ONLY   // analysis builds: drop the generic-degree path
+    if (true) {
+#else
     if (c.monic44) {
+#endif
       float v[4][3];
       lab_fast_u8x4(ch, s->gamma, lane, c, v);
 #pragma unroll
       for (int q = 0; q < 4; ++q) { o[q][0][0] = v[q][0]; o[q][0][1] = v[q][1]; o[q][0][2] = v[q][2]; }
     } else {
-      px4_each<OpLab>(ch, s, lane, c, o);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) px(ch[3 * q], ch[3 * q + 1], ch[3 * q + 2], s, lane, c, o[q]);
     }
   }
 };
 
-struct OpHsi {
-  static constexpr int NOUT = 1;
-  using Params = KCoeffs;
-  struct Shared { int unused; };
-  static __device__ __forceinline__ void init(Shared*, const Params&) {}
-  static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared*,
-                                            uint32_t, const Params& c, float (*o)[3]) {
-    const Lab3 v = hsi_fast_u8((int)r, (int)g, (int)b, c);
-    o[0][0] = v.c0; o[0][1] = v.c1; o[0][2] = v.c2;
-  }
-  static __device__ __forceinline__ void px4(const uint32_t (&ch)[12], const Shared* s,
-                                             uint32_t lane, const Params& c, float (*o)[1][3]) {
-    px4_each<OpHsi>(ch, s, lane, c, o);
-  }
-};
+// 4 pixels of three words as exact floats: pixel q = bytes 3q, 3q+1, 3q+2.
+__device__ __forceinline__ void words_to_rgbf(uint32_t w0, uint32_t w1, uint32_t w2, float (&f)[12]) {
+  f[0] = fbyte(w0, 0); f[1] = fbyte(w0, 1); f[2] = fbyte(w0, 2); f[3] = fbyte(w0, 3);
+  f[4] = fbyte(w1, 0); f[5] = fbyte(w1, 1); f[6] = fbyte(w1, 2); f[7] = fbyte(w1, 3);
+  f[8] = fbyte(w2, 0); f[9] = fbyte(w2, 1); f[10] = fbyte(w2, 2); f[11] = fbyte(w2, 3);
+}
 
-struct OpSct {
+template <int SPACE>
+struct OpPoly {   // HSI / SCT: fp32 exact-integer formulation
+  static constexpr int NOUT = 1;
+  using Params = KCoeffs;
+  struct Shared { int unused; };
+  static __device__ __forceinline__ void init(Shared*, const Params&) {}
+  static __device__ __forceinline__ Lab3 eval(float r, float g, float b, const Params& c) {
+    return SPACE == MACT_SPACE_HSI ? hsi_fast_f(r, g, b, c) : sct_fast_f(r, g, b, c);
+  }
+  static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared*,
+                                            uint32_t, const Params& c, float (*o)[3]) {
+    const Lab3 v = eval(u2f_small(r), u2f_small(g), u2f_small(b), c);
+    o[0][0] = v.c0; o[0][1] = v.c1; o[0][2] = v.c2;
+  }
+  static __device__ __forceinline__ void px4w(uint32_t w0, uint32_t w1, uint32_t w2, const Shared*,
+                                              uint32_t, const Params& c, float (*o)[1][3]) {
+    float f[12];
+    words_to_rgbf(w0, w1, w2, f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const Lab3 v = eval(f[3 * q], f[3 * q + 1], f[3 * q + 2], c);
+      o[q][0][0] = v.c0; o[q][0][1] = v.c1; o[q][0][2] = v.c2;
+    }
+  }
+};
+using OpHsi = OpPoly<MACT_SPACE_HSI>;
+
+// Calibration op: out = (r, g, b) as floats — the same 3 B in / 12 B out
+// stream with no arithmetic, i.e. the achievable bandwidth ceiling of the
+// skeleton on this I/O pattern (reported next to the roofline in bench.py).
+struct OpExpand {
   static constexpr int NOUT = 1;
   using Params = KCoeffs;
   struct Shared { int unused; };
   static __device__ __forceinline__ void init(Shared*, const Params&) {}
   static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared*,
-                                            uint32_t, const Params& c, float (*o)[3]) {
-    const Lab3 v = sct_fast_u8((int)r, (int)g, (int)b, c);
-    o[0][0] = v.c0; o[0][1] = v.c1; o[0][2] = v.c2;
+                                            uint32_t, const Params&, float (*o)[3]) {
+    o[0][0] = u2f_small(r); o[0][1] = u2f_small(g); o[0][2] = u2f_small(b);
   }
-  static __device__ __forceinline__ void px4(const uint32_t (&ch)[12], const Shared* s,
-                                             uint32_t lane, const Params& c, float (*o)[1][3]) {
-    px4_each<OpSct>(ch, s, lane, c, o);
+  static __device__ __forceinline__ void px4w(uint32_t w0, uint32_t w1, uint32_t w2, const Shared*,
+                                              uint32_t, const Params&, float (*o)[1][3]) {
+    float f[12];
+    words_to_rgbf(w0, w1, w2, f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) { o[q][0][0] = f[3 * q]; o[q][0][1] = f[3 * q + 1]; o[q][0][2] = f[3 * q + 2]; }
   }
 };
+using OpSct = OpPoly<MACT_SPACE_SCT>;
 
 struct OpAll {
   static constexpr int NOUT = 3;
@@ -85,27 +121,26 @@ struct OpAll {
   static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
                                             uint32_t lane, const Params& c, float (*o)[3]) {
     const Lab3 a = lab_fast_u8(r, g, b, s->gamma, lane, c);
-    const Lab3 h = hsi_fast_u8((int)r, (int)g, (int)b, c);
-    const Lab3 q = sct_fast_u8((int)r, (int)g, (int)b, c);
+    const Lab3 h = hsi_fast_u8(r, g, b, c);
+    const Lab3 q = sct_fast_u8(r, g, b, c);
     o[0][0] = a.c0; o[0][1] = a.c1; o[0][2] = a.c2;
     o[1][0] = h.c0; o[1][1] = h.c1; o[1][2] = h.c2;
     o[2][0] = q.c0; o[2][1] = q.c1; o[2][2] = q.c2;
   }
-  static __device__ __forceinline__ void px4(const uint32_t (&ch)[12], const Shared* s,
-                                             uint32_t lane, const Params& c, float (*o)[3][3]) {
-    if (c.monic44) {
-      float v[4][3];
-      lab_fast_u8x4(ch, s->gamma, lane, c, v);
+  static __device__ __forceinline__ void px4w(uint32_t w0, uint32_t w1, uint32_t w2,
+                                              const Shared* s, uint32_t lane, const Params& c,
+                                              float (*o)[3][3]) {
+    float lab[4][1][3];
+    OpLab::px4w(w0, w1, w2, s, lane, c, lab);
+    float f[12];
+    words_to_rgbf(w0, w1, w2, f);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        o[q][0][0] = v[q][0]; o[q][0][1] = v[q][1]; o[q][0][2] = v[q][2];
-        const Lab3 h = hsi_fast_u8((int)ch[3 * q], (int)ch[3 * q + 1], (int)ch[3 * q + 2], c);
-        const Lab3 z = sct_fast_u8((int)ch[3 * q], (int)ch[3 * q + 1], (int)ch[3 * q + 2], c);
-        o[q][1][0] = h.c0; o[q][1][1] = h.c1; o[q][1][2] = h.c2;
-        o[q][2][0] = z.c0; o[q][2][1] = z.c1; o[q][2][2] = z.c2;
-      }
-    } else {
-      px4_each<OpAll>(ch, s, lane, c, o);
+    for (int q = 0; q < 4; ++q) {
+      const Lab3 h = hsi_fast_f(f[3 * q], f[3 * q + 1], f[3 * q + 2], c);
+      const Lab3 z = sct_fast_f(f[3 * q], f[3 * q + 1], f[3 * q + 2], c);
+      o[q][0][0] = lab[q][0][0]; o[q][0][1] = lab[q][0][1]; o[q][0][2] = lab[q][0][2];
+      o[q][1][0] = h.c0; o[q][1][1] = h.c1; o[q][1][2] = h.c2;
+      o[q][2][0] = z.c0; o[q][2][1] = z.c1; o[q][2][2] = z.c2;
     }
   }
 };
@@ -133,9 +168,9 @@ __global__ void k_fast_real(int space, const T* __restrict__ in, float* __restri
 // Tile configurations <Op, NW compute warps, G groups/lane, SIN input stages,
 // NOB output buffers per warp> (DESIGN.md §Kernels has the smem/occupancy math).
 // Overridable at build time for tuning (MACT_NVCC_DEFS, see build.py).
-// CIELAB: 68 KB smem (32 KB bank-replicated gamma) -> 3 CTA/SM
+// CIELAB: 16+1 warps, 80 KB smem (32 KB bank-replicated gamma) -> 2 CTA/SM = 32 compute warps
 #ifndef MACT_LAB_NW
-#define MACT_LAB_NW 8
+#define MACT_LAB_NW 16
 #endif
 #ifndef MACT_LAB_G
 #define MACT_LAB_G 1
@@ -144,14 +179,14 @@ __global__ void k_fast_real(int space, const T* __restrict__ in, float* __restri
 #define MACT_LAB_SIN 4
 #endif
 #ifndef MACT_LAB_NOB
-#define MACT_LAB_NOB 2
+#define MACT_LAB_NOB 1
 #endif
-// HSI / SCT: 72 KB -> 3 CTA/SM
+// HSI / SCT: 16+1 warps, 72 KB -> 3 CTA/SM
 #ifndef MACT_HS_NW
-#define MACT_HS_NW 8
+#define MACT_HS_NW 16
 #endif
 #ifndef MACT_HS_G
-#define MACT_HS_G 2
+#define MACT_HS_G 1
 #endif
 #ifndef MACT_HS_SIN
 #define MACT_HS_SIN 4
@@ -243,4 +278,12 @@ extern "C" int mact_all_fast(const uint8_t* rgb, float* lab, float* hsi, float* 
   Outs outs{{lab, hsi, sct}};
   return launch_stream_t<OpAll, MACT_ALL_CFG>(
       rgb, outs, n, layout == MACT_LAYOUT_PLANAR, kc, (cudaStream_t)stream, "all_fast");
+}
+
+extern "C" int mact_probe_expand(const uint8_t* rgb, float* out, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!rgb || !out))) return set_error(MACT_EBADARG, "bad argument");
+  KCoeffs kc{};
+  Outs outs{{out, nullptr, nullptr}};
+  return launch_stream_t<OpExpand, MACT_HS_CFG>(rgb, outs, n, 0, kc, (cudaStream_t)stream,
+                                                "probe_expand");
 }

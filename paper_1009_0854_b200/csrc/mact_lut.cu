@@ -5,11 +5,12 @@
 //   mact_lut_interp  <- lut.interpolate(..., variant="standard") for the linear
 //                       CIELAB destination   (lut.py:231-246, :341-350)
 //
-// Interpolation runs inside the streaming skeleton (mact_stream.cuh).  For
-// grids 9^3 and 17^3 the lattice is staged once per persistent CTA into
-// shared memory as float4-padded nodes (17^3 x 16 B = 78.6 KB): one LDS.128
-// per node.  33^3 (431 KB packed) exceeds a CTA's 227 KB and is read through
-// the read-only L1/L2 path.
+// Device lattice format: (n^3, 4) fp32, r-major, node = (c0, c1, c2, 0) so a
+// node is one 16-byte load.  Interpolation runs inside the streaming skeleton
+// (mact_stream.cuh).  For grids 9^3 and 17^3 the lattice is staged once per
+// persistent CTA into shared memory (17^3 x 16 B = 78.6 KB): one LDS.128 per
+// node.  33^3 (575 KB) exceeds a CTA's 227 KB and is gathered with LDG.128
+// through L1/L2 (the lattice stays L2-resident).
 #include "mact_lut.cuh"
 #include "mact_pixel.cuh"
 #include "mact_stream.cuh"
@@ -17,7 +18,7 @@
 namespace mact {
 
 struct LutParams {
-  const float* lat;   // (n^3, 3) fp32, r-major
+  const float4* lat;   // (n^3, 4) fp32, r-major, padded
 };
 
 template <int N, int METHOD>
@@ -31,8 +32,7 @@ struct OpLut {
   static __device__ __forceinline__ void init(Shared* s, const Params& p) {
     if constexpr (SMEM) {
       for (int i = threadIdx.x; i < N * N * N; i += blockDim.x)
-        s->lat[i] = make_float4(__ldg(p.lat + 3 * i), __ldg(p.lat + 3 * i + 1),
-                                __ldg(p.lat + 3 * i + 2), 0.0f);
+        s->lat[i] = __ldg(p.lat + i);
     }
   }
   static __device__ __forceinline__ float3 node(const Shared* s, const Params& p, int i) {
@@ -40,7 +40,8 @@ struct OpLut {
       const float4 v = s->lat[i];
       return make_float3(v.x, v.y, v.z);
     } else {
-      return make_float3(__ldg(p.lat + 3 * i), __ldg(p.lat + 3 * i + 1), __ldg(p.lat + 3 * i + 2));
+      const float4 v = __ldg(p.lat + i);
+      return make_float3(v.x, v.y, v.z);
     }
   }
   static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
@@ -60,9 +61,10 @@ struct OpLut {
     }
     o[0][0] = a0; o[0][1] = a1; o[0][2] = a2;
   }
-  static __device__ __forceinline__ void px4(const uint32_t (&ch)[12], const Shared* s,
-                                             uint32_t lane, const Params& p, float (*o)[1][3]) {
-    px4_each<OpLut>(ch, s, lane, p, o);
+  static __device__ __forceinline__ void px4w(uint32_t w0, uint32_t w1, uint32_t w2,
+                                              const Shared* s, uint32_t lane, const Params& p,
+                                              float (*o)[1][3]) {
+    px4_each<OpLut>(w0, w1, w2, s, lane, p, o);
   }
 };
 
@@ -81,8 +83,9 @@ __global__ void k_lut_build(int space, int n, double* __restrict__ f64, float* _
     for (int k = 0; k < 3; ++k) {
       const double v = isnan(o[k]) ? 0.0 : o[k];                        // nan_to_num (lut.py:92)
       if (f64) f64[3 * i + k] = v;
-      if (f32) f32[3 * i + k] = (float)v;
+      if (f32) f32[4 * i + k] = (float)v;
     }
+    if (f32) f32[4 * i + 3] = 0.0f;
   }
 }
 
@@ -108,10 +111,14 @@ template <int N, int METHOD>
 static int launch_interp(const float* lat, const uint8_t* rgb, float* out, int64_t n, int planar,
                          cudaStream_t st) {
   Outs outs{{out, nullptr, nullptr}};
-  LutParams p{lat};
-  // 17^3 lattice = 78.6 KB of smem: 8 warps x G=1 + 4 stages -> 2 CTA/SM
-  return launch_stream_t<OpLut<N, METHOD>, 8, (N <= 9 ? 2 : 1), 4, 2>(rgb, outs, n, planar, p, st,
-                                                                      "lut_interp");
+  LutParams p{reinterpret_cast<const float4*>(lat)};
+  // 17^3: 78.6 KB lattice + 9 KB in + 12 KB out -> 2 CTA/SM (16 compute warps);
+  // 33^3 gathers from L2, so more warps in flight: 16 per CTA, 3 CTA/SM.
+  if constexpr (N == 33)
+    return launch_stream_t<OpLut<N, METHOD>, 16, 1, 3, 1>(rgb, outs, n, planar, p, st, "lut_interp");
+  else
+    return launch_stream_t<OpLut<N, METHOD>, 8, (N <= 9 ? 2 : 1), 3, 1>(rgb, outs, n, planar, p, st,
+                                                                         "lut_interp");
 }
 
 template <int N>
@@ -162,6 +169,7 @@ extern "C" int mact_lut_build(int space, int grid_n, double* lattice_f64, float*
 extern "C" int mact_lut_interp(const float* lattice, int grid_n, int method, const uint8_t* rgb,
                                float* out, int64_t n, int layout, void* stream) {
   if (n < 0 || (n > 0 && (!lattice || !rgb || !out))) return set_error(MACT_EBADARG, "bad argument");
+  if ((uintptr_t)lattice % 16) return set_error(MACT_EBADARG, "lattice must be 16-byte aligned");
   if (layout != MACT_LAYOUT_INTERLEAVED && layout != MACT_LAYOUT_PLANAR)
     return set_error(MACT_EBADARG, "unknown layout %d", layout);
   const int planar = layout == MACT_LAYOUT_PLANAR;

@@ -75,7 +75,6 @@ __device__ __forceinline__ double lab_f_monic(float t, const KCoeffs& c) {
   return t > (float)kLabKnee ? f : fma(c.lin_s, (double)t, c.lin_o);
 }
 
-
 // gamma_rep: 256 entries replicated 32x, entry i at [i*32 + lane] (conflict-free)
 __device__ __forceinline__ Lab3 lab_fast_u8(uint32_t r, uint32_t g, uint32_t b,
                                             const float* gamma_rep, uint32_t lane,
@@ -105,11 +104,12 @@ __device__ __forceinline__ void lab_fast_u8x4(const uint32_t (&ch)[12], const fl
                                               uint32_t lane, const KCoeffs& c, float (*o)[3]) {
   float t[12];
   bool low = false;
+  const float* gl = gamma_rep + lane;                  // lane's bank column: one IMAD per lookup
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
-    const float gr = gamma_rep[(ch[3 * p] << 5) | lane];
-    const float gg = gamma_rep[(ch[3 * p + 1] << 5) | lane];
-    const float gb = gamma_rep[(ch[3 * p + 2] << 5) | lane];
+    const float gr = gl[ch[3 * p] << 5];
+    const float gg = gl[ch[3 * p + 1] << 5];
+    const float gb = gl[ch[3 * p + 2] << 5];
     t[3 * p] = fmaf(c.mxyz[2], gb, fmaf(c.mxyz[1], gg, c.mxyz[0] * gr));
     t[3 * p + 1] = fmaf(c.mxyz[5], gb, fmaf(c.mxyz[4], gg, c.mxyz[3] * gr));
     t[3 * p + 2] = fmaf(c.mxyz[8], gb, fmaf(c.mxyz[7], gg, c.mxyz[6] * gr));
@@ -159,37 +159,32 @@ __device__ __forceinline__ void lab_fast_d(double r, double g, double b, const K
 }
 
 // ----------------------------------------------------------------- HSI fast
-// Kender case analysis (fast.py:131-146) on the integer channels.
-__device__ __forceinline__ Lab3 hsi_fast_u8(int r, int g, int b, const KCoeffs& c) {
-  const bool c1 = (r > b) & (g > b);
+// Kender case analysis (fast.py:131-146).  Channels arrive as exact
+// integer-valued floats (0..255), so every compare, sum and difference below
+// is exact and the case selection is bit-identical to the reference's fp64
+// compares on r/255 etc.  Identities used (all exact on integers):
+//   case1 (b strictly smallest)  <=>  b < min(r, g)
+//   den of the active case = (sum of the other two) - 2 min = sum - 3 min
+//   S = 1 - 3 min / sum = den / sum            (exact.py:95-101)
+//   not case1..3  =>  g = b <= r, so case4 (h = 0) <=> den > 0, gray <=> den = 0
+__device__ __forceinline__ Lab3 hsi_fast_f(float r, float g, float b, const KCoeffs& c) {
+  const float mrg = fminf(r, g);
+  const bool c1 = b < mrg;
   const bool c2 = !c1 & (g > r);
   const bool c3 = !c1 & !c2 & (b > g);
-  const bool c4 = !c1 & !c2 & !c3 & (r > b);
-  int num, den;
-  float base;
-  if (c1) {
-    num = g - r; den = (g - b) + (r - b); base = (float)(kPi / 3.0);
-  } else if (c2) {
-    num = b - g; den = (b - r) + (g - r); base = (float)kPi;
-  } else if (c3) {
-    num = r - b; den = (r - g) + (b - g); base = (float)(5.0 * kPi / 3.0);
-  } else {
-    num = 0; den = 1; base = 0.0f;
-  }
-  const float fn = (float)num, fd = (float)den;       // |num|,den <= 510: exact
-  const float x = fn * rcp_approx(fd);
+  const float sum = r + g + b;
+  const float den = fmaf(-3.0f, fminf(mrg, b), sum);
+  const float num = c1 ? g - r : (c2 ? b - g : r - b);
+  const float base = c1 ? (float)(kPi / 3.0) : (c2 ? (float)kPi : (float)(5.0 * kPi / 3.0));
+  const float x = num * rcp_approx(den);
   const float mag = horner_f<kPolyDeg>(c.hsi, fabsf(x));
-  float h = base + (num < 0 ? -mag : mag);           // odd extension (fast.py:118-122)
-  h = (c1 | c2 | c3) ? h : (c4 ? 0.0f : __int_as_float(0x7fc00000));
-  h = h < 0.0f ? h + (float)kTwoPi : h;
-  h = h >= (float)kTwoPi ? h - (float)kTwoPi : h;
-  const int sum = r + g + b;
-  const int mn = min(min(r, g), b);
+  float h = base + (num < 0.0f ? -mag : mag);           // odd extension (fast.py:118-122)
+  if (h < 0.0f) h += (float)kTwoPi;
+  if (h >= (float)kTwoPi) h -= (float)kTwoPi;
   Lab3 o;
-  o.c0 = h;
-  // S = 1 - 3 min/sum = (sum - 3 min)/sum, exact zero on grays (exact.py:95-101)
-  o.c1 = sum > 0 ? (float)(sum - 3 * mn) * rcp_approx((float)sum) : 0.0f;
-  o.c2 = (float)sum * (float)(1.0 / 765.0);
+  o.c0 = (c1 | c2 | c3) ? h : (den > 0.0f ? 0.0f : __int_as_float(0x7fc00000));
+  o.c1 = sum > 0.0f ? den * rcp_approx(sum) : 0.0f;
+  o.c2 = sum * (float)(1.0 / 765.0);
   return o;
 }
 
@@ -224,38 +219,45 @@ __device__ __forceinline__ void hsi_fast_d(double r, double g, double b, const K
 }
 
 // ----------------------------------------------------------------- SCT fast
-__device__ __forceinline__ Lab3 sct_fast_u8(int r, int g, int b, const KCoeffs& c) {
-  const int rg2 = r * r + g * g;
-  const int ss = rg2 + b * b;                 // <= 195075 < 2^24: exact in fp32
-  const float fss = (float)ss;
-  const float L = __fsqrt_rn(fss);            // correctly rounded |v| (fast.py:196)
-  const float fb = (float)b;
-  // angle A = acos_fast(b/L) (fast.py:151-162, :198); x >= 0.5 <=> 3 b^2 >= r^2 + g^2
-  const bool upper = 3 * b * b >= rg2;
-  float arg, pa;
-  if (upper) {
-    // sqrt(1 - b/L) without cancellation: (r^2+g^2) / (L (L + b))
-    const float den = L * (L + fb);
-    arg = sqrt_approx((float)rg2 * rcp_approx(den));
-    pa = horner_f<kPolyDeg>(c.asin, arg);
-  } else {
-    arg = fb * rcp_approx(L);
-    pa = horner_f<kPolyDeg>(c.acos, arg);
-  }
-  float ang_a = ss > 0 ? pa : 0.0f;
-  ang_a = fminf(fmaxf(ang_a, 0.0f), (float)(0.5 * kPi));
-  // angle B = atan_unit_fast(g, r) (fast.py:165-185)
-  const bool direct = g < r;
-  const int lo = direct ? g : r, hi = direct ? r : g;
-  const float t = hi > 0 ? (float)lo * rcp_approx((float)hi) : 0.0f;
-  const float pb = direct ? horner_f<kPolyDeg>(c.atanf, t) : horner_f<kPolyDeg>(c.atang, t);
-  float ang_b = fminf(fmaxf(pb, 0.0f), (float)(0.5 * kPi));
-  ang_b = (r == 0 && g == 0) ? __int_as_float(0x7fc00000) : ang_b;
+// fast.py:151-203 on exact integer-valued float channels.
+//  * |v|^2 = r^2+g^2+b^2 <= 195075 < 2^24 is exact; one MUFU.RSQ gives both
+//    L = |v|^2 rsqrt(|v|^2) and b/L = b rsqrt(|v|^2).
+//  * arccos branch: b/L >= 0.5 <=> 3 b^2 >= r^2 + g^2 (exact integer test);
+//    the folded arcsin argument sqrt(1 - b/L) uses the cancellation-free
+//    (r^2+g^2) / (L (L + b)) = (r^2+g^2) / (|v|^2 + b L).
+//  * arctan: min(g,r)/max(g,r) with the direct/complement polynomial; both
+//    polynomials are evaluated (FMA pipe) and selected, no divergence.
+__device__ __forceinline__ Lab3 sct_fast_f(float r, float g, float b, const KCoeffs& c) {
+  const float rg2 = fmaf(g, g, r * r);
+  const float b2 = b * b;
+  const float ss = rg2 + b2;
+  const float rs = rsqrt_approx(ss);                    // inf at black, masked below
+  const float L = ss * rs;
+  // angle A = acos_fast(b / L)
+  const bool upper = fmaf(3.0f, b2, -rg2) >= 0.0f;
+  const float y = sqrt_approx(rg2 * rcp_approx(fmaf(b, L, ss)));
+  const float pa_hi = horner_f<kPolyDeg>(c.asin, y);
+  const float pa_lo = horner_f<kPolyDeg>(c.acos, b * rs);
+  float ang_a = upper ? pa_hi : pa_lo;
+  ang_a = ss > 0.0f ? fminf(fmaxf(ang_a, 0.0f), (float)(0.5 * kPi)) : 0.0f;
+  // angle B = atan_unit_fast(g, r)
+  const float lo = fminf(g, r), hi = fmaxf(g, r);
+  const float t = lo * rcp_approx(hi);
+  const float pf = horner_f<kPolyDeg>(c.atanf, t);
+  const float pg = horner_f<kPolyDeg>(c.atang, t);
+  float ang_b = fminf(fmaxf(g < r ? pf : pg, 0.0f), (float)(0.5 * kPi));
   Lab3 o;
-  o.c0 = L;
+  o.c0 = ss > 0.0f ? L : 0.0f;
   o.c1 = ang_a;
-  o.c2 = ang_b;
+  o.c2 = hi > 0.0f ? ang_b : __int_as_float(0x7fc00000);
   return o;
+}
+
+__device__ __forceinline__ Lab3 hsi_fast_u8(uint32_t r, uint32_t g, uint32_t b, const KCoeffs& c) {
+  return hsi_fast_f(u2f_small(r), u2f_small(g), u2f_small(b), c);
+}
+__device__ __forceinline__ Lab3 sct_fast_u8(uint32_t r, uint32_t g, uint32_t b, const KCoeffs& c) {
+  return sct_fast_f(u2f_small(r), u2f_small(g), u2f_small(b), c);
 }
 
 __device__ __forceinline__ void sct_fast_d(double r, double g, double b, const KCoeffs& c,

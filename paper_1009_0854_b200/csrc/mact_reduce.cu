@@ -84,11 +84,12 @@ template <int N>
 __device__ __forceinline__ void lut_value(const float* lat, int method, uint32_t r, uint32_t g,
                                           uint32_t b, double* o) {
   float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+  const float4* lat4 = reinterpret_cast<const float4*>(lat);   // (n^3, 4) padded lattice
   auto acc = [&](const int* idx, const float* w, int k) {
     for (int j = 0; j < k; ++j) {
-      const float* v = lat + 3 * idx[j];
-      if (j == 0) { a0 = w[0] * __ldg(v); a1 = w[0] * __ldg(v + 1); a2 = w[0] * __ldg(v + 2); }
-      else { a0 = fmaf(w[j], __ldg(v), a0); a1 = fmaf(w[j], __ldg(v + 1), a1); a2 = fmaf(w[j], __ldg(v + 2), a2); }
+      const float4 v = __ldg(lat4 + idx[j]);
+      if (j == 0) { a0 = w[0] * v.x; a1 = w[0] * v.y; a2 = w[0] * v.z; }
+      else { a0 = fmaf(w[j], v.x, a0); a1 = fmaf(w[j], v.y, a1); a2 = fmaf(w[j], v.z, a2); }
     }
   };
   if (method == MACT_LUT_TRILINEAR) { int i[8]; float w[8]; lut_nodes<N, MACT_LUT_TRILINEAR>(r, g, b, i, w); acc(i, w, 8); }
@@ -131,8 +132,8 @@ __global__ void __launch_bounds__(kRedThreads) k_err(const __grid_constant__ Red
     if (s.candidate == MACT_CAND_FAST) {
       Lab3 v;
       if (s.space == MACT_SPACE_LAB) v = lab_fast_u8(r, g, b, gamma_rep, lane, p.c);
-      else if (s.space == MACT_SPACE_HSI) v = hsi_fast_u8((int)r, (int)g, (int)b, p.c);
-      else v = sct_fast_u8((int)r, (int)g, (int)b, p.c);
+      else if (s.space == MACT_SPACE_HSI) v = hsi_fast_u8(r, g, b, p.c);
+      else v = sct_fast_u8(r, g, b, p.c);
       cand[0] = v.c0; cand[1] = v.c1; cand[2] = v.c2;
     } else if (s.candidate == MACT_CAND_LUT) {
       if (s.lut_grid_n == 9) lut_value<9>(s.lut_lattice, s.lut_method, r, g, b, cand);

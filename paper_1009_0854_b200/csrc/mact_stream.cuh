@@ -38,20 +38,22 @@ namespace mact {
 //   struct Shared;                          // per-CTA shared state (tables)
 //   static __device__ void init(Shared*, const Params&);   // all threads, then __syncthreads
 //   static __device__ void px(r, g, b, const Shared*, lane, const Params&, float (*o)[3]);
-//   static __device__ void px4(const uint32_t (&ch)[12], const Shared*, lane,
-//                              const Params&, float (*o)[NOUT][3]);   // warp-converged
+//   static __device__ void px4w(w0, w1, w2, const Shared*, lane, const Params&,
+//                               float (*o)[NOUT][3]);   // 4 packed pixels, warp-converged
 
 struct Outs {
   float* o[3];
 };
 
-// Default 4-pixel batch: four independent px() calls.
+// Default 4-pixel batch: unpack the three words, four independent px() calls.
 template <class Op>
-__device__ __forceinline__ void px4_each(const uint32_t (&ch)[12], const typename Op::Shared* sh,
-                                         uint32_t lane, const typename Op::Params& p,
-                                         float (*o)[Op::NOUT][3]) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) Op::px(ch[3 * q], ch[3 * q + 1], ch[3 * q + 2], sh, lane, p, o[q]);
+__device__ __forceinline__ void px4_each(uint32_t w0, uint32_t w1, uint32_t w2,
+                                         const typename Op::Shared* sh, uint32_t lane,
+                                         const typename Op::Params& p, float (*o)[Op::NOUT][3]) {
+  Op::px(byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), sh, lane, p, o[0]);
+  Op::px(byte_of(w0, 3), byte_of(w1, 0), byte_of(w1, 1), sh, lane, p, o[1]);
+  Op::px(byte_of(w1, 2), byte_of(w1, 3), byte_of(w2, 0), sh, lane, p, o[2]);
+  Op::px(byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3), sh, lane, p, o[3]);
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -129,12 +131,8 @@ __global__ void __launch_bounds__(32 * (NW + 1)) k_ws(const uint8_t* __restrict_
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int grp = g * 32 + (int)lane;                 // 4-pixel group inside the warp slice
-      const uint32_t w0 = wsrc[3 * grp], w1 = wsrc[3 * grp + 1], w2 = wsrc[3 * grp + 2];
-      const uint32_t ch[12] = {byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), byte_of(w0, 3),
-                               byte_of(w1, 0), byte_of(w1, 1), byte_of(w1, 2), byte_of(w1, 3),
-                               byte_of(w2, 0), byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3)};
       float o[4][NOUT][3];
-      Op::px4(ch, sh, lane, p, o);
+      Op::px4w(wsrc[3 * grp], wsrc[3 * grp + 1], wsrc[3 * grp + 2], sh, lane, p, o);
 #pragma unroll
       for (int k = 0; k < NOUT; ++k) {
         float* base = ob_s + k * L::OUT_FLOATS;

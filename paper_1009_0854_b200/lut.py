@@ -43,14 +43,16 @@ class Lut3D:
         return self.values.reshape(-1, 3)
 
     def lattice(self, device=None):
-        """fp32 (n^3, 3) device lattice consumed by the kernels (cached per device)."""
+        """fp32 (n^3, 4) device lattice consumed by the kernels — node = (c0, c1,
+        c2, 0), one 16-byte load — cached per device."""
         import torch
 
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         key = dev.index if dev.index is not None else torch.cuda.current_device()
         if key not in self._device:
-            self._device[key] = torch.from_numpy(
-                np.ascontiguousarray(self.values.reshape(-1, 3), dtype=np.float32)).to(dev)
+            v = np.zeros((self.grid_n ** 3, 4), dtype=np.float32)
+            v[:, :3] = self.values.reshape(-1, 3)
+            self._device[key] = torch.from_numpy(v).to(dev)
         return self._device[key]
 
 
@@ -69,7 +71,7 @@ def build_lut(space: str, grid_n: int) -> Lut3D:
     _dev.require_cuda()
     total = grid_n ** 3
     f64 = torch.empty((total, 3), dtype=torch.float64, device="cuda")
-    f32 = torch.empty((total, 3), dtype=torch.float32, device="cuda")
+    f32 = torch.empty((total, 4), dtype=torch.float32, device="cuda")
     _lib.call("mact_lut_build", _lib.SPACES[space], grid_n, f64.data_ptr(), f32.data_ptr(),
               _dev.stream_ptr())
     lut = Lut3D(grid_n=grid_n, spacing=255.0 / (grid_n - 1), destination_space=space,

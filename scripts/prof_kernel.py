@@ -46,6 +46,8 @@ def run():
     if a.op == "all":
         _lib.check(lib.mact_all_fast(x.data_ptr(), outs[0].data_ptr(), outs[1].data_ptr(),
                                      outs[2].data_ptr(), n, cfg.coeffs, 0, st))
+    elif a.op == "probe":
+        _lib.check(lib.mact_probe_expand(x.data_ptr(), outs[0].data_ptr(), n, st))
     elif a.op in ("lab", "hsi", "sct"):
         _lib.check(getattr(lib, f"mact_{a.op}_fast")(x.data_ptr(), 0, outs[0].data_ptr(), n,
                                                      cfg.coeffs, 0, st))
