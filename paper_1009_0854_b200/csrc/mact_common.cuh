@@ -43,14 +43,17 @@ struct KCoeffs {
   float hsi[kPolyDeg + 1], asin[kPolyDeg + 1], acos[kPolyDeg + 1], atanf[kPolyDeg + 1],
       atang[kPolyDeg + 1];
   float mxyz[9];   // RGB->XYZ rows pre-divided by the white point (fp32)
-  // Monic form of a degree-(4,4) rational, used by the batched CIELAB path:
-  // P = p4 (t^4 + pm3 t^3 + ... + pm0), Q = q4 (t^4 + qm3 t^3 + ...),
-  // f = k P'/Q' with k = p4/q4 folded into the output constants.  The first
-  // Horner step becomes t + c3 (no constant pair to stage in registers).
+  // Degree-(4,4) fast path.  With P' = P/p4, Q' = Q/q4 (monic) and k = p4/q4,
+  //   f = P/Q = k P'/Q' = k (1 + (P' - Q')/Q') = k + s q,   q = D'(t)/Q'(t),
+  // where D' is the monic cubic (P' - Q')/e3 and s = k e3.  One fp64 Horner
+  // step fewer than evaluating P' (the t^4 terms cancel), and the constant k
+  // disappears into the CIELAB epilogue:
+  //   L* = 116 s qy + (116 k - 16),  a* = 500 s (qx - qy),  b* = 200 s (qy - qz).
   int32_t monic44;                  // 1 when the configuration is (4,4)
-  double pm[4], qm[4];
-  double lin_s, lin_o;              // linear branch / k
-  double out_l, out_a, out_b;       // 116 k, 500 k, 200 k
+  double qm[4], dm[3];              // Q' = t^4 + qm3 t^3 + ...,  D' = t^3 + dm2 t^2 + ...
+  double lin_s, lin_o;              // linear branch expressed in q: q = lin_s t + lin_o
+  double l_s, l_o;                  // 116 s, 116 k - 16
+  float a_s, b_s;                   // 500 s, 200 s
 };
 
 // ---------------------------------------------------------------- Horner

@@ -168,31 +168,44 @@ __global__ void k_fast_real(int space, const T* __restrict__ in, float* __restri
 // Tile configurations <Op, NW compute warps, G groups/lane, SIN input stages,
 // NOB output buffers per warp> (DESIGN.md §Kernels has the smem/occupancy math).
 // Overridable at build time for tuning (MACT_NVCC_DEFS, see build.py).
-// CIELAB: 16+1 warps, 80 KB smem (32 KB bank-replicated gamma) -> 2 CTA/SM = 32 compute warps
+// CIELAB: 16+1 warps, G=4, 2 stages: 176 KB smem (32 KB bank-replicated gamma) -> 1 CTA/SM (R01 sweep: 250 Gpix/s)
 #ifndef MACT_LAB_NW
 #define MACT_LAB_NW 16
 #endif
 #ifndef MACT_LAB_G
-#define MACT_LAB_G 1
+#define MACT_LAB_G 4
 #endif
 #ifndef MACT_LAB_SIN
-#define MACT_LAB_SIN 4
+#define MACT_LAB_SIN 2
 #endif
 #ifndef MACT_LAB_NOB
 #define MACT_LAB_NOB 1
 #endif
-// HSI / SCT: 16+1 warps, 72 KB -> 3 CTA/SM
-#ifndef MACT_HS_NW
-#define MACT_HS_NW 16
+// HSI: 16+1 warps, G=4, 2 stages: 144 KB -> 1 CTA/SM (R01 sweep: 406 Gpix/s)
+#ifndef MACT_HSI_NW
+#define MACT_HSI_NW 16
 #endif
-#ifndef MACT_HS_G
-#define MACT_HS_G 1
+#ifndef MACT_HSI_G
+#define MACT_HSI_G 4
 #endif
-#ifndef MACT_HS_SIN
-#define MACT_HS_SIN 4
+#ifndef MACT_HSI_SIN
+#define MACT_HSI_SIN 2
 #endif
-#ifndef MACT_HS_NOB
-#define MACT_HS_NOB 2
+#ifndef MACT_HSI_NOB
+#define MACT_HSI_NOB 1
+#endif
+// SCT: 16+1 warps, G=2, 4 stages: 144 KB -> 1 CTA/SM (R01 sweep: 412 Gpix/s)
+#ifndef MACT_SCT_NW
+#define MACT_SCT_NW 16
+#endif
+#ifndef MACT_SCT_G
+#define MACT_SCT_G 2
+#endif
+#ifndef MACT_SCT_SIN
+#define MACT_SCT_SIN 4
+#endif
+#ifndef MACT_SCT_NOB
+#define MACT_SCT_NOB 2
 #endif
 // fused triple: 77 KB -> 2 CTA/SM
 #ifndef MACT_ALL_NW
@@ -208,7 +221,8 @@ __global__ void k_fast_real(int space, const T* __restrict__ in, float* __restri
 #define MACT_ALL_NOB 1
 #endif
 #define MACT_LAB_CFG MACT_LAB_NW, MACT_LAB_G, MACT_LAB_SIN, MACT_LAB_NOB
-#define MACT_HS_CFG MACT_HS_NW, MACT_HS_G, MACT_HS_SIN, MACT_HS_NOB
+#define MACT_HSI_CFG MACT_HSI_NW, MACT_HSI_G, MACT_HSI_SIN, MACT_HSI_NOB
+#define MACT_SCT_CFG MACT_SCT_NW, MACT_SCT_G, MACT_SCT_SIN, MACT_SCT_NOB
 #define MACT_ALL_CFG MACT_ALL_NW, MACT_ALL_G, MACT_ALL_SIN, MACT_ALL_NOB
 
 template <typename T>
@@ -240,8 +254,8 @@ static int fast_entry(int space, const void* rgb, int in_dtype, float* out, int6
       if (space == MACT_SPACE_LAB)
         return launch_stream_t<OpLab, MACT_LAB_CFG>(in, outs, n, planar, kc, st, "lab_fast");
       if (space == MACT_SPACE_HSI)
-        return launch_stream_t<OpHsi, MACT_HS_CFG>(in, outs, n, planar, kc, st, "hsi_fast");
-      return launch_stream_t<OpSct, MACT_HS_CFG>(in, outs, n, planar, kc, st, "sct_fast");
+        return launch_stream_t<OpHsi, MACT_HSI_CFG>(in, outs, n, planar, kc, st, "hsi_fast");
+      return launch_stream_t<OpSct, MACT_SCT_CFG>(in, outs, n, planar, kc, st, "sct_fast");
     case MACT_DTYPE_F32:
       return launch_real<float>(space, (const float*)rgb, out, n, planar, kc, st);
     case MACT_DTYPE_F64:
@@ -284,6 +298,6 @@ extern "C" int mact_probe_expand(const uint8_t* rgb, float* out, int64_t n, void
   if (n < 0 || (n > 0 && (!rgb || !out))) return set_error(MACT_EBADARG, "bad argument");
   KCoeffs kc{};
   Outs outs{{out, nullptr, nullptr}};
-  return launch_stream_t<OpExpand, MACT_HS_CFG>(rgb, outs, n, 0, kc, (cudaStream_t)stream,
+  return launch_stream_t<OpExpand, MACT_HSI_CFG>(rgb, outs, n, 0, kc, (cudaStream_t)stream,
                                                 "probe_expand");
 }

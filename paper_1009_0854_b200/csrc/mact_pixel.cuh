@@ -66,13 +66,28 @@ __device__ __forceinline__ double monic4(const double* cm, double t) {
   acc = fma(acc, t, cm[1]);
   return fma(acc, t, cm[0]);
 }
-__device__ __forceinline__ double lab_f_monic(float t, const KCoeffs& c) {
-  const double td = f2d_pos(t);
-  const double P = monic4(c.pm, td), Q = monic4(c.qm, td);
+__device__ __forceinline__ double monic3(const double* cm, double t) {
+  double acc = t + cm[2];
+  acc = fma(acc, t, cm[1]);
+  return fma(acc, t, cm[0]);
+}
+// q = D'(t)/Q'(t): MUFU.RCP64H seed + one fp64 Newton correction of the quotient.
+__device__ __forceinline__ double lab_q(double td, const KCoeffs& c) {
+  const double D = monic3(c.dm, td), Q = monic4(c.qm, td);
   const double y0 = rcp_approx_d(Q);
-  const double q0 = P * y0;
-  const double f = fma(fma(-q0, Q, P), y0, q0);
-  return t > (float)kLabKnee ? f : fma(c.lin_s, (double)t, c.lin_o);
+  const double q0 = D * y0;
+  return fma(fma(-q0, Q, D), y0, q0);
+}
+__device__ __forceinline__ double lab_q_sel(float t, const KCoeffs& c) {
+  return t > (float)kLabKnee ? lab_q(f2d_pos(t), c) : fma(c.lin_s, (double)t, c.lin_o);
+}
+// CIELAB epilogue from the three q's: L* in fp64 (its two terms nearly cancel),
+// a*, b* from an fp64 difference rounded once to fp32.
+__device__ __forceinline__ void lab_from_q(double qx, double qy, double qz, const KCoeffs& c,
+                                           float& L, float& A, float& B) {
+  L = (float)fma(c.l_s, qy, c.l_o);
+  A = c.a_s * (float)(qx - qy);
+  B = c.b_s * (float)(qy - qz);
 }
 
 // gamma_rep: 256 entries replicated 32x, entry i at [i*32 + lane] (conflict-free)
@@ -87,10 +102,7 @@ __device__ __forceinline__ Lab3 lab_fast_u8(uint32_t r, uint32_t g, uint32_t b,
   const float tz = fmaf(c.mxyz[8], gb, fmaf(c.mxyz[7], gg, c.mxyz[6] * gr));
   Lab3 o;
   if (c.monic44) {   // same arithmetic as lab_fast_u8x4 (bit-identical tile/tail paths)
-    const double fx = lab_f_monic(tx, c), fy = lab_f_monic(ty, c), fz = lab_f_monic(tz, c);
-    o.c0 = (float)fma(c.out_l, fy, -16.0);
-    o.c1 = (float)(c.out_a * (fx - fy));
-    o.c2 = (float)(c.out_b * (fy - fz));
+    lab_from_q(lab_q_sel(tx, c), lab_q_sel(ty, c), lab_q_sel(tz, c), c, o.c0, o.c1, o.c2);
     return o;
   }
   const double fx = lab_f_fast(tx, c), fy = lab_f_fast(ty, c), fz = lab_f_fast(tz, c);
@@ -114,27 +126,19 @@ __device__ __forceinline__ void lab_fast_u8x4(const uint32_t (&ch)[12], const fl
     t[3 * p + 1] = fmaf(c.mxyz[5], gb, fmaf(c.mxyz[4], gg, c.mxyz[3] * gr));
     t[3 * p + 2] = fmaf(c.mxyz[8], gb, fmaf(c.mxyz[7], gg, c.mxyz[6] * gr));
   }
-  double f[12];
 #pragma unroll
-  for (int j = 0; j < 12; ++j) {
-    low |= !(t[j] > (float)kLabKnee);
-    const double td = f2d_pos(t[j]);
-    const double P = monic4(c.pm, td), Q = monic4(c.qm, td);
-    const double y0 = rcp_approx_d(Q);
-    const double q0 = P * y0;
-    f[j] = fma(fma(-q0, Q, P), y0, q0);
-  }
+  for (int j = 0; j < 12; ++j) low |= !(t[j] > (float)kLabKnee);
+  double q[12];
+#pragma unroll
+  for (int j = 0; j < 12; ++j) q[j] = lab_q(f2d_pos(t[j]), c);
   if (__any_sync(0xffffffffu, low)) {
 #pragma unroll
     for (int j = 0; j < 12; ++j)
-      if (!(t[j] > (float)kLabKnee)) f[j] = fma(c.lin_s, (double)t[j], c.lin_o);
+      if (!(t[j] > (float)kLabKnee)) q[j] = fma(c.lin_s, (double)t[j], c.lin_o);
   }
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    o[p][0] = (float)fma(c.out_l, f[3 * p + 1], -16.0);
-    o[p][1] = (float)(c.out_a * (f[3 * p] - f[3 * p + 1]));
-    o[p][2] = (float)(c.out_b * (f[3 * p + 1] - f[3 * p + 2]));
-  }
+  for (int p = 0; p < 4; ++p)
+    lab_from_q(q[3 * p], q[3 * p + 1], q[3 * p + 2], c, o[p][0], o[p][1], o[p][2]);
 }
 
 // Reference-faithful fp64 evaluation on real-valued channels (float input

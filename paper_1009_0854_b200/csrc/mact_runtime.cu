@@ -120,15 +120,24 @@ int make_kcoeffs(const MactCoeffs* c, KCoeffs* k) {
                 c->cbrt_den[4] != 0.0) ? 1 : 0;
   if (k->monic44) {
     const double p4 = c->cbrt_num[4], q4 = c->cbrt_den[4], kk = p4 / q4;
+    double pm[4];
     for (int i = 0; i < 4; ++i) {
-      k->pm[i] = c->cbrt_num[i] / p4;
+      pm[i] = c->cbrt_num[i] / p4;
       k->qm[i] = c->cbrt_den[i] / q4;
     }
-    k->lin_s = kLabSlope / kk;
-    k->lin_o = kLabOffset / kk;
-    k->out_l = 116.0 * kk;
-    k->out_a = 500.0 * kk;
-    k->out_b = 200.0 * kk;
+    const double e3 = pm[3] - k->qm[3];          // leading coefficient of P' - Q'
+    if (e3 == 0.0) {
+      k->monic44 = 0;
+    } else {
+      for (int i = 0; i < 3; ++i) k->dm[i] = (pm[i] - k->qm[i]) / e3;
+      const double sc = kk * e3;
+      k->lin_s = kLabSlope / sc;
+      k->lin_o = (kLabOffset - kk) / sc;
+      k->l_s = 116.0 * sc;
+      k->l_o = 116.0 * kk - 16.0;
+      k->a_s = (float)(500.0 * sc);
+      k->b_s = (float)(200.0 * sc);
+    }
   }
   return MACT_OK;
 }

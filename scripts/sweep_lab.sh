@@ -1,2 +1,2 @@
 #!/bin/bash
-for lib in paper_1009_0854_b200/libmact_cuda*.so; do echo -n "$lib: "; MACT_LIB=$PWD/$lib python scripts/prof_kernel.py --op lab --iters 10 --time; done
+for rep in 1 2; do for lib in paper_1009_0854_b200/libmact_cuda*.so; do echo -n "$(basename $lib): "; MACT_LIB=$PWD/$lib python scripts/prof_kernel.py --op lab --iters 20 --time; done; done
