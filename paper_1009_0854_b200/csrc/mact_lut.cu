@@ -61,10 +61,42 @@ struct OpLut {
     }
     o[0][0] = a0; o[0][1] = a1; o[0][2] = a2;
   }
+  // 4 pixels: all node indices first, then every node load, then the FMAs, so
+  // 4*K independent gathers are in flight per thread (L2 latency for 33^3,
+  // LDS latency for the smem lattice).  Trilinear (K = 8) goes 2 pixels at a
+  // time to bound register pressure.
   static __device__ __forceinline__ void px4w(uint32_t w0, uint32_t w1, uint32_t w2,
                                               const Shared* s, uint32_t lane, const Params& p,
                                               float (*o)[1][3]) {
-    px4_each<OpLut>(w0, w1, w2, s, lane, p, o);
+    constexpr int K = LutK<METHOD>::K;
+    constexpr int PB = K > 6 ? 2 : 4;                 // pixels per batch
+    const uint32_t ch[12] = {byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), byte_of(w0, 3),
+                             byte_of(w1, 0), byte_of(w1, 1), byte_of(w1, 2), byte_of(w1, 3),
+                             byte_of(w2, 0), byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3)};
+#pragma unroll
+    for (int q0 = 0; q0 < 4; q0 += PB) {
+      int idx[PB][K];
+      float w[PB][K];
+      float3 v[PB][K];
+#pragma unroll
+      for (int q = 0; q < PB; ++q)
+        lut_nodes<N, METHOD>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], idx[q], w[q]);
+#pragma unroll
+      for (int q = 0; q < PB; ++q)
+#pragma unroll
+        for (int j = 0; j < K; ++j) v[q][j] = node(s, p, idx[q][j]);
+#pragma unroll
+      for (int q = 0; q < PB; ++q) {
+        float a0 = w[q][0] * v[q][0].x, a1 = w[q][0] * v[q][0].y, a2 = w[q][0] * v[q][0].z;
+#pragma unroll
+        for (int j = 1; j < K; ++j) {
+          a0 = fmaf(w[q][j], v[q][j].x, a0);
+          a1 = fmaf(w[q][j], v[q][j].y, a1);
+          a2 = fmaf(w[q][j], v[q][j].z, a2);
+        }
+        o[q0 + q][0][0] = a0; o[q0 + q][0][1] = a1; o[q0 + q][0][2] = a2;
+      }
+    }
   }
 };
 
