@@ -138,6 +138,14 @@ int mact_lut_build(int space, int grid_n, double* lattice_f64, float* lattice_f3
  * device lattice of mact_lut_build; pixels uint8. */
 int mact_lut_interp(const float* lattice, int grid_n, int method, const uint8_t* rgb,
                     float* out, int64_t n, int layout, void* stream);
+/* the same for angular destinations: `angular_mask` bit c marks component c as
+ * an angle (lut.Lut3D.angular_mask, lut.py:44-48: hsi 1, sct 6), blended on
+ * the circle as lut.py:202-262 does (trilinear: cascaded angular_lerp; simplex
+ * methods: weighted circular mean); linear components use the weighted sum.
+ * Evaluated in fp64 on the fp64 lattice (n^3,3) of mact_lut_build (the
+ * circular mean is ill-conditioned near the gray axis). */
+int mact_lut_interp_angular(const double* lattice64, int grid_n, int method, int angular_mask,
+                            const uint8_t* rgb, float* out, int64_t n, int layout, void* stream);
 /* replaces mact.lut.node_weights (lut.py:115-199): flat node indices (n,k)
  * and weights (n,k), k = 8/6/5/4; indices bit-exact with the reference. */
 int mact_lut_nodes(int grid_n, int method, const uint8_t* rgb, int64_t n,

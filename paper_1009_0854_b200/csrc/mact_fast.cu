@@ -207,15 +207,15 @@ __global__ void k_fast_real(int space, const T* __restrict__ in, float* __restri
 #ifndef MACT_SCT_NOB
 #define MACT_SCT_NOB 2
 #endif
-// fused triple: 77 KB -> 2 CTA/SM
+// fused triple: 16+1 warps, G=1, 2 stages: 116 KB -> 1 CTA/SM (R01 sweep: 127 G px-triples/s)
 #ifndef MACT_ALL_NW
-#define MACT_ALL_NW 8
+#define MACT_ALL_NW 16
 #endif
 #ifndef MACT_ALL_G
 #define MACT_ALL_G 1
 #endif
 #ifndef MACT_ALL_SIN
-#define MACT_ALL_SIN 4
+#define MACT_ALL_SIN 2
 #endif
 #ifndef MACT_ALL_NOB
 #define MACT_ALL_NOB 1

@@ -100,6 +100,85 @@ struct OpLut {
   }
 };
 
+// ------------------------------------------------------- angular destinations
+// lut.py:202-262.  Components flagged in MASK (bit c: component c is an angle —
+// HSI hue, both SCT angles) are blended on the circle; the others take the
+// standard weighted sum.  Simplex methods use the weight-blended circular mean
+// of their nodes (_circular_blend, lut.py:219-228); trilinear cascades
+// pairwise angular_lerp along r, then g, then b (lut.py:249-262).  A vanishing
+// blended direction (hypot < 1e-12) falls back to the heaviest node (first
+// maximum weight) or to theta0, wrapped into [0, 2 pi).
+//
+// Near the gray axis the circular mean is a sum of almost-cancelling unit
+// vectors, so it is evaluated like the reference: fp64 lattice (n^3, 3),
+// fp64 weights (exact integer products / 255^k), fp64 sincos/atan2.  This
+// destination is not on the throughput metric; a per-pixel kernel suffices.
+__device__ __forceinline__ double fmod2pi_d(double a) {
+  a = fmod(a, kTwoPi);
+  return a < 0.0 ? a + kTwoPi : a;
+}
+__device__ __forceinline__ double angular_lerp_d(double t0, double t1, double a) {
+  double s0, c0, s1, c1;
+  sincos(t0, &s0, &c0);
+  sincos(t1, &s1, &c1);
+  const double c = (1.0 - a) * c0 + a * c1, s = (1.0 - a) * s0 + a * s1;
+  if (hypot(c, s) < 1e-12) return fmod2pi_d(t0);
+  const double out = atan2(s, c);
+  return out < 0.0 ? out + kTwoPi : out;
+}
+
+template <int N, int METHOD>
+__global__ void k_lut_angular(const double* __restrict__ lat, int mask, const uint8_t* __restrict__ rgb,
+                              float* __restrict__ out, int64_t n, int planar) {
+  constexpr int K = LutK<METHOD>::K;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = rgb[3 * i], g = rgb[3 * i + 1], b = rgb[3 * i + 2];
+    int idx[K];
+    double w[K];
+    lut_nodes<N, METHOD, double>(r, g, b, idx, w);
+    double res[3];
+    for (int comp = 0; comp < 3; ++comp) {
+      if (!((mask >> comp) & 1)) {
+        double a = 0.0;
+        for (int j = 0; j < K; ++j) a += w[j] * lat[3 * idx[j] + comp];
+        res[comp] = a;
+      } else if (METHOD == MACT_LUT_TRILINEAR) {
+        int br, bg, bb, rr, rg, rb;
+        lut_locate<N>(r, br, rr);
+        lut_locate<N>(g, bg, rg);
+        lut_locate<N>(b, bb, rb);
+        const double dr = rr / 255.0, dg = rg / 255.0, db = rb / 255.0;
+        double v[8];
+        for (int j = 0; j < 8; ++j) v[j] = lat[3 * idx[j] + comp];   // corner c = r<<2|g<<1|b
+        const double r00 = angular_lerp_d(v[0], v[4], dr), r01 = angular_lerp_d(v[1], v[5], dr);
+        const double r10 = angular_lerp_d(v[2], v[6], dr), r11 = angular_lerp_d(v[3], v[7], dr);
+        res[comp] = angular_lerp_d(angular_lerp_d(r00, r10, dg), angular_lerp_d(r01, r11, dg), db);
+      } else {
+        double c = 0.0, sn = 0.0, wmax = w[0], heavy = lat[3 * idx[0] + comp];
+        for (int j = 0; j < K; ++j) {
+          const double t = lat[3 * idx[j] + comp];
+          double sj, cj;
+          sincos(t, &sj, &cj);
+          c += w[j] * cj;
+          sn += w[j] * sj;
+          if (w[j] > wmax) { wmax = w[j]; heavy = t; }
+        }
+        if (hypot(c, sn) < 1e-12) {
+          res[comp] = fmod2pi_d(heavy);
+        } else {
+          const double o = atan2(sn, c);
+          res[comp] = o < 0.0 ? o + kTwoPi : o;
+        }
+      }
+    }
+    for (int comp = 0; comp < 3; ++comp) {
+      if (planar) out[comp * n + i] = (float)res[comp];
+      else out[3 * i + comp] = (float)res[comp];
+    }
+  }
+}
+
 // ---------------------------------------------------------------- build
 __global__ void k_lut_build(int space, int n, double* __restrict__ f64, float* __restrict__ f32) {
   const int total = n * n * n;
@@ -166,6 +245,22 @@ static int interp_grid(int method, const float* lat, const uint8_t* rgb, float* 
 }
 
 template <int N>
+static int interp_ang(int method, int mask, const double* lat, const uint8_t* rgb, float* out,
+                      int64_t n, int planar, cudaStream_t st) {
+  int64_t g = (n + 255) / 256;
+  if (g > 8LL * num_sms()) g = 8LL * num_sms();
+  switch (method) {
+    case MACT_LUT_TRILINEAR: k_lut_angular<N, MACT_LUT_TRILINEAR><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
+    case MACT_LUT_PRISM: k_lut_angular<N, MACT_LUT_PRISM><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
+    case MACT_LUT_PYRAMIDAL: k_lut_angular<N, MACT_LUT_PYRAMIDAL><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
+    case MACT_LUT_TETRAHEDRAL: k_lut_angular<N, MACT_LUT_TETRAHEDRAL><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
+    default: return set_error(MACT_EBADARG, "unknown interpolation method %d", method);
+  }
+  count_launch();
+  return check_launch("lut_interp_angular");
+}
+
+template <int N>
 static int nodes_grid(int method, const uint8_t* rgb, int64_t n, int32_t* nodes, float* w,
                       cudaStream_t st) {
   int64_t g = (n + 255) / 256;
@@ -223,6 +318,24 @@ extern "C" int mact_lut_nodes(int grid_n, int method, const uint8_t* rgb, int64_
     case 9: return nodes_grid<9>(method, rgb, n, nodes, weights, st);
     case 17: return nodes_grid<17>(method, rgb, n, nodes, weights, st);
     case 33: return nodes_grid<33>(method, rgb, n, nodes, weights, st);
+  }
+  return set_error(MACT_EBADARG, "grid_n must be one of 9, 17, 33");
+}
+
+extern "C" int mact_lut_interp_angular(const double* lattice64, int grid_n, int method,
+                                       int angular_mask, const uint8_t* rgb, float* out, int64_t n,
+                                       int layout, void* stream) {
+  if (n < 0 || (n > 0 && (!lattice64 || !rgb || !out))) return set_error(MACT_EBADARG, "bad argument");
+  if (angular_mask < 0 || angular_mask > 7) return set_error(MACT_EBADARG, "bad angular mask %d", angular_mask);
+  if (layout != MACT_LAYOUT_INTERLEAVED && layout != MACT_LAYOUT_PLANAR)
+    return set_error(MACT_EBADARG, "unknown layout %d", layout);
+  if (n == 0) return MACT_OK;
+  const int planar = layout == MACT_LAYOUT_PLANAR;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (grid_n) {
+    case 9: return interp_ang<9>(method, angular_mask, lattice64, rgb, out, n, planar, st);
+    case 17: return interp_ang<17>(method, angular_mask, lattice64, rgb, out, n, planar, st);
+    case 33: return interp_ang<33>(method, angular_mask, lattice64, rgb, out, n, planar, st);
   }
   return set_error(MACT_EBADARG, "grid_n must be one of 9, 17, 33");
 }

@@ -33,22 +33,22 @@ __device__ __forceinline__ void lut_locate(uint32_t p, int& base, int& rem) {
 }
 
 // Node flat indices and weights of one pixel.  rem values in [0,255].
-template <int N, int METHOD>
+template <int N, int METHOD, typename W = float>
 __device__ __forceinline__ void lut_nodes(uint32_t pr, uint32_t pg, uint32_t pb,
                                           int (&idx)[LutK<METHOD>::K],
-                                          float (&w)[LutK<METHOD>::K]) {
+                                          W (&w)[LutK<METHOD>::K]) {
   constexpr int SR = N * N, SG = N, SB = 1;
   int br, bg, bb, rr, rg, rb;
   lut_locate<N>(pr, br, rr);
   lut_locate<N>(pg, bg, rg);
   lut_locate<N>(pb, bb, rb);
   const int bf = (br * N + bg) * N + bb;
-  const float fr = (float)rr, fg = (float)rg, fb = (float)rb;
-  constexpr float inv1 = (float)(1.0 / 255.0);
-  constexpr float inv2 = (float)(1.0 / (255.0 * 255.0));
-  constexpr float inv3 = (float)(1.0 / (255.0 * 255.0 * 255.0));
+  const W fr = (W)rr, fg = (W)rg, fb = (W)rb;
+  constexpr W inv1 = (W)(1.0 / 255.0);
+  constexpr W inv2 = (W)(1.0 / (255.0 * 255.0));
+  constexpr W inv3 = (W)(1.0 / (255.0 * 255.0 * 255.0));
   if constexpr (METHOD == MACT_LUT_TRILINEAR) {
-    const float ar[2] = {255.0f - fr, fr}, ag[2] = {255.0f - fg, fg}, ab[2] = {255.0f - fb, fb};
+    const W ar[2] = {(W)255 - fr, fr}, ag[2] = {(W)255 - fg, fg}, ab[2] = {(W)255 - fb, fb};
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int cr = c >> 2 & 1, cg = c >> 1 & 1, cb = c & 1;
@@ -57,11 +57,11 @@ __device__ __forceinline__ void lut_nodes(uint32_t pr, uint32_t pg, uint32_t pb,
     }
   } else if constexpr (METHOD == MACT_LUT_PRISM) {
     const bool up = rg >= rb;                        // lut.py:146
-    const float ta = up ? 255.0f - fg : 255.0f - fb;
-    const float tb = (float)(up ? rg - rb : rb - rg);
-    const float tc = up ? fb : fg;
+    const W ta = up ? (W)255 - fg : (W)255 - fb;
+    const W tb = (W)(up ? rg - rb : rb - rg);
+    const W tc = up ? fb : fg;
     const int mid = up ? SG : SB, far = SG + SB;
-    const float a0 = 255.0f - fr;
+    const W a0 = (W)255 - fr;
     idx[0] = bf; idx[1] = bf + mid; idx[2] = bf + far;
     idx[3] = bf + SR; idx[4] = bf + mid + SR; idx[5] = bf + far + SR;
     w[0] = ta * a0 * inv2; w[1] = tb * a0 * inv2; w[2] = tc * a0 * inv2;
@@ -74,14 +74,14 @@ __device__ __forceinline__ void lut_nodes(uint32_t pr, uint32_t pg, uint32_t pb,
     const int v = sel_r ? rb : sel_g ? rb : rg;
     const int nu = sel_r ? SG : SR;
     const int nv = (sel_r | sel_g) ? SB : SG;
-    const float fu = (float)u, fv = (float)v;
+    const W fu = (W)u, fv = (W)v;
     idx[0] = bf; idx[1] = bf + nu; idx[2] = bf + nv; idx[3] = bf + nu + nv;
     idx[4] = bf + SR + SG + SB;
-    w[0] = (255.0f - fu) * (255.0f - fv) * inv2;
-    w[1] = fu * (255.0f - fv) * inv2;
-    w[2] = fv * (255.0f - fu) * inv2;
-    w[3] = (float)(u * v - 255 * m) * inv2;
-    w[4] = (float)m * inv1;
+    w[0] = ((W)255 - fu) * ((W)255 - fv) * inv2;
+    w[1] = fu * ((W)255 - fv) * inv2;
+    w[2] = fv * ((W)255 - fu) * inv2;
+    w[3] = (W)(u * v - 255 * m) * inv2;
+    w[4] = (W)m * inv1;
   } else {
     // stable argsort of -d (lut.py:185): ties keep r before g before b
     const int pos_r = (rg > rr) + (rb > rr);
@@ -92,10 +92,10 @@ __device__ __forceinline__ void lut_nodes(uint32_t pr, uint32_t pg, uint32_t pb,
     const int d2 = pos_r == 1 ? rr : pos_g == 1 ? rg : rb;
     const int d3 = pos_r == 2 ? rr : pos_g == 2 ? rg : rb;
     idx[0] = bf; idx[1] = bf + s1; idx[2] = bf + s1 + s2; idx[3] = bf + SR + SG + SB;
-    w[0] = (float)(255 - d1) * inv1;
-    w[1] = (float)(d1 - d2) * inv1;
-    w[2] = (float)(d2 - d3) * inv1;
-    w[3] = (float)d3 * inv1;
+    w[0] = (W)(255 - d1) * inv1;
+    w[1] = (W)(d1 - d2) * inv1;
+    w[2] = (W)(d2 - d3) * inv1;
+    w[3] = (W)d3 * inv1;
   }
 }
 

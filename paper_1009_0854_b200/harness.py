@@ -112,8 +112,9 @@ def _classify(space: str, candidate):
         cfg = candidate.keywords.get("cfg", cfg)
     if _FAST_FN.get(fn) == space and isinstance(cfg, fast.MactConfig):
         return "fast", cfg
-    if isinstance(candidate, LutCandidate) and space == candidate.lut.destination_space:
-        return "lut", candidate
+    if (isinstance(candidate, LutCandidate) and space == candidate.lut.destination_space
+            and not any(candidate.lut.angular_mask)):
+        return "lut", candidate                # fused (linear destinations); angular -> array path
     return "array", None
 
 

@@ -6,8 +6,8 @@
 
 The lattice is built on device from the fp64 exact transforms; interpolation
 and node selection run in libmact_cuda (integer cell location, bit-exact
-node indices).  Linear destinations (CIELAB) are supported; the angular
-HSI/SCT blend (lut.py:202-262) is listed as next work in DESIGN.md.
+node indices).  Angular destination components (HSI hue, SCT angles) are
+blended on the circle as the reference does (lut.py:202-262).
 """
 
 from __future__ import annotations
@@ -18,7 +18,7 @@ from typing import Dict, Optional, Tuple
 import numpy as np
 
 from . import _dev, _lib
-from .errors import CacheMissing, MactError
+from .errors import CacheMissing
 
 METHODS = ("trilinear", "prism", "pyramidal", "tetrahedral")
 VARIANTS = ("standard", "caching")
@@ -53,6 +53,17 @@ class Lut3D:
             v = np.zeros((self.grid_n ** 3, 4), dtype=np.float32)
             v[:, :3] = self.values.reshape(-1, 3)
             self._device[key] = torch.from_numpy(v).to(dev)
+        return self._device[key]
+
+    def lattice64(self, device=None):
+        """fp64 (n^3, 3) device lattice used by angular destinations."""
+        import torch
+
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        key = ("f64", dev.index if dev.index is not None else torch.cuda.current_device())
+        if key not in self._device:
+            self._device[key] = torch.from_numpy(
+                np.ascontiguousarray(self.values.reshape(-1, 3), dtype=np.float64)).to(dev)
         return self._device[key]
 
 
@@ -126,11 +137,15 @@ def interpolate(lut: Lut3D, pixels, method: str = "tetrahedral", variant: str = 
         raise ValueError(f"unknown variant {variant!r}")
     if variant == "caching" and lut.cache is None:
         raise CacheMissing("caching interpolation requested without a cache; call build_cache first")
-    if any(lut.angular_mask):
-        raise MactError("angular (HSI/SCT) LUT interpolation is not implemented on the device yet")
     t, lead, on_dev = _u8_pixels(pixels)
     res = out if (out is not None and on_dev) else _dev.empty_out(lead, layout, t.device)
-    lat = lut.lattice(t.device)
-    _lib.call("mact_lut_interp", lat.data_ptr(), lut.grid_n, m, t.data_ptr(), res.data_ptr(),
-              t.numel() // 3, _lib.LAYOUTS[layout], _dev.stream_ptr())
+    mask = sum(1 << c for c, ang in enumerate(lut.angular_mask) if ang)
+    if mask:
+        lat = lut.lattice64(t.device)
+        _lib.call("mact_lut_interp_angular", lat.data_ptr(), lut.grid_n, m, mask, t.data_ptr(),
+                  res.data_ptr(), t.numel() // 3, _lib.LAYOUTS[layout], _dev.stream_ptr())
+    else:
+        lat = lut.lattice(t.device)
+        _lib.call("mact_lut_interp", lat.data_ptr(), lut.grid_n, m, t.data_ptr(), res.data_ptr(),
+                  t.numel() // 3, _lib.LAYOUTS[layout], _dev.stream_ptr())
     return _dev.to_caller(res, on_dev)

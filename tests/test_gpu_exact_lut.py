@@ -124,3 +124,23 @@ def test_lut_errors(P):
         lut.interpolate(lt, np.zeros((2, 3), np.uint8), "tetrahedral", "fancy")
     with pytest.raises(CacheMissing):
         lut.interpolate(lt, np.zeros((2, 3), np.uint8), "tetrahedral", "caching")
+
+
+def _circ(a, b):
+    d = np.abs(np.asarray(a, np.float64) - np.asarray(b, np.float64)) % (2 * np.pi)
+    return np.minimum(d, 2 * np.pi - d)
+
+
+@pytest.mark.parametrize("space", ["hsi", "sct"])
+@pytest.mark.parametrize("n", [9, 17, 33])
+@pytest.mark.parametrize("method", O.METHODS)
+def test_lut_angular_interp_vs_reference(P, golden, space, n, method):
+    """Angular destinations (lut.py:202-262): hue / SCT angles blended on the circle."""
+    lt = P["lut"].build_lut(space, n)
+    got = P["lut"].interpolate(lt, dev(golden["small"]), method).cpu().numpy().astype(np.float64)
+    ref = golden[f"interp_{space}_{n}_{method}"]
+    mask = O.ANGULAR_MASKS[space]
+    scale = [2 * np.pi, 1.0, 1.0] if space == "hsi" else [255 * np.sqrt(3), np.pi / 2, np.pi / 2]
+    for c in range(3):
+        err = (_circ(got[:, c], ref[:, c]) if mask[c] else np.abs(got[:, c] - ref[:, c])) / scale[c]
+        assert err.max() <= 1e-5, (c, float(err.max()), int(err.argmax()))

@@ -125,3 +125,18 @@ def test_reduction_deterministic_and_sharded(P):
     assert tot["max"] == one["max"] and tot["argmax"] == one["argmax"]
     assert tot["count"] == one["count"]
     assert abs(tot["sum"] - one["sum"]) <= 1e-12 * one["sum"]
+
+
+def test_hsi_lut_trilinear_figure(P):
+    """PAPER.md:717 row (HSI trilinear LUT): angular LUT candidate scored by the HSI distance.
+    Checked against the oracle on a 1/64 sample of the cube (full-cube oracle angular
+    interpolation is too slow for a unit test)."""
+    h = P["harness"]
+    lt = P["lut"].build_lut("hsi", 17)
+    cube = O.cube_chunk(0, 1 << 24)[::64]
+    st = h.measure_error("hsi", h.LutCandidate(lt, "trilinear"), P["exact"].rgb_to_hsi_exact,
+                         population=cube)
+    vals = O.build_lut_values("hsi", 17)
+    ref = O.measure_error("hsi", lambda p: O.interpolate(vals, p, "trilinear", O.ANGULAR_MASKS["hsi"]),
+                          O.rgb_to_hsi_exact, cube)
+    check_figure(st.avg, st.max, ref.avg, ref.max, avg_rtol=1e-4, max_rtol=1e-3)
