@@ -210,10 +210,13 @@ def run_ours(args, wl):
     value = n_total * transforms * args.steps / (total_ms / 1e3) / 1e9
 
     achieved = n_local * BYTES_PER_PX / (kern_ms / 1e3) / 1e9
-    traffic = None
+    traffic, traffic_b = None, None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
-        traffic = json.load(open(prof)).get(args.workload)
+    if os.path.exists(prof) and world == 1:
+        t = json.load(open(prof)).get(args.workload)
+        if t:   # ncu dram bytes per launch of this kernel, as GB/s over the live launch time
+            traffic_b = t["bytes_per_launch"]
+            traffic = round(traffic_b / (kern_ms / 1e3) / 1e9, 1)
 
     # ---------------- error statistics (outside the timed region)
     err = None
@@ -274,6 +277,8 @@ def run_ours(args, wl):
                        else "working set fits L2 (no flush; latency-bound config)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                          "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
+                         "traffic_bytes_per_launch": traffic_b,
+                         "algorithmic_bytes_per_launch": n_local * BYTES_PER_PX * transforms,
                          "peak_source": hbm_src, "algorithmic_bytes_per_px": BYTES_PER_PX,
                          "kernel_ms_per_launch": round(kern_ms, 4),
                          "gpix_per_s_per_gpu_kernel": round(n_local / (kern_ms / 1e3) / 1e9, 2)},
