@@ -11,6 +11,8 @@
 // persistent CTA into shared memory (17^3 x 16 B = 78.6 KB): one LDS.128 per
 // node.  33^3 (575 KB) exceeds a CTA's 227 KB and is gathered with LDG.128
 // through L1/L2 (the lattice stays L2-resident).
+#include <cooperative_groups.h>
+
 #include "mact_lut.cuh"
 #include "mact_pixel.cuh"
 #include "mact_stream.cuh"
@@ -218,14 +220,171 @@ __global__ void k_lut_nodes(const uint8_t* __restrict__ rgb, int64_t n, int32_t*
   }
 }
 
+// ------------------------------------------------- 33^3: component-split clusters
+// The 33^3 lattice (35937 nodes) does not fit one CTA's shared memory as
+// float4 nodes (575 KB), but ONE component of it does (144 KB).  A cluster of
+// three CTAs (one per SM) works on the same 4096-pixel step: CTA rank c
+// stages component c of the lattice and computes component c of every pixel
+// of the step, gathering nodes with LDS.32 (random-gather cost per byte equal
+// to the float4 path) instead of LDG.128 through L1/L2, whose per-line tag
+// processing bounded the L2-resident version at ~0.25 px/clk/SM.
+// Output stays interleaved and line-complete: the step's pixels are split in
+// three ranges (1368/1364/1364, multiples of 4 so every range is a 16-byte
+// aligned byte span).  Every CTA sends its component of range k to CTA k as a
+// planar block with coalesced 16-byte distributed-shared-memory stores; after
+// one cluster barrier per step each owner interleaves its three planes into
+// an (N,3) staging buffer and drains it with one bulk store.  (Measured
+// alternatives: scattered STG.32 from the three CTAs -> 2.8x DRAM traffic;
+// 4-byte DSMEM scatter straight into interleaved staging -> DSMEM-bound.)
+constexpr int kLut33Threads = 1024;
+constexpr int kLut33Step = 4 * kLut33Threads;          // pixels per step
+__host__ __device__ constexpr int lut33_range_start(int k) { return k == 0 ? 0 : k == 1 ? 1368 : 2732; }
+
+template <int METHOD>
+__global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
+    k_lut33_comp(const float4* __restrict__ lat4, const uint8_t* __restrict__ rgb,
+                 float* __restrict__ out, int64_t nsteps) {
+  namespace cg = cooperative_groups;
+  constexpr int N = 33, NN = N * N * N, K = LutK<METHOD>::K;
+  constexpr int RMAX = 1368;                             // largest owner range (pixels)
+  constexpr int PLANE = RMAX, PBUF = 3 * RMAX, SBUF = 3 * RMAX;
+  extern __shared__ __align__(128) float sm33[];
+  float* lat_c = sm33;                                   // NN floats
+  float* planar = sm33 + ((NN + 31) / 32) * 32;          // [2][3][RMAX]: components of MY range
+  float* stage = planar + 2 * PBUF;                      // [2][RMAX*3]: interleaved, bulk-stored
+  cg::cluster_group cluster = cg::this_cluster();
+  const int comp = (int)cluster.block_rank();
+  const int64_t cl = blockIdx.x / 3, ncl = gridDim.x / 3;
+  for (int i = threadIdx.x; i < NN; i += blockDim.x) {
+    const float4 v = __ldg(lat4 + i);
+    lat_c[i] = comp == 0 ? v.x : comp == 1 ? v.y : v.z;
+  }
+  const int t4 = 4 * (int)threadIdx.x;                   // first pixel of this thread in a step
+  const int owner = t4 < 1368 ? 0 : (t4 < 2732 ? 1 : 2);
+  const int off = t4 - lut33_range_start(owner);
+  // my component's slot in the owner's planar block: coalesced 16-byte DSMEM stores
+  float* dst0 = cluster.map_shared_rank(planar, owner) + comp * PLANE + off;
+  const int r0 = lut33_range_start(comp);
+  const int rlen = (comp == 2 ? kLut33Step : lut33_range_start(comp + 1)) - r0;
+  cluster.sync();                                        // lattices staged, partners resident
+  const uint32_t* in_w = reinterpret_cast<const uint32_t*>(rgb);
+  // input words of the next step are loaded one step ahead: every step ends in
+  // barriers, so an un-prefetched load would expose the full DRAM latency
+  uint32_t n0 = 0, n1 = 0, n2 = 0;
+  if (cl < nsteps) {
+    const int64_t g = cl * kLut33Threads + threadIdx.x;
+    n0 = __ldg(in_w + 3 * g); n1 = __ldg(in_w + 3 * g + 1); n2 = __ldg(in_w + 3 * g + 2);
+  }
+  int it = 0;
+  for (int64_t step = cl; step < nsteps; step += ncl, ++it) {
+    const int buf = it & 1;
+    const uint32_t w0 = n0, w1 = n1, w2 = n2;
+    if (step + ncl < nsteps) {
+      const int64_t g = (step + ncl) * kLut33Threads + threadIdx.x;
+      n0 = __ldg(in_w + 3 * g); n1 = __ldg(in_w + 3 * g + 1); n2 = __ldg(in_w + 3 * g + 2);
+    }
+    const uint32_t ch[12] = {byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), byte_of(w0, 3),
+                             byte_of(w1, 0), byte_of(w1, 1), byte_of(w1, 2), byte_of(w1, 3),
+                             byte_of(w2, 0), byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3)};
+    int idx[4][K];
+    float w[4][K], v[4][K];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) lut_nodes<N, METHOD>(ch[3 * q], ch[3 * q + 1], ch[3 * q + 2], idx[q], w[q]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int j = 0; j < K; ++j) v[q][j] = lat_c[idx[q][j]];
+    float a[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      a[q] = w[q][0] * v[q][0];
+#pragma unroll
+      for (int j = 1; j < K; ++j) a[q] = fmaf(w[q][j], v[q][j], a[q]);
+    }
+    *reinterpret_cast<float4*>(dst0 + buf * PBUF) = make_float4(a[0], a[1], a[2], a[3]);
+    cluster.sync();                                      // all three components of my range landed
+    if (threadIdx.x == 0) bulk_wait_read<1>();           // stage[buf] drained by step it-2's store
+    __syncthreads();
+    const float* pl = planar + buf * PBUF;
+    float* sg = stage + buf * SBUF;
+    for (int i = threadIdx.x; 4 * i < rlen; i += blockDim.x) {   // interleave 4 pixels per thread
+      const float4 c0 = *reinterpret_cast<const float4*>(pl + 4 * i);
+      const float4 c1 = *reinterpret_cast<const float4*>(pl + PLANE + 4 * i);
+      const float4 c2 = *reinterpret_cast<const float4*>(pl + 2 * PLANE + 4 * i);
+      float4* d = reinterpret_cast<float4*>(sg + 12 * i);
+      d[0] = make_float4(c0.x, c1.x, c2.x, c0.y);
+      d[1] = make_float4(c1.y, c2.y, c0.z, c1.z);
+      d[2] = make_float4(c2.z, c0.w, c1.w, c2.w);
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_s2g(out + 3 * (step * kLut33Step + r0), sg, (uint32_t)rlen * 12u);
+      bulk_commit();
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait<0>();
+  cluster.sync();                                        // no CTA exits while partners may still write
+}
+
+template <int METHOD>
+static int launch_lut33_comp(const float* lat, const uint8_t* rgb, float* out, int64_t n, int planar,
+                             cudaStream_t st) {
+  constexpr size_t smem = (((33 * 33 * 33) + 31) / 32 * 32 + 4 * 1368 * 3) * sizeof(float);
+  const bool ok = !planar && (uintptr_t)rgb % 16 == 0 && (uintptr_t)out % 16 == 0;
+  const int64_t nsteps = ok ? n / kLut33Step : 0;
+  if (nsteps > 0) {
+    auto kfn = k_lut33_comp<METHOD>;
+    static int max_clusters[4] = {-1, -1, -1, -1};       // per method; single B200 device type
+    int& mc = max_clusters[METHOD];
+    if (mc < 0) {
+      cudaFuncSetAttribute((const void*)kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(3 * 48);
+      cfg.blockDim = dim3(kLut33Threads);
+      cfg.dynamicSmemBytes = smem;
+      if (cudaOccupancyMaxActiveClusters(&mc, (const void*)kfn, &cfg) != cudaSuccess || mc < 1) {
+        cudaGetLastError();
+        mc = num_sms() / 4;
+      }
+    }
+    const int64_t clusters = mc < nsteps ? mc : nsteps;
+    kfn<<<(unsigned)(3 * clusters), kLut33Threads, smem, st>>>(reinterpret_cast<const float4*>(lat),
+                                                               rgb, out, nsteps);
+    count_launch();
+    if (int rc = check_launch("lut33_comp")) return rc;
+  }
+  const int64_t done = nsteps * kLut33Step;
+  if (done < n) {   // tail, planar output or unaligned buffers: the L2-gather streaming kernel
+    Outs outs{{out, nullptr, nullptr}};
+    LutParams p{reinterpret_cast<const float4*>(lat)};
+    if (done == 0)
+      return launch_stream_t<OpLut<33, METHOD>, 16, 1, 3, 1>(rgb, outs, n, planar, p, st, "lut_interp");
+    auto kfn = k_generic<OpLut<33, METHOD>, 256>;
+    const size_t sb = sizeof(typename OpLut<33, METHOD>::Shared);
+    const int64_t cap = persistent_grid((const void*)kfn, 256, sb);
+    if (cap <= 0) return MACT_ECUDA;
+    int64_t grid = (n - done + 255) / 256;
+    if (grid > cap) grid = cap;
+    kfn<<<(unsigned)grid, 256, sb, st>>>(rgb, outs, done, n, planar, p);
+    count_launch();
+    return check_launch("lut_interp");
+  }
+  return MACT_OK;
+}
+
 template <int N, int METHOD>
 static int launch_interp(const float* lat, const uint8_t* rgb, float* out, int64_t n, int planar,
                          cudaStream_t st) {
   Outs outs{{out, nullptr, nullptr}};
   LutParams p{reinterpret_cast<const float4*>(lat)};
-  // 17^3: 78.6 KB lattice + 9 KB in + 12 KB out -> 2 CTA/SM (16 compute warps);
-  // 33^3 gathers from L2, so more warps in flight: 16 per CTA, 3 CTA/SM.
-  if constexpr (N == 33)
+  // 17^3 / 9^3: lattice staged in smem as float4 nodes, 78.6 KB + 9 KB in +
+  // 12 KB out -> 2 CTA/SM (16 compute warps).  33^3: component-split CTAs.
+  // 33^3: the component-split cluster wins for trilinear/prism/pyramidal (54-64
+  // vs 42-60 Gpix/s, R01); tetrahedral's 4 gathers keep the L2 path ahead (74 vs 64).
+  if constexpr (N == 33 && METHOD != MACT_LUT_TETRAHEDRAL)
+    return launch_lut33_comp<METHOD>(lat, rgb, out, n, planar, st);
+  else if constexpr (N == 33)
     return launch_stream_t<OpLut<N, METHOD>, 16, 1, 3, 1>(rgb, outs, n, planar, p, st, "lut_interp");
   else
     return launch_stream_t<OpLut<N, METHOD>, 8, (N <= 9 ? 2 : 1), 3, 1>(rgb, outs, n, planar, p, st,
