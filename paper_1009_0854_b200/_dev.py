@@ -77,6 +77,15 @@ def empty_out(lead: tuple, layout: str, device, dtype=None):
     return torch.empty(shape, dtype=dtype, device=device)
 
 
+def check_out(out, lead: tuple, layout: str, device):
+    """Validate a caller-supplied device output tensor (shape, dtype, contiguity)."""
+    shape = lead + (3,) if layout == "interleaved" else (3,) + lead
+    if not is_device_tensor(out) or out.dtype != torch.float32 or tuple(out.shape) != shape \
+            or not out.is_contiguous() or out.device != device:
+        raise ValueError(f"out must be a contiguous float32 CUDA tensor of shape {shape} on {device}")
+    return out
+
+
 def to_caller(t, on_dev: bool):
     """Device result back to the caller's world (numpy for host callers)."""
     if on_dev:

@@ -124,7 +124,8 @@ def transform(space: str, pixels, cfg: MactConfig = DEFAULT_CONFIG, *, out=None,
             return _host_u8(space, arr, cfg, out, layout)
     t, code, lead, on_dev = _dev.as_device_pixels(pixels)
     n = t.numel() // 3
-    res = out if (out is not None and on_dev) else _dev.empty_out(lead, layout, t.device)
+    res = (_dev.check_out(out, lead, layout, t.device) if (out is not None and on_dev)
+           else _dev.empty_out(lead, layout, t.device))
     _lib.call(_ENTRY[space], t.data_ptr(), code, res.data_ptr(), n, cfg.coeffs,
               _lib.LAYOUTS[layout], _dev.stream_ptr())
     if not on_dev and out is not None:

@@ -138,7 +138,8 @@ def interpolate(lut: Lut3D, pixels, method: str = "tetrahedral", variant: str = 
     if variant == "caching" and lut.cache is None:
         raise CacheMissing("caching interpolation requested without a cache; call build_cache first")
     t, lead, on_dev = _u8_pixels(pixels)
-    res = out if (out is not None and on_dev) else _dev.empty_out(lead, layout, t.device)
+    res = (_dev.check_out(out, lead, layout, t.device) if (out is not None and on_dev)
+           else _dev.empty_out(lead, layout, t.device))
     mask = sum(1 << c for c, ang in enumerate(lut.angular_mask) if ang)
     if mask:
         lat = lut.lattice64(t.device)
@@ -149,3 +150,44 @@ def interpolate(lut: Lut3D, pixels, method: str = "tetrahedral", variant: str = 
         _lib.call("mact_lut_interp", lat.data_ptr(), lut.grid_n, m, t.data_ptr(), res.data_ptr(),
                   t.numel() // 3, _lib.LAYOUTS[layout], _dev.stream_ptr())
     return _dev.to_caller(res, on_dev)
+
+
+# ------------------------------------------------------------------ MLUT files
+# lut.py:353-383 of the reference: "MLUT" magic, little-endian u32 version,
+# grid, space index, angular-mask bits, then (n,n,n,3) float64 values.
+_MAGIC = b"MLUT"
+_VERSION = 1
+
+
+def save_lut(lut: Lut3D, path) -> None:
+    """Write the lattice (never the cache) in the reference's binary format."""
+    import struct
+
+    mask = sum(1 << i for i, a in enumerate(lut.angular_mask) if a)
+    with open(path, "wb") as fh:
+        fh.write(_MAGIC + struct.pack("<IIII", _VERSION, lut.grid_n,
+                                      SPACES.index(lut.destination_space), mask))
+        fh.write(np.ascontiguousarray(lut.values, dtype="<f8").tobytes())
+
+
+def load_lut(path) -> Lut3D:
+    """Read an MLUT file; MalformedHeader on a bad magic, version, grid or size."""
+    import struct
+
+    from .errors import MalformedHeader
+
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    if len(blob) < 20 or blob[:4] != _MAGIC:
+        raise MalformedHeader("not a LUT file (bad magic)")
+    version, grid_n, space_idx, mask = struct.unpack("<IIII", blob[4:20])
+    if version != _VERSION:
+        raise MalformedHeader(f"unsupported LUT version {version}")
+    if space_idx >= len(SPACES) or grid_n not in (9, 17, 33):
+        raise MalformedHeader("corrupt LUT header")
+    payload = blob[20:]
+    if len(payload) != grid_n ** 3 * 3 * 8:
+        raise MalformedHeader(f"LUT payload size {len(payload)} != expected {grid_n ** 3 * 24}")
+    values = np.frombuffer(payload, dtype="<f8").reshape(grid_n, grid_n, grid_n, 3).astype(np.float64)
+    return Lut3D(grid_n=grid_n, spacing=255.0 / (grid_n - 1), destination_space=SPACES[space_idx],
+                 values=values, angular_mask=tuple(bool(mask >> i & 1) for i in range(3)))

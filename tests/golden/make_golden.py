@@ -135,6 +135,7 @@ def main() -> None:
                 else:
                     arrays[f"interp_{space}_{n}_{method}"] = lut.interpolate(L, small, method)
     arrays["probe_offsets"] = np.array(offsets)
+    lut.save_lut(lut.build_lut("hsi", 9), OUT / "ref_hsi9.mlut")       # MLUT format fixture
     np.savez_compressed(OUT / "reference_outputs.npz", **arrays)
     if "--arrays-only" in sys.argv:
         print(f"arrays written in {time.time() - t0:.1f}s")

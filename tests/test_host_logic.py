@@ -1,0 +1,67 @@
+"""CPU tests of the host-side logic of the package (no GPU needed)."""
+
+import numpy as np
+import pytest
+
+from oracle import mact_oracle as O
+from paper_1009_0854_b200 import approximants, lut
+from paper_1009_0854_b200.errors import MalformedHeader, UnknownApproximant
+from paper_1009_0854_b200.fast import DEFAULT_CONFIG, MactConfig
+
+
+def test_config_resolves_like_reference():
+    c = DEFAULT_CONFIG
+    assert (c.cielab_degrees, c.hsi_degree, c.sct_degrees) == ((4, 4), 5, (5, 5, 5))
+    k = c.coeffs
+    assert (k.cbrt_num_deg, k.cbrt_den_deg, k.hsi_deg, k.asin_deg, k.acos_deg, k.atan_deg) == (4, 4, 5, 5, 5, 5)
+    # the HSI pipeline evaluates the [0,1] refit, not the bundled Table 3 set (fast.py:38-43)
+    assert tuple(k.atan_sqrt3[:6]) == O.HSI_REFIT[5]
+    assert tuple(k.cbrt_num[:5]) == tuple(float(x) for x in O.CBRT_RATIONALS[(4, 4)][0])
+
+
+@pytest.mark.parametrize("kw", [dict(cielab_degrees=(5, 5)), dict(hsi_degree=6),
+                                dict(sct_degrees=(3, 5, 5)), dict(cielab_degrees=(4,))])
+def test_unknown_degrees_raise(kw):
+    with pytest.raises((UnknownApproximant, ValueError)):
+        MactConfig(**kw)
+
+
+def test_registry_matches_oracle_tables():
+    for (n, m), (num, den) in O.CBRT_RATIONALS.items():
+        a = approximants.registry_get(approximants.TargetFn.CBRT, (n, m))
+        assert a.form.numerator.coeffs == tuple(map(float, num))
+        assert a.form.denominator.coeffs == tuple(map(float, den))
+    for deg in (4, 5):
+        assert approximants.registry_get(approximants.TargetFn.ASIN_HALF, (deg,)).form.coeffs == \
+            tuple(map(float, O.ASIN_HALF[deg]))
+        assert approximants.registry_get(approximants.TargetFn.ATAN_G, (deg,)).form.coeffs == \
+            tuple(map(float, O.ATAN_G[deg]))
+    assert len(approximants.registry_keys()) == 25
+
+
+def test_mlut_roundtrip_and_errors(tmp_path):
+    vals = O.build_lut_values("hsi", 9)
+    L = lut.Lut3D(9, 255 / 8, "hsi", vals, lut.ANGULAR_MASKS["hsi"])
+    p = tmp_path / "a.mlut"
+    lut.save_lut(L, p)
+    R = lut.load_lut(p)
+    assert R.grid_n == 9 and R.destination_space == "hsi" and R.angular_mask == (True, False, False)
+    np.testing.assert_array_equal(R.values, vals)
+    raw = p.read_bytes()
+    for bad in (b"XXXX" + raw[4:], raw[:4] + (2).to_bytes(4, "little") + raw[8:], raw[:-8]):
+        q = tmp_path / "bad.mlut"
+        q.write_bytes(bad)
+        with pytest.raises(MalformedHeader):
+            lut.load_lut(q)
+
+
+def test_mlut_bytes_match_reference(tmp_path):
+    """save_lut writes byte-identical files to the reference's (lut.py:353-361)."""
+    import os
+    ref = os.path.join(os.path.dirname(__file__), "golden", "ref_hsi9.mlut")
+    L = lut.Lut3D(9, 255 / 8, "hsi", O.build_lut_values("hsi", 9), lut.ANGULAR_MASKS["hsi"])
+    p = tmp_path / "ours.mlut"
+    lut.save_lut(L, p)
+    assert p.read_bytes() == open(ref, "rb").read()
+    R = lut.load_lut(ref)
+    np.testing.assert_array_equal(R.values, L.values)
