@@ -8,7 +8,9 @@
 // three different chunks at once.  Pinned host buffers are DMA'd directly;
 // pageable buffers are staged through pinned bounce buffers, with the CPU
 // memcpy of chunk k overlapping the DMA of chunk k-1.
+#include <algorithm>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "mact_common.cuh"
@@ -26,6 +28,27 @@ struct MactHostCtx {
 };
 
 using namespace mact;
+
+// Parallel memcpy for the pageable staging path: one host thread moves ~5-10
+// GB/s (less while first-touch page faults land in a fresh numpy array), so
+// large copies are split across hardware threads.
+static void par_memcpy(void* dst, const void* src, size_t bytes) {
+  const size_t kMinPerThread = 4u << 20;
+  unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  size_t nt = std::min<size_t>(std::min<size_t>(hw, 16), std::max<size_t>(1, bytes / kMinPerThread));
+  if (nt <= 1) {
+    memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t part = (bytes + nt - 1) / nt;
+  for (size_t i = 0; i < nt; ++i) {
+    const size_t lo = i * part, hi = std::min(bytes, lo + part);
+    if (lo >= hi) break;
+    th.emplace_back([=] { memcpy((char*)dst + lo, (const char*)src + lo, hi - lo); });
+  }
+  for (auto& t : th) t.join();
+}
 
 static bool is_pinned(const void* p) {
   cudaPointerAttributes a;
@@ -142,9 +165,9 @@ extern "C" int mact_transform_host(MactHostCtx* c, int op, const uint8_t* host_r
     if (e != cudaSuccess) return set_error(MACT_ECUDA, "d2h: %s", cudaGetErrorString(e));
     const int64_t off = k * c->chunk, m = std::min<int64_t>(c->chunk, n - off);
     if (layout == MACT_LAYOUT_INTERLEAVED) {
-      memcpy(host_out + 3 * off, c->h_out[s], (size_t)m * 12);
+      par_memcpy(host_out + 3 * off, c->h_out[s], (size_t)m * 12);
     } else {
-      for (int p = 0; p < 3; ++p) memcpy(host_out + p * n + off, c->h_out[s] + p * m, (size_t)m * 4);
+      for (int p = 0; p < 3; ++p) par_memcpy(host_out + p * n + off, c->h_out[s] + p * m, (size_t)m * 4);
     }
     pending[s] = -1;
     return MACT_OK;
@@ -160,7 +183,7 @@ extern "C" int mact_transform_host(MactHostCtx* c, int op, const uint8_t* host_r
       if (rc == MACT_OK && e == cudaSuccess) e = copy_out(host_out, c->d_out[s], off, m, n, layout, st);
     } else {
       if ((rc = drain(s)) != MACT_OK) break;
-      memcpy(c->h_in[s], host_rgb + 3 * off, (size_t)m * 3);
+      par_memcpy(c->h_in[s], host_rgb + 3 * off, (size_t)m * 3);
       e = cudaMemcpyAsync(c->d_in[s], c->h_in[s], (size_t)m * 3, cudaMemcpyHostToDevice, st);
       if (e == cudaSuccess) rc = run_kernel(op, c->d_in[s], c->d_out[s], m, cf, layout, st);
       if (rc == MACT_OK && e == cudaSuccess)
