@@ -11,6 +11,8 @@
 // persistent CTA into shared memory (17^3 x 16 B = 78.6 KB): one LDS.128 per
 // node.  33^3 (575 KB) exceeds a CTA's 227 KB and is gathered with LDG.128
 // through L1/L2 (the lattice stays L2-resident).
+#include <atomic>
+
 #include <cooperative_groups.h>
 
 #include "mact_lut.cuh"
@@ -324,7 +326,7 @@ __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
     }
   }
   if (threadIdx.x == 0) bulk_wait<0>();
-  cluster.sync();                                        // no CTA exits while partners may still write
+  cluster.sync();                                        // partners may still write my planar buffer
 }
 
 template <int METHOD>
@@ -335,8 +337,8 @@ static int launch_lut33_comp(const float* lat, const uint8_t* rgb, float* out, i
   const int64_t nsteps = ok ? n / kLut33Step : 0;
   if (nsteps > 0) {
     auto kfn = k_lut33_comp<METHOD>;
-    static int max_clusters[4] = {-1, -1, -1, -1};       // per method; single B200 device type
-    int& mc = max_clusters[METHOD];
+    static std::atomic<int> max_clusters{-1};           // per method instantiation (benign race)
+    int mc = max_clusters.load();
     if (mc < 0) {
       cudaFuncSetAttribute((const void*)kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       cudaLaunchConfig_t cfg = {};
@@ -347,6 +349,7 @@ static int launch_lut33_comp(const float* lat, const uint8_t* rgb, float* out, i
         cudaGetLastError();
         mc = num_sms() / 4;
       }
+      max_clusters.store(mc);
     }
     const int64_t clusters = mc < nsteps ? mc : nsteps;
     kfn<<<(unsigned)(3 * clusters), kLut33Threads, smem, st>>>(reinterpret_cast<const float4*>(lat),

@@ -143,3 +143,30 @@ def test_unknown_approximant_and_bad_args(P):
         fast.rgb_to_lab_fast(np.zeros((4, 2), np.uint8))
     with pytest.raises(ValueError):
         fast.transform("xyz", np.zeros((4, 3), np.uint8))
+
+
+@pytest.mark.parametrize("degenerate", [False, True])
+def test_corpus_images_vs_oracle(P, degenerate):
+    """BASELINE configs 4/5 content: correlated synthetic images (config 5 adds 10 %
+    saturated channels and 5 % exact grays, exercising the hue singularity)."""
+    from paper_1009_0854_b200 import corpus
+    img = corpus.correlated_image(3, 270, 480, degenerate=degenerate)      # 1/8-scale 1080p
+    host = img.cpu().numpy()
+    flat = host.reshape(-1, 3)
+    if degenerate:
+        gray = (flat[:, 0] == flat[:, 1]) & (flat[:, 1] == flat[:, 2])
+        assert gray.mean() > 0.04 and ((flat == 0) | (flat == 255)).any(axis=1).mean() > 0.08
+    lab, hsi, sct = P["fast"].rgb_to_all_fast(img)
+    CHECK["lab"](lab.cpu().numpy(), O.rgb_to_lab_fast(host))
+    CHECK["hsi"](hsi.cpu().numpy(), O.rgb_to_hsi_fast(host))
+    CHECK["sct"](sct.cpu().numpy(), O.rgb_to_sct_fast(host))
+    # the same bytes through the single-transform kernels
+    np.testing.assert_array_equal(P["fast"].rgb_to_hsi_fast(img).cpu().numpy(), hsi.cpu().numpy())
+
+
+def test_corpus_deterministic_per_image_seed(P):
+    """Image i has the same bytes whatever the shard (sharding by image)."""
+    from paper_1009_0854_b200 import corpus
+    a = corpus.batch(range(2, 5), 64, 96)
+    b = corpus.batch([4], 64, 96)
+    np.testing.assert_array_equal(a[2].cpu().numpy(), b[0].cpu().numpy())
