@@ -14,8 +14,6 @@ plumbing (torch ops), not part of the measured path.
 
 from __future__ import annotations
 
-import math
-
 
 def _gauss_kernel(sigma: float, truncate: float, device):
     import torch

@@ -41,11 +41,7 @@ struct OpLab {
     const uint32_t ch[12] = {byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), byte_of(w0, 3),
                              byte_of(w1, 0), byte_of(w1, 1), byte_of(w1, 2), byte_of(w1, 3),
                              byte_of(w2, 0), byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3)};
-#ifdef MACT_LAB_MONIC_ONLY   // analysis builds: drop the generic-degree path
-    if (true) {
-#else
     if (c.monic44) {
-#endif
       float v[4][3];
       lab_fast_u8x4(ch, s->gamma, lane, c, v);
 #pragma unroll

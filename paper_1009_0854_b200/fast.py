@@ -22,14 +22,13 @@ Every call runs libmact_cuda kernels; there is no CPU fallback.
 
 from __future__ import annotations
 
-import functools
 from dataclasses import dataclass
 from typing import Tuple
 
 import numpy as np
 
 from . import _dev, _lib
-from .approximants import (Approximant, Rational, TargetFn, hsi_refit, registry_get)
+from .approximants import Rational, TargetFn, hsi_refit, registry_get
 
 TWO_PI = 2.0 * np.pi
 

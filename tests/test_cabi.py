@@ -5,7 +5,6 @@ layout (checked by compiling the header with gcc)."""
 import os
 import re
 import subprocess
-import sys
 
 import pytest
 
