@@ -244,6 +244,13 @@ def run_ours(args, wl):
         tot = parallel.combine(parallel.all_gather_partials(parts, dev))[0]
         err = {"dE_mean": tot["sum"] / tot["count"], "dE_max": tot["max"],
                "dE_argmax_index": tot["argmax"], "pixels": tot["count"]}
+        if space == "all":   # config 5: per-component |fast - exact| for HSI and SCT too
+            for sp in ("hsi", "sct"):
+                parts = harness.reduce_partials(sp, harness.fast_candidate(sp), None, xf,
+                                                index_base=base, metric="component")
+                comps = parallel.combine(parallel.all_gather_partials(parts, dev))
+                err[sp] = [{"mean": c["sum"] / max(c["count"], 1), "max": c["max"],
+                            "excluded_nan": c["nan"]} for c in comps]
 
     # ---------------- end to end through the public API with HOST buffers
     e2e = None
