@@ -167,6 +167,11 @@ int mact_err_reduce(const MactErrSpec* spec, const MactCoeffs* c, const uint8_t*
 /* harness.cube_chunk (harness.py:35-46) on device: rgb[i] = cube pixel start+i */
 int mact_cube_fill(uint8_t* rgb, int64_t start, int64_t n, void* stream);
 
+/* harness.call_probabilities (harness.py:137-175) as exact full-cube counts:
+ * counts (device, 6 x u64) = {cbrt_x, cbrt_y, cbrt_z, arcsin, arccos, arctan}
+ * call-site hits over all 2^24 colours; probability = count / 2^24. */
+int mact_call_counts(unsigned long long* counts, void* stream);
+
 /* ---- host streaming executor (end-to-end, HOST buffers) ------------------ */
 /* Runs a fast transform over HOST buffers: chunked H2D -> kernel -> D2H on
  * `nstreams` CUDA streams so both copy engines and the SMs overlap.  Host

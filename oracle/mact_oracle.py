@@ -603,6 +603,33 @@ def component_abs_error(space: str, fast_out, exact_out):
     return res
 
 
+CALL_SITES = ("cbrt_x", "cbrt_y", "cbrt_z", "arcsin", "arccos", "arctan")
+
+
+def call_counts() -> Dict[str, int]:
+    """harness.py:137-175 — full-cube call-site counts of the approximated functions.
+
+    Restated by brute force over every colour (not the reference's row/plane
+    counting), with the same fp64 evaluation order: X/X0 > knee is
+    m[row,0]*gamma[r] + (m[row,1]*gamma[g] + m[row,2]*gamma[b]) > LAB_KNEE*white[row]
+    (harness.py:146-156); arcsin <=> 3b^2 >= r^2+g^2 in integers (:158-170);
+    arctan defined unless r = g = 0 (:174).
+    """
+    gamma = inverse_gamma(np.arange(256) / 255.0)
+    out = {}
+    for row, name in enumerate(("cbrt_x", "cbrt_y", "cbrt_z")):
+        tr, tg, tb = (RGB_TO_XYZ[row, k] * gamma for k in range(3))
+        plane = tg[:, None] + tb[None, :]
+        thr = LAB_KNEE * WHITE[row]
+        out[name] = int(sum(np.count_nonzero(tr[r] + plane > thr) for r in range(256)))
+    i = np.arange(256, dtype=np.int64)
+    rg2 = (i[:, None] ** 2 + i[None, :] ** 2).reshape(-1)
+    out["arcsin"] = int(sum(np.count_nonzero(3 * b * b >= rg2) for b in range(256)))
+    out["arccos"] = CUBE_SIZE - out["arcsin"]
+    out["arctan"] = CUBE_SIZE - 256
+    return out
+
+
 # ---------------------------------------------------------------------------
 # CPU baseline runner (bench.py cpu_baseline / --impl reference).  Mirrors
 # the reference's only concurrency: a ThreadPoolExecutor over fixed pixel

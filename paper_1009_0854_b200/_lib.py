@@ -68,6 +68,7 @@ _SIGNATURES = {
     "mact_err_reduce": (_i, [C.POINTER(MactErrSpec), C.POINTER(MactCoeffs), _vp, _i64, _i64,
                              _i64, _vp, _vp, _vp]),
     "mact_cube_fill": (_i, [_vp, _i64, _i64, _vp]),
+    "mact_call_counts": (_i, [_vp, _vp]),
     "mact_probe_expand": (_i, [_vp, _vp, _i64, _vp]),
     "mact_host_ctx_create": (_i, [_i, _i64, _i, C.POINTER(_vp)]),
     "mact_host_ctx_destroy": (_i, [_vp]),

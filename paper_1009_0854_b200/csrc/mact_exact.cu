@@ -5,10 +5,13 @@
 //   mact_distance     <- exact.lab_distance / hsi_distance / sct_distance_indirect
 //                        (exact.py:163-190)
 //   mact_cube_fill    <- harness.cube_chunk               (harness.py:35-46)
+//   mact_call_counts  <- harness.call_probabilities       (harness.py:137-175)
 //
 // These are not on the roofline metric (the error path and lattice builds
 // use them); they follow the reference formulas in fp64 with libdevice
 // cbrt/pow/atan/acos/atan2/sincos.
+#include <cmath>
+
 #include "mact_pixel.cuh"
 
 namespace mact {
@@ -97,6 +100,58 @@ __global__ void k_cube_fill(uint8_t* __restrict__ rgb, int64_t start, int64_t n)
   }
 }
 
+// harness.call_probabilities (harness.py:137-175) as exact counts over the
+// cube.  One thread per (r, g) walks b = 0..255.  The lightness-kernel test
+// keeps the reference's fp64 evaluation order, m0*gamma[r] + (m1*gamma[g] +
+// m2*gamma[b]) > knee*white (harness.py:146-156), with explicit _rn ops so no
+// FMA contraction changes a rounding; gamma[] is the host-libm table (the
+// reference's numpy pow), not libdevice pow, so a value within an ulp of the
+// threshold cannot flip.  Integer counts -> atomics are order-independent.
+struct CallParams {
+  double gamma[256];
+};
+
+__global__ void __launch_bounds__(256) k_call_counts(const __grid_constant__ CallParams p,
+                                                     unsigned long long* __restrict__ counts) {
+  __shared__ double m[3][3], thr[3];
+  if (threadIdx.x < 9) m[threadIdx.x / 3][threadIdx.x % 3] = rgb2xyz(threadIdx.x / 3, threadIdx.x % 3);
+  if (threadIdx.x < 3)
+    thr[threadIdx.x] = __dmul_rn(kLabKnee, threadIdx.x == 0 ? kWhiteX : threadIdx.x == 1 ? kWhiteY : kWhiteZ);
+  __syncthreads();
+  const int rg = blockIdx.x * blockDim.x + threadIdx.x;          // grid covers 65536 exactly
+  const int r = rg >> 8, g = rg & 255;
+  uint32_t cx = 0, cy = 0, cz = 0, casin = 0;
+  double tr[3], tg[3];
+#pragma unroll
+  for (int row = 0; row < 3; ++row) {
+    tr[row] = __dmul_rn(m[row][0], p.gamma[r]);
+    tg[row] = __dmul_rn(m[row][1], p.gamma[g]);
+  }
+  const int rg2 = r * r + g * g;
+  for (int b = 0; b < 256; ++b) {
+    const double gb = p.gamma[b];
+    cx += __dadd_rn(tr[0], __dadd_rn(tg[0], __dmul_rn(m[0][2], gb))) > thr[0];
+    cy += __dadd_rn(tr[1], __dadd_rn(tg[1], __dmul_rn(m[1][2], gb))) > thr[1];
+    cz += __dadd_rn(tr[2], __dadd_rn(tg[2], __dmul_rn(m[2][2], gb))) > thr[2];
+    casin += 3 * b * b >= rg2;
+  }
+  const uint32_t catan = (r | g) ? 256u : 0u;
+  uint32_t v[5] = {cx, cy, cz, casin, catan};
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) atomicAdd(&counts[k < 4 ? k : 5], (unsigned long long)v[k]);
+  }
+}
+
+__global__ void k_call_counts_finish(unsigned long long* counts) {
+  counts[4] = (1ull << 24) - counts[3];                           // arccos = complement
+}
+
 static unsigned grid_for(int64_t n, int per_sm = 8) {
   int64_t g = (n + 255) / 256;
   const int64_t cap = (int64_t)per_sm * num_sms();
@@ -165,6 +220,25 @@ extern "C" int mact_distance(int space, const void* x, int x_dtype, const void* 
   if (x_dtype == MACT_DTYPE_F64) return dist_y(space, (const double*)x, y, y_dtype, out, n, st);
   if (x_dtype == MACT_DTYPE_F32) return dist_y(space, (const float*)x, y, y_dtype, out, n, st);
   return set_error(MACT_EBADARG, "unsupported dtype %d", x_dtype);
+}
+
+extern "C" int mact_call_counts(unsigned long long* counts, void* stream) {
+  if (!counts) return set_error(MACT_EBADARG, "bad argument");
+  static const CallParams params = [] {
+    CallParams q;
+    for (int i = 0; i < 256; ++i) {          // exact.inverse_gamma(i / 255) (exact.py:52-57), host libm
+      const double k = i / 255.0;
+      q.gamma[i] = k < kGammaKnee ? k / kGammaSlope : std::pow((k + kGammaOffset) / kGammaScale, kGammaPower);
+    }
+    return q;
+  }();
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(counts, 0, 6 * sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return set_error(MACT_ECUDA, "call_counts: %s", cudaGetErrorString(e));
+  k_call_counts<<<256, 256, 0, st>>>(params, counts);
+  k_call_counts_finish<<<1, 1, 0, st>>>(counts);
+  count_launch(2);
+  return check_launch("call_counts");
 }
 
 extern "C" int mact_cube_fill(uint8_t* rgb, int64_t start, int64_t n, void* stream) {

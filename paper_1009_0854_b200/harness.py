@@ -4,6 +4,7 @@
     measure_error(space, candidate, reference, population=None)   (harness.py:77-122)
     ErrorStats                                         (harness.py:63-68)
     component_error(...)   per-component |fast - exact|  (not in the reference)
+    call_probabilities()  CallProbabilities             (harness.py:125-175)
 
 ``measure_error`` keeps the reference's plugin seam — any callable
 ``pixels -> (..., 3)`` — and fuses the whole evaluation into one kernel
@@ -281,6 +282,37 @@ def component_error(space: str, candidate: Callable = None, reference: Callable 
                                   argmax_index=tot["argmax"],
                                   argmax_pixel=_pixel_at(shards, tot["argmax"])))
     return out
+
+
+@dataclass(frozen=True)
+class CallProbabilities:
+    """Relative full-cube frequencies of the approximated-function call sites
+    (harness.py:125-134)."""
+
+    cbrt_x: float
+    cbrt_y: float
+    cbrt_z: float
+    arcsin: float
+    arccos: float
+    arctan: float
+
+
+def call_counts(device=None) -> dict:
+    """Exact call-site counts over all 2^24 colours, counted on the GPU
+    (mact_call_counts; harness.py:137-175)."""
+    import torch
+
+    _dev.require_cuda()
+    buf = torch.empty(6, dtype=torch.int64, device=device or "cuda")
+    _lib.call("mact_call_counts", buf.data_ptr(), _dev.stream_ptr())
+    vals = buf.cpu().tolist()
+    return dict(zip(("cbrt_x", "cbrt_y", "cbrt_z", "arcsin", "arccos", "arctan"), vals))
+
+
+def call_probabilities() -> CallProbabilities:
+    """harness.call_probabilities (harness.py:137-175): counts / 2^24."""
+    c = call_counts()
+    return CallProbabilities(**{k: v / CUBE_SIZE for k, v in c.items()})
 
 
 def measure_gain(*_a, **_k):  # pragma: no cover - out of scope (SURVEY §2 row 7)

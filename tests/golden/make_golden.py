@@ -74,8 +74,22 @@ def probe_pixels() -> dict:
     return sets
 
 
+def call_probs(harness) -> dict:
+    """harness.call_probabilities() (harness.py:137-175) as exact cube counts."""
+    p = harness.call_probabilities()
+    names = ("cbrt_x", "cbrt_y", "cbrt_z", "arcsin", "arccos", "arctan")
+    return {k: {"p": getattr(p, k), "count": int(round(getattr(p, k) * harness.CUBE_SIZE))}
+            for k in names}
+
+
 def main() -> None:
     sys.path.insert(0, str(REF))
+    if "--call-probs-only" in sys.argv:     # refresh one figure without the full sweep
+        from mact import harness
+        fig = json.loads((OUT / "figures.json").read_text())
+        fig["call_probabilities"] = call_probs(harness)
+        (OUT / "figures.json").write_text(json.dumps(fig, indent=1))
+        return
     os.environ.setdefault("MACT_THREADS", str(os.cpu_count() or 1))
     from mact import exact, fast, harness, lut
     from mact.fast import MactConfig
@@ -220,6 +234,7 @@ def main() -> None:
             acc[c]["argmax_pixel"] = [a >> 16, (a >> 8) & 255, a & 255]
         comp[space] = acc
     fig["c2_component"] = comp
+    fig["call_probabilities"] = call_probs(harness)
 
     (OUT / "figures.json").write_text(json.dumps(fig, indent=1))
     (OUT / "hsi_refit.json").write_text(json.dumps({"coeffs": refit, "eps": refit_eps}, indent=1))

@@ -140,3 +140,13 @@ def test_hsi_lut_trilinear_figure(P):
     ref = O.measure_error("hsi", lambda p: O.interpolate(vals, p, "trilinear", O.ANGULAR_MASKS["hsi"]),
                           O.rgb_to_hsi_exact, cube)
     check_figure(st.avg, st.max, ref.avg, ref.max, avg_rtol=1e-4, max_rtol=1e-3)
+
+
+def test_call_probabilities(P, figures):
+    """GPU cube counting (mact_call_counts) == reference harness.call_probabilities exactly."""
+    h = P["harness"]
+    counts = h.call_counts()
+    probs = h.call_probabilities()
+    for k, v in figures["call_probabilities"].items():
+        assert counts[k] == v["count"], k
+        assert getattr(probs, k) == v["p"], k

@@ -130,3 +130,11 @@ def test_cube_hsi_figure(figures):
     ref = figures["cube"]["hsi_5"]
     assert st.avg == pytest.approx(ref["avg"], rel=1e-13)
     assert st.max == ref["max"] and list(st.argmax_pixel) == ref["argmax_pixel"]
+
+
+def test_call_counts_vs_reference(figures):
+    """Oracle brute-force call-site counts == reference harness.call_probabilities."""
+    got = O.call_counts()
+    for k, v in figures["call_probabilities"].items():
+        assert got[k] == v["count"], k
+        assert got[k] / O.CUBE_SIZE == v["p"], k
