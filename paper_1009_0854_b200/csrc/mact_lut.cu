@@ -8,9 +8,13 @@
 // Device lattice format: (n^3, 4) fp32, r-major, node = (c0, c1, c2, 0) so a
 // node is one 16-byte load.  Interpolation runs inside the streaming skeleton
 // (mact_stream.cuh).  For grids 9^3 and 17^3 the lattice is staged once per
-// persistent CTA into shared memory (17^3 x 16 B = 78.6 KB): one LDS.128 per
-// node.  33^3 (575 KB) exceeds a CTA's 227 KB and is gathered with LDG.128
-// through L1/L2 (the lattice stays L2-resident).
+// persistent CTA into shared memory as two planes, (c0, c1) float2 and c2
+// float (17^3 x 12 B = 59 KB): one LDS.64 + one LDS.32 per node.  Random
+// gathers are bank-conflict bound, and on B200 a random warp LDS.64 + LDS.32
+// costs 7.9 smem cycles against 9.4 for one LDS.128 of a padded float4 node
+// (tools/ldsbench.cu), with 25 % less smem per CTA.  33^3 (575 KB) exceeds a
+// CTA's 227 KB and is gathered with LDG.128 through L1/L2 (the lattice stays
+// L2-resident).
 #include <atomic>
 
 #include <cooperative_groups.h>
@@ -18,6 +22,13 @@
 #include "mact_lut.cuh"
 #include "mact_pixel.cuh"
 #include "mact_stream.cuh"
+
+#ifndef MACT_LUT_NW
+#define MACT_LUT_NW 16
+#endif
+#ifndef MACT_LUT_SIN
+#define MACT_LUT_SIN 3
+#endif
 
 namespace mact {
 
@@ -30,35 +41,50 @@ struct OpLut {
   static constexpr int NOUT = 1;
   static constexpr bool SMEM = N <= 17;
   using Params = LutParams;
+  // 9^3: bank-private copies.  An LDS.128 warp access is served 8 lanes per
+  // phase, one 16-byte bank group per lane when conflict-free; node i of lane
+  // slot k = lane & 7 lives at float4 index 8 i + k, so the 8 lanes of a
+  // phase always hit 8 different groups (8 x 729 x 16 B = 93 KB).
+  static constexpr bool PRIV = N <= 9;
   struct Shared {
-    float4 lat[SMEM ? N * N * N : 1];
+    float4 lat[PRIV ? 8 * N * N * N : 1];
+    float2 c01[SMEM && !PRIV ? N * N * N : 1];
+    float c2[SMEM && !PRIV ? N * N * N : 1];
   };
   static __device__ __forceinline__ void init(Shared* s, const Params& p) {
-    if constexpr (SMEM) {
-      for (int i = threadIdx.x; i < N * N * N; i += blockDim.x)
-        s->lat[i] = __ldg(p.lat + i);
+    if constexpr (PRIV) {
+      for (int i = threadIdx.x; i < 8 * N * N * N; i += blockDim.x) s->lat[i] = __ldg(p.lat + (i >> 3));
+    } else if constexpr (SMEM) {
+      for (int i = threadIdx.x; i < N * N * N; i += blockDim.x) {
+        const float4 v = __ldg(p.lat + i);
+        s->c01[i] = make_float2(v.x, v.y);
+        s->c2[i] = v.z;
+      }
     }
   }
-  static __device__ __forceinline__ float3 node(const Shared* s, const Params& p, int i) {
-    if constexpr (SMEM) {
-      const float4 v = s->lat[i];
+  static __device__ __forceinline__ float3 node(const Shared* s, const Params& p, int i, uint32_t lane) {
+    if constexpr (PRIV) {
+      const float4 v = s->lat[(i << 3) | (lane & 7)];
       return make_float3(v.x, v.y, v.z);
+    } else if constexpr (SMEM) {
+      const float2 v = s->c01[i];
+      return make_float3(v.x, v.y, s->c2[i]);
     } else {
       const float4 v = __ldg(p.lat + i);
       return make_float3(v.x, v.y, v.z);
     }
   }
   static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
-                                            uint32_t, const Params& p, float (*o)[3]) {
+                                            uint32_t lane, const Params& p, float (*o)[3]) {
     constexpr int K = LutK<METHOD>::K;
     int idx[K];
     float w[K];
     lut_nodes<N, METHOD>(r, g, b, idx, w);
-    float3 v = node(s, p, idx[0]);
+    float3 v = node(s, p, idx[0], lane);
     float a0 = w[0] * v.x, a1 = w[0] * v.y, a2 = w[0] * v.z;
 #pragma unroll
     for (int j = 1; j < K; ++j) {
-      v = node(s, p, idx[j]);
+      v = node(s, p, idx[j], lane);
       a0 = fmaf(w[j], v.x, a0);
       a1 = fmaf(w[j], v.y, a1);
       a2 = fmaf(w[j], v.z, a2);
@@ -88,7 +114,7 @@ struct OpLut {
 #pragma unroll
       for (int q = 0; q < PB; ++q)
 #pragma unroll
-        for (int j = 0; j < K; ++j) v[q][j] = node(s, p, idx[q][j]);
+        for (int j = 0; j < K; ++j) v[q][j] = node(s, p, idx[q][j], lane);
 #pragma unroll
       for (int q = 0; q < PB; ++q) {
         float a0 = w[q][0] * v[q][0].x, a1 = w[q][0] * v[q][0].y, a2 = w[q][0] * v[q][0].z;
@@ -390,8 +416,8 @@ static int launch_interp(const float* lat, const uint8_t* rgb, float* out, int64
   else if constexpr (N == 33)
     return launch_stream_t<OpLut<N, METHOD>, 16, 1, 3, 1>(rgb, outs, n, planar, p, st, "lut_interp");
   else
-    return launch_stream_t<OpLut<N, METHOD>, 8, (N <= 9 ? 2 : 1), 3, 1>(rgb, outs, n, planar, p, st,
-                                                                         "lut_interp");
+    return launch_stream_t<OpLut<N, METHOD>, MACT_LUT_NW, (N <= 9 ? 2 : 1), MACT_LUT_SIN, 1>(
+        rgb, outs, n, planar, p, st, "lut_interp");
 }
 
 template <int N>
