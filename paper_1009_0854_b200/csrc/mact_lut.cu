@@ -259,14 +259,48 @@ __global__ void k_lut_nodes(const uint8_t* __restrict__ rgb, int64_t n, int32_t*
 // Output stays interleaved and line-complete: the step's pixels are split in
 // three ranges (1368/1364/1364, multiples of 4 so every range is a 16-byte
 // aligned byte span).  Every CTA sends its component of range k to CTA k as a
-// planar block with coalesced 16-byte distributed-shared-memory stores; after
-// one cluster barrier per step each owner interleaves its three planes into
-// an (N,3) staging buffer and drains it with one bulk store.  (Measured
-// alternatives: scattered STG.32 from the three CTAs -> 2.8x DRAM traffic;
-// 4-byte DSMEM scatter straight into interleaved staging -> DSMEM-bound.)
+// planar block with 16-byte st.async distributed-shared-memory stores that
+// complete transaction bytes on the owner's "full" mbarrier; each owner
+// interleaves its three planes into an (N,3) staging buffer and drains it
+// with one bulk store.  The planar and staging buffers are double-buffered
+// and handed back through per-(owner, buffer) "empty" mbarriers in the
+// writers' shared memory, so the three CTAs never meet at a cluster barrier
+// inside the loop (the R01 version's per-step cluster.sync cost ~25 % of its
+// time in barrier/membar stalls).  (Measured alternatives: scattered STG.32
+// from the three CTAs -> 2.8x DRAM traffic; 4-byte DSMEM scatter straight
+// into interleaved staging -> DSMEM-bound.)
 constexpr int kLut33Threads = 1024;
 constexpr int kLut33Step = 4 * kLut33Threads;          // pixels per step
 __host__ __device__ constexpr int lut33_range_start(int k) { return k == 0 ? 0 : k == 1 ? 1368 : 2732; }
+constexpr int kLut33Rmax = 1368;                       // largest owner range (pixels)
+constexpr size_t kLut33Smem =
+    (((33 * 33 * 33) + 31) / 32 * 32 + 4 * kLut33Rmax * 3) * sizeof(float) + 8 * sizeof(uint64_t);
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_v4(uint32_t addr, float4 v, uint32_t mbar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(addr),
+      "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x100000u)
+      : "memory");
+}
 
 template <int METHOD>
 __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
@@ -274,30 +308,38 @@ __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
                  float* __restrict__ out, int64_t nsteps) {
   namespace cg = cooperative_groups;
   constexpr int N = 33, NN = N * N * N, K = LutK<METHOD>::K;
-  constexpr int RMAX = 1368;                             // largest owner range (pixels)
-  constexpr int PLANE = RMAX, PBUF = 3 * RMAX, SBUF = 3 * RMAX;
+  constexpr int PLANE = kLut33Rmax, PBUF = 3 * kLut33Rmax, SBUF = 3 * kLut33Rmax;
   extern __shared__ __align__(128) float sm33[];
   float* lat_c = sm33;                                   // NN floats
   float* planar = sm33 + ((NN + 31) / 32) * 32;          // [2][3][RMAX]: components of MY range
   float* stage = planar + 2 * PBUF;                      // [2][RMAX*3]: interleaved, bulk-stored
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage + 2 * SBUF);   // [2]: my planar buffer b landed
+  uint64_t* empty = full + 2;                            // [3][2]: owner k's planar buffer b is free
   cg::cluster_group cluster = cg::this_cluster();
-  const int comp = (int)cluster.block_rank();
+  const uint32_t comp = cluster.block_rank();
   const int64_t cl = blockIdx.x / 3, ncl = gridDim.x / 3;
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    for (int i = 0; i < 6; ++i) mbar_init(&empty[i], 1);
+    fence_mbar_init();
+  }
   for (int i = threadIdx.x; i < NN; i += blockDim.x) {
     const float4 v = __ldg(lat4 + i);
     lat_c[i] = comp == 0 ? v.x : comp == 1 ? v.y : v.z;
   }
   const int t4 = 4 * (int)threadIdx.x;                   // first pixel of this thread in a step
-  const int owner = t4 < 1368 ? 0 : (t4 < 2732 ? 1 : 2);
+  const uint32_t owner = t4 < 1368 ? 0 : (t4 < 2732 ? 1 : 2);
   const int off = t4 - lut33_range_start(owner);
-  // my component's slot in the owner's planar block: coalesced 16-byte DSMEM stores
-  float* dst0 = cluster.map_shared_rank(planar, owner) + comp * PLANE + off;
+  // my component's slot in the owner's planar block (buffer 0) and the owner's full barriers
+  const uint32_t dst0 = mapa_u32(smem_u32(planar + comp * PLANE + off), owner);
+  const uint32_t ofull0 = mapa_u32(smem_u32(&full[0]), owner);
   const int r0 = lut33_range_start(comp);
   const int rlen = (comp == 2 ? kLut33Step : lut33_range_start(comp + 1)) - r0;
-  cluster.sync();                                        // lattices staged, partners resident
+  const uint32_t full_bytes = (uint32_t)rlen * 3u * 4u;
+  cluster.sync();                                        // barriers initialised, lattices staged
   const uint32_t* in_w = reinterpret_cast<const uint32_t*>(rgb);
-  // input words of the next step are loaded one step ahead: every step ends in
-  // barriers, so an un-prefetched load would expose the full DRAM latency
+  // input words of the next step are loaded one step ahead
   uint32_t n0 = 0, n1 = 0, n2 = 0;
   if (cl < nsteps) {
     const int64_t g = cl * kLut33Threads + threadIdx.x;
@@ -306,6 +348,7 @@ __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
   int it = 0;
   for (int64_t step = cl; step < nsteps; step += ncl, ++it) {
     const int buf = it & 1;
+    const uint32_t use = (uint32_t)it >> 1;
     const uint32_t w0 = n0, w1 = n1, w2 = n2;
     if (step + ncl < nsteps) {
       const int64_t g = (step + ncl) * kLut33Threads + threadIdx.x;
@@ -329,12 +372,15 @@ __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
 #pragma unroll
       for (int j = 1; j < K; ++j) a[q] = fmaf(w[q][j], v[q][j], a[q]);
     }
-    *reinterpret_cast<float4*>(dst0 + buf * PBUF) = make_float4(a[0], a[1], a[2], a[3]);
-    cluster.sync();                                      // all three components of my range landed
-    if (threadIdx.x == 0) bulk_wait_read<1>();           // stage[buf] drained by step it-2's store
-    __syncthreads();
+    // owner's buffer `buf` must have been consumed (its use - 1), then send my component
+    if (it >= 2) mbar_wait_acq_cluster(&empty[owner * 2 + buf], (use - 1) & 1);
+    st_async_v4(dst0 + (uint32_t)(buf * PBUF * 4), make_float4(a[0], a[1], a[2], a[3]),
+                ofull0 + (uint32_t)(buf * 8));
+    // owner role: wait for the three components of my range, interleave, store
+    if (threadIdx.x == 0) mbar_arrive_expect_tx(&full[buf], full_bytes);
+    mbar_wait_acq_cluster(&full[buf], use & 1);
     const float* pl = planar + buf * PBUF;
-    float* sg = stage + buf * SBUF;
+    float* sg = stage + buf * SBUF;                      // free: drained before the last barrier
     for (int i = threadIdx.x; 4 * i < rlen; i += blockDim.x) {   // interleave 4 pixels per thread
       const float4 c0 = *reinterpret_cast<const float4*>(pl + 4 * i);
       const float4 c1 = *reinterpret_cast<const float4*>(pl + PLANE + 4 * i);
@@ -345,20 +391,23 @@ __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
       d[2] = make_float4(c2.z, c0.w, c1.w, c2.w);
     }
     fence_proxy_async_smem();
-    __syncthreads();
+    if (threadIdx.x == 0) bulk_wait_read<0>();           // stage[buf ^ 1] (previous step) drained
+    __syncthreads();                                     // stage written, planar[buf] read
     if (threadIdx.x == 0) {
       bulk_s2g(out + 3 * (step * kLut33Step + r0), sg, (uint32_t)rlen * 12u);
       bulk_commit();
+#pragma unroll
+      for (uint32_t c = 0; c < 3; ++c) mbar_arrive_cluster(mapa_u32(smem_u32(&empty[comp * 2 + buf]), c));
     }
   }
   if (threadIdx.x == 0) bulk_wait<0>();
-  cluster.sync();                                        // partners may still write my planar buffer
+  cluster.sync();                                        // partners may still signal / write my smem
 }
 
 template <int METHOD>
 static int launch_lut33_comp(const float* lat, const uint8_t* rgb, float* out, int64_t n, int planar,
                              cudaStream_t st) {
-  constexpr size_t smem = (((33 * 33 * 33) + 31) / 32 * 32 + 4 * 1368 * 3) * sizeof(float);
+  constexpr size_t smem = kLut33Smem;
   const bool ok = !planar && (uintptr_t)rgb % 16 == 0 && (uintptr_t)out % 16 == 0;
   const int64_t nsteps = ok ? n / kLut33Step : 0;
   if (nsteps > 0) {
@@ -407,11 +456,16 @@ static int launch_interp(const float* lat, const uint8_t* rgb, float* out, int64
                          cudaStream_t st) {
   Outs outs{{out, nullptr, nullptr}};
   LutParams p{reinterpret_cast<const float4*>(lat)};
-  // 17^3 / 9^3: lattice staged in smem as float4 nodes, 78.6 KB + 9 KB in +
-  // 12 KB out -> 2 CTA/SM (16 compute warps).  33^3: component-split CTAs.
-  // 33^3: the component-split cluster wins for trilinear/prism/pyramidal (54-64
-  // vs 42-60 Gpix/s, R01); tetrahedral's 4 gathers keep the L2 path ahead (74 vs 64).
+  // 17^3: (c0,c1)+c2 smem planes, 59 KB; 9^3: 8 bank-private float4 copies,
+  // 93 KB; 16 compute warps per CTA.  33^3: the component-split cluster wins
+  // for trilinear/prism/pyramidal (60/66/70 vs 42-60 Gpix/s through L2);
+  // tetrahedral's 4 gathers leave the L2 path level with it (74 vs 72), and
+  // the cluster repeats the node selection in all three CTAs (ALU-bound).
+#ifdef MACT_LUT33_TET_CLUSTER
+  if constexpr (N == 33)
+#else
   if constexpr (N == 33 && METHOD != MACT_LUT_TETRAHEDRAL)
+#endif
     return launch_lut33_comp<METHOD>(lat, rgb, out, n, planar, st);
   else if constexpr (N == 33)
     return launch_stream_t<OpLut<N, METHOD>, 16, 1, 3, 1>(rgb, outs, n, planar, p, st, "lut_interp");
