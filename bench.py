@@ -45,8 +45,8 @@ WORKLOADS = {
                desc="BASELINE config 1: one 512x512 uint8 image, default_rng(0), RGB->CIELAB MACT"),
     "c2": dict(kind="cube", n=1 << 24, space="hsi+sct",
                desc="BASELINE config 2: 2^24 cube, RGB->HSI and RGB->SCT MACT"),
-    "c3": dict(kind="random", n=4096 * 4096, space="lut17_tetrahedral",
-               desc="BASELINE config 3: 4096^2 uint8, tetrahedral 17^3 LUT (RGB->CIELAB)"),
+    "c3": dict(kind="random", n=4096 * 4096, space="lut",
+               desc="BASELINE config 3: 4096^2 uint8, default_rng(0), {method} {grid}^3 LUT (RGB->CIELAB)"),
 }
 
 
@@ -163,7 +163,8 @@ def run_ours(args, wl):
     space = wl["space"]
     outs = [torch.empty((n_local, 3), dtype=torch.float32, device=dev)
             for _ in range(3 if space in ("all",) else (2 if space == "hsi+sct" else 1))]
-    lt = lut.build_lut("lab", 17) if space.startswith("lut") else None
+    lt = lut.build_lut("lab", args.lut_grid) if space == "lut" else None
+    lut_code = lut._method_code(args.lut_method)
     def step():
         sp_ptr = torch.cuda.current_stream(dev).cuda_stream   # capture-safe (graph mode)
         if space == "all":
@@ -176,8 +177,8 @@ def run_ours(args, wl):
             _lib.check(lib.mact_lab_fast(xf.data_ptr(), 0, outs[0].data_ptr(), n_local, cfg.coeffs, 0, sp_ptr))
         else:
             lat = lt.lattice(dev)
-            _lib.check(lib.mact_lut_interp(lat.data_ptr(), 17, 3, xf.data_ptr(), outs[0].data_ptr(),
-                                           n_local, 0, sp_ptr))
+            _lib.check(lib.mact_lut_interp(lat.data_ptr(), args.lut_grid, lut_code, xf.data_ptr(),
+                                           outs[0].data_ptr(), n_local, 0, sp_ptr))
 
     transforms = {"all": 3, "hsi+sct": 2}.get(space, 1)
     for _ in range(max(args.warmup, 3)):
@@ -238,9 +239,9 @@ def run_ours(args, wl):
 
     # ---------------- error statistics (outside the timed region)
     err = None
-    if space in ("lab", "all") and wl["kind"] == "images":
-        parts = harness.reduce_partials("lab", harness.fast_candidate("lab"), None, xf,
-                                        index_base=base)
+    if space in ("lab", "all", "lut"):
+        cand = harness.LutCandidate(lt, args.lut_method) if space == "lut" else harness.fast_candidate("lab")
+        parts = harness.reduce_partials("lab", cand, None, xf, index_base=base)
         tot = parallel.combine(parallel.all_gather_partials(parts, dev))[0]
         err = {"dE_mean": tot["sum"] / tot["count"], "dE_max": tot["max"],
                "dE_argmax_index": tot["argmax"], "pixels": tot["count"]}
@@ -345,8 +346,8 @@ def run_reference(args, wl):
     fns = {"lab": [O.rgb_to_lab_fast], "all": [O.rgb_to_lab_fast, O.rgb_to_hsi_fast, O.rgb_to_sct_fast],
            "hsi+sct": [O.rgb_to_hsi_fast, O.rgb_to_sct_fast]}.get(space)
     if fns is None:
-        vals = O.build_lut_values("lab", 17)
-        fns = [lambda p: O.interpolate(vals, p, "tetrahedral")]
+        vals = O.build_lut_values("lab", args.lut_grid)
+        fns = [lambda p: O.interpolate(vals, p, args.lut_method)]
     for _ in range(max(args.warmup, 1)):
         for f in fns:
             O.run_chunked(f, sample, threads)
@@ -384,12 +385,16 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--lut-grid", type=int, choices=[9, 17, 33], default=17, help="c3 only")
+    ap.add_argument("--lut-method", choices=["trilinear", "prism", "pyramidal", "tetrahedral"],
+                    default="tetrahedral", help="c3 only")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=None,
                     help="capture the K steps in a CUDA graph (default: only for workloads < 4 Mpx)")
     args = ap.parse_args()
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload])
+    wl["desc"] = wl["desc"].format(grid=args.lut_grid, method=args.lut_method)
     if args.impl == "reference":
         run_reference(args, wl)
     else:

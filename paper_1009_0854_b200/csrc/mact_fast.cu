@@ -17,6 +17,13 @@ namespace mact {
 // px(): one pixel (tail / unaligned kernel); px4w(): the 4 pixels packed in
 // three input words (streaming kernel, warp-converged).  Both run the same
 // arithmetic, so tile and tail results are bit-identical.
+// GAMMA_TABLE rounded to fp32, generated from the oracle's fp64 table (the
+// reference's numpy pow).  Loading it costs a CTA ~0.1 us; evaluating 256
+// fp64 pow() per CTA cost ~0.9 us, 20 % of a 512^2 image (BASELINE C1).
+__device__ const float kGammaF32[256] = {
+#include "mact_gamma_table.inc"
+};
+
 struct OpLab {
   static constexpr int NOUT = 1;
   using Params = KCoeffs;
@@ -24,8 +31,8 @@ struct OpLab {
     float gamma[256 * 32];   // GAMMA_TABLE (fast.py:35) in fp32, replicated per bank
   };
   static __device__ __forceinline__ void init(Shared* s, const Params&) {
-    for (int k = threadIdx.x; k < 256; k += blockDim.x) {   // 256 pow() per CTA, then replicate
-      const float v = (float)inverse_gamma_d((double)k / 255.0);
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) {   // L2-resident table, replicated per bank
+      const float v = __ldg(kGammaF32 + k);
 #pragma unroll 8
       for (int r = 0; r < 32; ++r) s->gamma[(k << 5) | ((r + k) & 31)] = v;
     }
@@ -165,6 +172,12 @@ __global__ void k_fast_real(int space, const T* __restrict__ in, float* __restri
 // NOB output buffers per warp> (DESIGN.md §Kernels has the smem/occupancy math).
 // Overridable at build time for tuning (MACT_NVCC_DEFS, see build.py).
 // CIELAB: 16+1 warps, G=4, 2 stages: 176 KB smem (32 KB bank-replicated gamma) -> 1 CTA/SM (R01 sweep: 250 Gpix/s)
+#ifndef MACT_LAB_SMALL_N
+#define MACT_LAB_SMALL_N (1 << 21)
+#endif
+#ifndef MACT_LAB_SNW
+#define MACT_LAB_SNW 16
+#endif
 #ifndef MACT_LAB_NW
 #define MACT_LAB_NW 16
 #endif
@@ -247,8 +260,13 @@ static int fast_entry(int space, const void* rgb, int in_dtype, float* out, int6
   const uint8_t* in = (const uint8_t*)rgb;
   switch (in_dtype) {
     case MACT_DTYPE_U8:
-      if (space == MACT_SPACE_LAB)
+      if (space == MACT_SPACE_LAB) {
+        // images below ~one tile per SM (C1: 512^2 = 32 tiles of 8192) take
+        // 4x smaller tiles so the work spreads over 4x more SMs
+        if (n < (int64_t)MACT_LAB_SMALL_N)
+          return launch_stream_t<OpLab, MACT_LAB_SNW, 1, 2, 1>(in, outs, n, planar, kc, st, "lab_fast");
         return launch_stream_t<OpLab, MACT_LAB_CFG>(in, outs, n, planar, kc, st, "lab_fast");
+      }
       if (space == MACT_SPACE_HSI)
         return launch_stream_t<OpHsi, MACT_HSI_CFG>(in, outs, n, planar, kc, st, "hsi_fast");
       return launch_stream_t<OpSct, MACT_SCT_CFG>(in, outs, n, planar, kc, st, "sct_fast");

@@ -92,3 +92,14 @@ def test_product_never_imports_oracle():
             if f.endswith(".py"):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*", "", txt).replace('"""', ""), f
+
+
+def test_gamma_table_header_is_current():
+    """csrc/mact_gamma_table.inc == fp32(oracle GAMMA_TABLE) (regenerate with scripts/gen_gamma_table.py)."""
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("gen", os.path.join(root, "scripts", "gen_gamma_table.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    with open(os.path.join(root, "paper_1009_0854_b200", "csrc", "mact_gamma_table.inc")) as fh:
+        assert fh.read() == gen.render()
