@@ -9,6 +9,8 @@
 // input (the reference's float path, fast.py:96-99) runs a per-pixel fp64
 // kernel that follows the reference formulas operation for operation.
 #include "mact_pixel.cuh"
+#include <type_traits>
+
 #include "mact_stream.cuh"
 
 namespace mact {
@@ -116,37 +118,47 @@ struct OpExpand {
 };
 using OpSct = OpPoly<MACT_SPACE_SCT>;
 
-struct OpAll {
-  static constexpr int NOUT = 3;
+// Any subset of {Lab, HSI, SCT} from one read of the pixels (MASK bit 0 =
+// Lab, 1 = HSI, 2 = SCT); outputs are packed in that order.  Config 5 runs
+// all three, config 2 the HSI + SCT pair (no gamma table, no fp64).
+template <int MASK>
+struct OpMulti {
+  static constexpr bool LAB = MASK & 1, HSI = MASK & 2, SCT = MASK & 4;
+  static constexpr int NOUT = LAB + HSI + SCT;
   using Params = KCoeffs;
-  using Shared = OpLab::Shared;
-  static __device__ __forceinline__ void init(Shared* s, const Params& c) { OpLab::init(s, c); }
+  struct NoShared { int unused; };
+  using Shared = typename std::conditional<LAB, OpLab::Shared, NoShared>::type;
+  static __device__ __forceinline__ void init(Shared* s, const Params& c) {
+    if constexpr (LAB) OpLab::init(s, c);
+  }
+  static __device__ __forceinline__ void put(float* o, const Lab3& v) { o[0] = v.c0; o[1] = v.c1; o[2] = v.c2; }
   static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
                                             uint32_t lane, const Params& c, float (*o)[3]) {
-    const Lab3 a = lab_fast_u8(r, g, b, s->gamma, lane, c);
-    const Lab3 h = hsi_fast_u8(r, g, b, c);
-    const Lab3 q = sct_fast_u8(r, g, b, c);
-    o[0][0] = a.c0; o[0][1] = a.c1; o[0][2] = a.c2;
-    o[1][0] = h.c0; o[1][1] = h.c1; o[1][2] = h.c2;
-    o[2][0] = q.c0; o[2][1] = q.c1; o[2][2] = q.c2;
+    int k = 0;
+    if constexpr (LAB) put(o[k++], lab_fast_u8(r, g, b, s->gamma, lane, c));
+    if constexpr (HSI) put(o[k++], hsi_fast_u8(r, g, b, c));
+    if constexpr (SCT) put(o[k++], sct_fast_u8(r, g, b, c));
   }
   static __device__ __forceinline__ void px4w(uint32_t w0, uint32_t w1, uint32_t w2,
                                               const Shared* s, uint32_t lane, const Params& c,
-                                              float (*o)[3][3]) {
-    float lab[4][1][3];
-    OpLab::px4w(w0, w1, w2, s, lane, c, lab);
+                                              float (*o)[NOUT][3]) {
+    if constexpr (LAB) {
+      float lab[4][1][3];
+      OpLab::px4w(w0, w1, w2, s, lane, c, lab);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { o[q][0][0] = lab[q][0][0]; o[q][0][1] = lab[q][0][1]; o[q][0][2] = lab[q][0][2]; }
+    }
     float f[12];
     words_to_rgbf(w0, w1, w2, f);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const Lab3 h = hsi_fast_f(f[3 * q], f[3 * q + 1], f[3 * q + 2], c);
-      const Lab3 z = sct_fast_f(f[3 * q], f[3 * q + 1], f[3 * q + 2], c);
-      o[q][0][0] = lab[q][0][0]; o[q][0][1] = lab[q][0][1]; o[q][0][2] = lab[q][0][2];
-      o[q][1][0] = h.c0; o[q][1][1] = h.c1; o[q][1][2] = h.c2;
-      o[q][2][0] = z.c0; o[q][2][1] = z.c1; o[q][2][2] = z.c2;
+      int k = LAB;
+      if constexpr (HSI) put(o[q][k++], hsi_fast_f(f[3 * q], f[3 * q + 1], f[3 * q + 2], c));
+      if constexpr (SCT) put(o[q][k++], sct_fast_f(f[3 * q], f[3 * q + 1], f[3 * q + 2], c));
     }
   }
 };
+using OpAll = OpMulti<7>;
 
 // Real-valued input, fp64, reference formulas verbatim.
 template <typename T>
@@ -233,6 +245,20 @@ __global__ void k_fast_real(int space, const T* __restrict__ in, float* __restri
 #define MACT_HSI_CFG MACT_HSI_NW, MACT_HSI_G, MACT_HSI_SIN, MACT_HSI_NOB
 #define MACT_SCT_CFG MACT_SCT_NW, MACT_SCT_G, MACT_SCT_SIN, MACT_SCT_NOB
 #define MACT_ALL_CFG MACT_ALL_NW, MACT_ALL_G, MACT_ALL_SIN, MACT_ALL_NOB
+// HSI + SCT pair (config 2): fp32 only, 27 B/px
+#ifndef MACT_HS_NW
+#define MACT_HS_NW 16
+#endif
+#ifndef MACT_HS_G
+#define MACT_HS_G 1
+#endif
+#ifndef MACT_HS_SIN
+#define MACT_HS_SIN 4
+#endif
+#ifndef MACT_HS_NOB
+#define MACT_HS_NOB 2
+#endif
+#define MACT_HS_CFG MACT_HS_NW, MACT_HS_G, MACT_HS_SIN, MACT_HS_NOB
 
 template <typename T>
 static int launch_real(int space, const T* in, float* out, int64_t n, int planar,
@@ -303,9 +329,19 @@ extern "C" int mact_all_fast(const uint8_t* rgb, float* lab, float* hsi, float* 
     return set_error(MACT_EBADARG, "unknown layout %d", layout);
   KCoeffs kc;
   if (int rc = make_kcoeffs(c, &kc)) return rc;
-  Outs outs{{lab, hsi, sct}};
-  return launch_stream_t<OpAll, MACT_ALL_CFG>(
-      rgb, outs, n, layout == MACT_LAYOUT_PLANAR, kc, (cudaStream_t)stream, "all_fast");
+  const int mask = (lab != nullptr) | (hsi != nullptr) << 1 | (sct != nullptr) << 2;
+  const int planar = layout == MACT_LAYOUT_PLANAR;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (mask) {
+    case 0: return MACT_OK;
+    case 1: return mact_lab_fast(rgb, MACT_DTYPE_U8, lab, n, c, layout, stream);
+    case 2: return mact_hsi_fast(rgb, MACT_DTYPE_U8, hsi, n, c, layout, stream);
+    case 4: return mact_sct_fast(rgb, MACT_DTYPE_U8, sct, n, c, layout, stream);
+    case 3: return launch_stream_t<OpMulti<3>, MACT_ALL_CFG>(rgb, Outs{{lab, hsi, nullptr}}, n, planar, kc, st, "multi_fast");
+    case 5: return launch_stream_t<OpMulti<5>, MACT_ALL_CFG>(rgb, Outs{{lab, sct, nullptr}}, n, planar, kc, st, "multi_fast");
+    case 6: return launch_stream_t<OpMulti<6>, MACT_HS_CFG>(rgb, Outs{{hsi, sct, nullptr}}, n, planar, kc, st, "multi_fast");
+    default: return launch_stream_t<OpAll, MACT_ALL_CFG>(rgb, Outs{{lab, hsi, sct}}, n, planar, kc, st, "all_fast");
+  }
 }
 
 extern "C" int mact_probe_expand(const uint8_t* rgb, float* out, int64_t n, void* stream) {

@@ -148,18 +148,21 @@ def rgb_to_sct_fast(pixels, cfg: MactConfig = DEFAULT_CONFIG, **kw):
     return transform("sct", pixels, cfg, **kw)
 
 
-def rgb_to_all_fast(pixels, cfg: MactConfig = DEFAULT_CONFIG, *, layout: str = "interleaved"):
-    """All three transforms from one read of the pixels (BASELINE config 5).
+def rgb_to_all_fast(pixels, cfg: MactConfig = DEFAULT_CONFIG, *, layout: str = "interleaved",
+                    spaces=("lab", "hsi", "sct")):
+    """Several transforms from one read of the pixels (BASELINE configs 5 and 2).
 
-    Device tensor in (uint8) -> (lab, hsi, sct) device tensors out.
+    uint8 pixels in -> one output per name in ``spaces`` (a subset of lab, hsi,
+    sct), returned in the order given; each equals the single transform.
     """
-    import torch
-
     t, code, lead, on_dev = _dev.as_device_pixels(pixels)
     if code != _lib.DTYPE_U8:
         raise ValueError("rgb_to_all_fast takes 8-bit pixels")
+    spaces = tuple(spaces)
+    if not spaces or any(s not in ("lab", "hsi", "sct") for s in spaces) or len(set(spaces)) != len(spaces):
+        raise ValueError(f"spaces must be distinct names from lab, hsi, sct; got {spaces}")
     n = t.numel() // 3
-    outs = [_dev.empty_out(lead, layout, t.device) for _ in range(3)]
-    _lib.call("mact_all_fast", t.data_ptr(), *[o.data_ptr() for o in outs], n, cfg.coeffs,
-              _lib.LAYOUTS[layout], _dev.stream_ptr())
-    return tuple(_dev.to_caller(o, on_dev) for o in outs)
+    outs = {s: _dev.empty_out(lead, layout, t.device) for s in spaces}
+    ptrs = [outs[s].data_ptr() if s in outs else None for s in ("lab", "hsi", "sct")]
+    _lib.call("mact_all_fast", t.data_ptr(), *ptrs, n, cfg.coeffs, _lib.LAYOUTS[layout], _dev.stream_ptr())
+    return tuple(_dev.to_caller(outs[s], on_dev) for s in spaces)

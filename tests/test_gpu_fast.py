@@ -83,6 +83,22 @@ def test_unaligned_and_planar(P, space):
     np.testing.assert_array_equal(planar.T, full[:65536])
 
 
+@pytest.mark.parametrize("spaces", [("hsi", "sct"), ("lab", "hsi"), ("sct", "lab"), ("hsi",)])
+def test_fused_subsets_match_single(P, spaces):
+    """mact_all_fast with NULL outputs: every subset equals the single transforms."""
+    fast = P["fast"]
+    rng = np.random.default_rng(12)
+    d = dev(rng.integers(0, 256, ((1 << 20) + 77, 3), dtype=np.uint8))
+    got = fast.rgb_to_all_fast(d, spaces=spaces)
+    for sp, g in zip(spaces, got):
+        np.testing.assert_array_equal(g.cpu().numpy(), getattr(fast, f"rgb_to_{sp}_fast")(d).cpu().numpy())
+    planar = fast.rgb_to_all_fast(d[:65536], spaces=spaces, layout="planar")
+    for sp, g in zip(spaces, planar):
+        np.testing.assert_array_equal(g.cpu().numpy().T, getattr(fast, f"rgb_to_{sp}_fast")(d[:65536]).cpu().numpy())
+    with pytest.raises(ValueError):
+        fast.rgb_to_all_fast(d, spaces=("hsi", "hsi"))
+
+
 def test_fused_all_matches_single(P):
     fast = P["fast"]
     rng = np.random.default_rng(11)
