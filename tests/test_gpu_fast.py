@@ -186,3 +186,18 @@ def test_corpus_deterministic_per_image_seed(P):
     a = corpus.batch(range(2, 5), 64, 96)
     b = corpus.batch([4], 64, 96)
     np.testing.assert_array_equal(a[2].cpu().numpy(), b[0].cpu().numpy())
+
+
+@pytest.mark.parametrize("space", ["lab", "sct"])
+def test_beyond_int32_pixel_count(P, space):
+    """One call over 2^31 + 4099 pixels (BASELINE config 5 is 2.12 G px per GPU):
+    64-bit indexing in the tile, tail and store paths.  Pixels repeat the cube
+    enumeration, so any output position can be checked against the oracle."""
+    n = (1 << 31) + 4099
+    x = P["harness"].cube_chunk(0, 1 << 24, device="cuda").repeat((n >> 24) + 1, 1)[:n]
+    out = getattr(P["fast"], f"rgb_to_{space}_fast")(x)
+    idx = np.r_[0:64, (1 << 31) - 64:(1 << 31) + 64, n - 4099 - 64:n]
+    got = out[torch.from_numpy(idx).cuda()].cpu().numpy()
+    CHECK[space](got, O.FAST[space](O.cube_chunk(0, 1 << 24)[idx % (1 << 24)]))
+    del out, x
+    torch.cuda.empty_cache()
