@@ -109,11 +109,14 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------- CPU legs
-def cpu_port_run(space: str, images, budget_s: float, threads: int):
+def cpu_port_run(space: str, images, budget_s: float, threads: int, lut_spec=None):
     """Oracle port (numpy, the reference algorithm) over host images until budget_s."""
     from oracle import mact_oracle as O
 
     fn = {"lab": O.rgb_to_lab_fast, "hsi": O.rgb_to_hsi_fast, "sct": O.rgb_to_sct_fast}
+    if space == "lut":
+        vals = O.build_lut_values("lab", lut_spec[0])
+        fn["lut"] = lambda p: O.interpolate(vals, p, lut_spec[1])
     spaces = ["lab", "hsi", "sct"] if space == "all" else [space]
     px, t0 = 0, time.perf_counter()
     i = 0
@@ -257,9 +260,10 @@ def run_ours(args, wl):
 
     # ---------------- end to end through the public API with HOST buffers
     e2e = None
-    if args.e2e_steps > 0 and space in ("lab", "hsi+sct", "all"):
-        sp1 = "lab" if space in ("lab", "all") else "hsi"
-        fn = {"lab": fast.rgb_to_lab_fast, "hsi": fast.rgb_to_hsi_fast}[sp1]
+    if args.e2e_steps > 0:
+        sp1 = {"lab": "lab", "all": "lab", "hsi+sct": "hsi"}.get(space, "lut")
+        fn = {"lab": fast.rgb_to_lab_fast, "hsi": fast.rgb_to_hsi_fast,
+              "lut": lambda p, out: lut.interpolate(lt, p, args.lut_method, out=out)}[sp1]
         h_in = torch.empty((n_local, 3), dtype=torch.uint8).pin_memory()
         h_in.copy_(xf.cpu())
         h_out = torch.empty((n_local, 3), dtype=torch.float32).pin_memory()
@@ -274,7 +278,8 @@ def run_ours(args, wl):
         dt = parallel.max_over_ranks(time.perf_counter() - t, dev)
         e2e = {"value": n_total * args.e2e_steps / dt / 1e9, "unit": "Gpixels/s",
                "h2d_bytes_per_step": n_total * 3, "d2h_bytes_per_step": n_total * 12,
-               "api": f"paper_1009_0854_b200.fast.rgb_to_{sp1}_fast(numpy pinned, out=numpy pinned)",
+               "api": (f"paper_1009_0854_b200.fast.rgb_to_{sp1}_fast" if sp1 != "lut" else
+                       "paper_1009_0854_b200.lut.interpolate") + "(numpy pinned, out=numpy pinned)",
                "steps": args.e2e_steps, "transform": sp1}
         del h_in, h_out
 
@@ -284,10 +289,11 @@ def run_ours(args, wl):
         from oracle import mact_oracle as O
         sample = [xf[i * 2_073_600:(i + 1) * 2_073_600].cpu().numpy() for i in range(2)]
         threads = O.host_threads()
-        sp = "lab" if space in ("lab", "all") else ("hsi" if space == "hsi+sct" else "lab")
-        px, dt = cpu_port_run(sp, sample, args.cpu_seconds, threads)
+        sp = {"lab": "lab", "all": "lab", "hsi+sct": "hsi"}.get(space, "lut")
+        px, dt = cpu_port_run(sp, sample, args.cpu_seconds, threads, (args.lut_grid, args.lut_method))
+        what = f"rgb_to_{sp}_fast" if sp != "lut" else f"interpolate({args.lut_method}, {args.lut_grid}^3)"
         cpu = {"value": px / dt / 1e9, "unit": "Gpixels/s", "cores": threads, "kind": "port",
-               "sample": f"oracle/mact_oracle.py rgb_to_{sp}_fast (numpy fp64 restatement of the "
+               "sample": f"oracle/mact_oracle.py {what} (numpy fp64 restatement of the "
                          f"reference) over 2,073,600-px slices of the same workload, {px} px in "
                          f"{dt:.1f} s, ThreadPoolExecutor x{threads} (harness.py:92-103 pattern)"}
 

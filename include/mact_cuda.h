@@ -182,6 +182,10 @@ int mact_host_ctx_create(int device, int64_t chunk_px, int nstreams, MactHostCtx
 int mact_host_ctx_destroy(MactHostCtx* ctx);
 int mact_transform_host(MactHostCtx* ctx, int op, const uint8_t* host_rgb, float* host_out,
                         int64_t n, const MactCoeffs* c, int layout);
+/* mact.lut.interpolate over HOST buffers (lut.py:341-350) through the same
+ * chunk pipeline; `lattice` is the device (n^3,4) lattice, linear destination. */
+int mact_lut_interp_host(MactHostCtx* ctx, const float* lattice, int grid_n, int method,
+                         const uint8_t* host_rgb, float* host_out, int64_t n, int layout);
 
 /* ---- calibration ---------------------------------------------------------- */
 /* out = (r, g, b) as fp32 through the same streaming kernel: the achievable

@@ -86,6 +86,17 @@ def check_out(out, lead: tuple, layout: str, device):
     return out
 
 
+def host_out(out, lead: tuple, layout: str):
+    """Validate (or allocate) a numpy float32 output for the host executor."""
+    shape = lead + (3,) if layout == "interleaved" else (3,) + lead
+    if out is None:
+        return np.empty(shape, dtype=np.float32)
+    if not isinstance(out, np.ndarray) or out.dtype != np.float32 or out.shape != shape \
+            or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a C-contiguous float32 array of shape {shape}")
+    return out
+
+
 def to_caller(t, on_dev: bool):
     """Device result back to the caller's world (numpy for host callers)."""
     if on_dev:

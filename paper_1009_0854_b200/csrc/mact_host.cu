@@ -143,12 +143,11 @@ static cudaError_t copy_out(float* host_out, const float* dout, int64_t off, int
                            cudaMemcpyDeviceToHost, st);
 }
 
-extern "C" int mact_transform_host(MactHostCtx* c, int op, const uint8_t* host_rgb, float* host_out,
-                                   int64_t n, const MactCoeffs* cf, int layout) {
-  if (!c || n < 0 || (n > 0 && (!host_rgb || !host_out)) || !cf)
-    return set_error(MACT_EBADARG, "bad argument");
-  if (n == 0) return MACT_OK;
-  if (op < 0 || op > 2) return set_error(MACT_EBADARG, "unknown transform %d", op);
+// The chunk pipeline shared by every host entry point; `launch` runs the
+// kernel of one chunk (device in, device out, pixels, stream).
+template <class Launch>
+static int stream_host(MactHostCtx* c, const uint8_t* host_rgb, float* host_out, int64_t n,
+                       int layout, Launch&& launch) {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(c->device);
@@ -179,13 +178,13 @@ extern "C" int mact_transform_host(MactHostCtx* c, int op, const uint8_t* host_r
     cudaError_t e;
     if (direct) {
       e = cudaMemcpyAsync(c->d_in[s], host_rgb + 3 * off, (size_t)m * 3, cudaMemcpyHostToDevice, st);
-      if (e == cudaSuccess) rc = run_kernel(op, c->d_in[s], c->d_out[s], m, cf, layout, st);
+      if (e == cudaSuccess) rc = launch(c->d_in[s], c->d_out[s], m, st);
       if (rc == MACT_OK && e == cudaSuccess) e = copy_out(host_out, c->d_out[s], off, m, n, layout, st);
     } else {
       if ((rc = drain(s)) != MACT_OK) break;
       par_memcpy(c->h_in[s], host_rgb + 3 * off, (size_t)m * 3);
       e = cudaMemcpyAsync(c->d_in[s], c->h_in[s], (size_t)m * 3, cudaMemcpyHostToDevice, st);
-      if (e == cudaSuccess) rc = run_kernel(op, c->d_in[s], c->d_out[s], m, cf, layout, st);
+      if (e == cudaSuccess) rc = launch(c->d_in[s], c->d_out[s], m, st);
       if (rc == MACT_OK && e == cudaSuccess)
         e = cudaMemcpyAsync(c->h_out[s], c->d_out[s], (size_t)m * 12, cudaMemcpyDeviceToHost, st);
       if (e == cudaSuccess) e = cudaEventRecord(c->done[s], st);
@@ -201,4 +200,27 @@ extern "C" int mact_transform_host(MactHostCtx* c, int op, const uint8_t* host_r
   }
   cudaSetDevice(prev);
   return rc;
+}
+
+extern "C" int mact_transform_host(MactHostCtx* c, int op, const uint8_t* host_rgb, float* host_out,
+                                   int64_t n, const MactCoeffs* cf, int layout) {
+  if (!c || n < 0 || (n > 0 && (!host_rgb || !host_out)) || !cf)
+    return set_error(MACT_EBADARG, "bad argument");
+  if (n == 0) return MACT_OK;
+  if (op < 0 || op > 2) return set_error(MACT_EBADARG, "unknown transform %d", op);
+  return stream_host(c, host_rgb, host_out, n, layout,
+                     [&](const uint8_t* din, float* dout, int64_t m, cudaStream_t st) {
+                       return run_kernel(op, din, dout, m, cf, layout, st);
+                     });
+}
+
+extern "C" int mact_lut_interp_host(MactHostCtx* c, const float* lattice, int grid_n, int method,
+                                    const uint8_t* host_rgb, float* host_out, int64_t n, int layout) {
+  if (!c || !lattice || n < 0 || (n > 0 && (!host_rgb || !host_out)))
+    return set_error(MACT_EBADARG, "bad argument");
+  if (n == 0) return MACT_OK;
+  return stream_host(c, host_rgb, host_out, n, layout,
+                     [&](const uint8_t* din, float* dout, int64_t m, cudaStream_t st) {
+                       return mact_lut_interp(lattice, grid_n, method, din, dout, m, layout, st);
+                     });
 }

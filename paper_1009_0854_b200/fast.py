@@ -97,11 +97,7 @@ def _host_u8(space: str, arr: np.ndarray, cfg: MactConfig, out, layout: str):
     src = np.ascontiguousarray(arr)
     lead = src.shape[:-1]
     n = int(np.prod(lead, dtype=np.int64)) if lead else 1
-    shape = lead + (3,) if layout == "interleaved" else (3,) + lead
-    if out is None:
-        out = np.empty(shape, dtype=np.float32)
-    elif out.dtype != np.float32 or out.shape != shape or not out.flags.c_contiguous:
-        raise ValueError(f"out must be a C-contiguous float32 array of shape {shape}")
+    out = _dev.host_out(out, lead, layout)
     dev = torch.cuda.current_device()
     ctx = _dev.host_ctx(dev)
     _lib.call("mact_transform_host", ctx, _lib.SPACES[space], _dev.np_ptr(src), _dev.np_ptr(out),

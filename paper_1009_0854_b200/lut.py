@@ -129,6 +129,23 @@ def build_cache(lut: Lut3D) -> Lut3D:
                  _device=lut._device)
 
 
+def _host_interp(lut: Lut3D, method_code: int, arr: np.ndarray, out, layout: str):
+    """numpy uint8 -> numpy fp32 through the native chunked H2D/kernel/D2H executor."""
+    import torch
+
+    _dev.require_cuda()
+    src = np.ascontiguousarray(arr)
+    lead = src.shape[:-1]
+    n = int(np.prod(lead, dtype=np.int64)) if lead else 1
+    out = _dev.host_out(out, lead, layout)
+    dev = torch.cuda.current_device()
+    lat = lut.lattice(torch.device("cuda", dev))
+    torch.cuda.current_stream().synchronize()          # the executor runs on its own streams
+    _lib.call("mact_lut_interp_host", _dev.host_ctx(dev), lat.data_ptr(), lut.grid_n, method_code,
+              _dev.np_ptr(src), _dev.np_ptr(out), n, _lib.LAYOUTS[layout])
+    return out
+
+
 def interpolate(lut: Lut3D, pixels, method: str = "tetrahedral", variant: str = "standard", *,
                 out=None, layout: str = "interleaved"):
     """Interpolate destination triples for RGB in [0, 255] (lut.py:341-350)."""
@@ -137,10 +154,16 @@ def interpolate(lut: Lut3D, pixels, method: str = "tetrahedral", variant: str = 
         raise ValueError(f"unknown variant {variant!r}")
     if variant == "caching" and lut.cache is None:
         raise CacheMissing("caching interpolation requested without a cache; call build_cache first")
+    if layout not in _lib.LAYOUTS:
+        raise ValueError(f"unknown layout {layout!r}")
+    mask = sum(1 << c for c, ang in enumerate(lut.angular_mask) if ang)
+    if not mask and not _dev.is_device_tensor(pixels):
+        arr = np.asarray(pixels)
+        if arr.dtype == np.uint8 and arr.ndim >= 1 and arr.shape[-1] == 3:
+            return _host_interp(lut, m, arr, out, layout)
     t, lead, on_dev = _u8_pixels(pixels)
     res = (_dev.check_out(out, lead, layout, t.device) if (out is not None and on_dev)
            else _dev.empty_out(lead, layout, t.device))
-    mask = sum(1 << c for c, ang in enumerate(lut.angular_mask) if ang)
     if mask:
         lat = lut.lattice64(t.device)
         _lib.call("mact_lut_interp_angular", lat.data_ptr(), lut.grid_n, m, mask, t.data_ptr(),

@@ -144,3 +144,24 @@ def test_lut_angular_interp_vs_reference(P, golden, space, n, method):
     for c in range(3):
         err = (_circ(got[:, c], ref[:, c]) if mask[c] else np.abs(got[:, c] - ref[:, c])) / scale[c]
         assert err.max() <= 1e-5, (c, float(err.max()), int(err.argmax()))
+
+
+@pytest.mark.parametrize("grid,method", [(17, "tetrahedral"), (33, "trilinear"), (9, "pyramidal")])
+def test_lut_interp_host_executor(grid, method):
+    """numpy in -> numpy out through mact_lut_interp_host (pageable, pinned, planar)
+    equals the device-tensor path."""
+    from paper_1009_0854_b200 import lut
+    rng = np.random.default_rng(grid)
+    n = (1 << 23) + 12345                         # two executor chunks + a ragged tail
+    px = rng.integers(0, 256, (n, 3), dtype=np.uint8)
+    L = lut.build_lut("lab", grid)
+    ref = lut.interpolate(L, torch.from_numpy(px).cuda(), method).cpu().numpy()
+    got = lut.interpolate(L, px, method)
+    assert isinstance(got, np.ndarray) and got.dtype == np.float32
+    np.testing.assert_array_equal(got, ref)
+    pin_in = torch.empty((n, 3), dtype=torch.uint8).pin_memory()
+    pin_in.numpy()[...] = px
+    pin_out = torch.empty((n, 3), dtype=torch.float32).pin_memory()
+    lut.interpolate(L, pin_in.numpy(), method, out=pin_out.numpy())
+    np.testing.assert_array_equal(pin_out.numpy(), ref)
+    np.testing.assert_array_equal(lut.interpolate(L, px[:5000], method, layout="planar").T, ref[:5000])
