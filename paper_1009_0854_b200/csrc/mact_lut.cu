@@ -29,6 +29,9 @@
 #ifndef MACT_LUT_SIN
 #define MACT_LUT_SIN 3
 #endif
+#ifndef MACT_LUT33_TRI_PB
+#define MACT_LUT33_TRI_PB 1
+#endif
 
 namespace mact {
 
@@ -290,17 +293,6 @@ __device__ __forceinline__ void st_async_v4(uint32_t addr, float4 v, uint32_t mb
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
-__device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x100000u)
-      : "memory");
-}
 
 template <int METHOD>
 __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
@@ -328,60 +320,84 @@ __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
     const float4 v = __ldg(lat4 + i);
     lat_c[i] = comp == 0 ? v.x : comp == 1 ? v.y : v.z;
   }
-  const int t4 = 4 * (int)threadIdx.x;                   // first pixel of this thread in a step
-  const uint32_t owner = t4 < 1368 ? 0 : (t4 < 2732 ? 1 : 2);
-  const int off = t4 - lut33_range_start(owner);
-  // my component's slot in the owner's planar block (buffer 0) and the owner's full barriers
-  const uint32_t dst0 = mapa_u32(smem_u32(planar + comp * PLANE + off), owner);
-  const uint32_t ofull0 = mapa_u32(smem_u32(&full[0]), owner);
+  // Two warp groups of 512 threads alternate steps: group g owns buffer g and
+  // runs steps it = g, g+2, ..., so one group's gathers overlap the other's
+  // exchange wait, interleave and store (a named barrier per group, no
+  // CTA-wide barrier in the loop).  Each thread handles two 4-pixel chunks
+  // of a step: pixels 4*tg and 2048 + 4*tg.
+  const int grp = (int)(threadIdx.x >> 9), tg = (int)(threadIdx.x & 511);
+  uint32_t owner[2], dst[2], ofull[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int t4 = 4 * tg + 2048 * h;
+    owner[h] = t4 < 1368 ? 0 : (t4 < 2732 ? 1 : 2);
+    const int off = t4 - lut33_range_start(owner[h]);
+    dst[h] = mapa_u32(smem_u32(planar + grp * PBUF + comp * PLANE + off), owner[h]);
+    ofull[h] = mapa_u32(smem_u32(&full[grp]), owner[h]);
+  }
   const int r0 = lut33_range_start(comp);
   const int rlen = (comp == 2 ? kLut33Step : lut33_range_start(comp + 1)) - r0;
   const uint32_t full_bytes = (uint32_t)rlen * 3u * 4u;
   cluster.sync();                                        // barriers initialised, lattices staged
   const uint32_t* in_w = reinterpret_cast<const uint32_t*>(rgb);
-  // input words of the next step are loaded one step ahead
-  uint32_t n0 = 0, n1 = 0, n2 = 0;
-  if (cl < nsteps) {
-    const int64_t g = cl * kLut33Threads + threadIdx.x;
-    n0 = __ldg(in_w + 3 * g); n1 = __ldg(in_w + 3 * g + 1); n2 = __ldg(in_w + 3 * g + 2);
-  }
-  int it = 0;
-  for (int64_t step = cl; step < nsteps; step += ncl, ++it) {
-    const int buf = it & 1;
-    const uint32_t use = (uint32_t)it >> 1;
-    const uint32_t w0 = n0, w1 = n1, w2 = n2;
-    if (step + ncl < nsteps) {
-      const int64_t g = (step + ncl) * kLut33Threads + threadIdx.x;
-      n0 = __ldg(in_w + 3 * g); n1 = __ldg(in_w + 3 * g + 1); n2 = __ldg(in_w + 3 * g + 2);
+  // input words of the group's next step are loaded one step ahead
+  uint32_t nw[2][3] = {};
+  auto load_words = [&](int64_t step) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t g = step * kLut33Threads + h * 512 + tg;
+      nw[h][0] = __ldg(in_w + 3 * g); nw[h][1] = __ldg(in_w + 3 * g + 1); nw[h][2] = __ldg(in_w + 3 * g + 2);
     }
-    const uint32_t ch[12] = {byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), byte_of(w0, 3),
-                             byte_of(w1, 0), byte_of(w1, 1), byte_of(w1, 2), byte_of(w1, 3),
-                             byte_of(w2, 0), byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3)};
-    int idx[4][K];
-    float w[4][K], v[4][K];
+  };
+  if (cl + grp * ncl < nsteps) load_words(cl + grp * ncl);
+  for (int64_t it = grp; cl + it * ncl < nsteps; it += 2) {
+    const int64_t step = cl + it * ncl;
+    const uint32_t use = (uint32_t)(it >> 1);
+    uint32_t cw[2][3];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) lut_nodes<N, METHOD>(ch[3 * q], ch[3 * q + 1], ch[3 * q + 2], idx[q], w[q]);
+    for (int h = 0; h < 2; ++h) { cw[h][0] = nw[h][0]; cw[h][1] = nw[h][1]; cw[h][2] = nw[h][2]; }
+    if (step + 2 * ncl < nsteps) load_words(step + 2 * ncl);
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t ch[12] = {byte_of(cw[h][0], 0), byte_of(cw[h][0], 1), byte_of(cw[h][0], 2), byte_of(cw[h][0], 3),
+                               byte_of(cw[h][1], 0), byte_of(cw[h][1], 1), byte_of(cw[h][1], 2), byte_of(cw[h][1], 3),
+                               byte_of(cw[h][2], 0), byte_of(cw[h][2], 1), byte_of(cw[h][2], 2), byte_of(cw[h][2], 3)};
+      // all node loads of a batch in flight together; trilinear (K = 8) goes
+      // 2 pixels at a time so a 1024-thread CTA stays within 64 registers
+      constexpr int PB = K > 6 ? MACT_LUT33_TRI_PB : 4;
+      float a[4];
 #pragma unroll
-      for (int j = 0; j < K; ++j) v[q][j] = lat_c[idx[q][j]];
-    float a[4];
+      for (int q0 = 0; q0 < 4; q0 += PB) {
+        int idx[PB][K];
+        float w[PB][K], v[PB][K];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      a[q] = w[q][0] * v[q][0];
+        for (int q = 0; q < PB; ++q)
+          lut_nodes<N, METHOD>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], idx[q], w[q]);
 #pragma unroll
-      for (int j = 1; j < K; ++j) a[q] = fmaf(w[q][j], v[q][j], a[q]);
+        for (int q = 0; q < PB; ++q)
+#pragma unroll
+          for (int j = 0; j < K; ++j) v[q][j] = lat_c[idx[q][j]];
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+          a[q0 + q] = w[q][0] * v[q][0];
+#pragma unroll
+          for (int j = 1; j < K; ++j) a[q0 + q] = fmaf(w[q][j], v[q][j], a[q0 + q]);
+        }
+      }
+      // the owner's buffer must have been consumed (its use - 1) before it is
+      // refilled.  Plain CTA-scope-acquire waits, as CUTLASS's cluster pipelines
+      // use: an .acquire.cluster wait compiles to CCTL.IVALL (L1 invalidate),
+      // which cost 21 % of the stall samples; the st.async payload is made
+      // visible by the mbarrier's transaction completion itself.
+      if (use >= 1) mbar_wait(&empty[owner[h] * 2 + grp], (use - 1) & 1);
+      st_async_v4(dst[h], make_float4(a[0], a[1], a[2], a[3]), ofull[h]);
     }
-    // owner's buffer `buf` must have been consumed (its use - 1), then send my component
-    if (it >= 2) mbar_wait_acq_cluster(&empty[owner * 2 + buf], (use - 1) & 1);
-    st_async_v4(dst0 + (uint32_t)(buf * PBUF * 4), make_float4(a[0], a[1], a[2], a[3]),
-                ofull0 + (uint32_t)(buf * 8));
     // owner role: wait for the three components of my range, interleave, store
-    if (threadIdx.x == 0) mbar_arrive_expect_tx(&full[buf], full_bytes);
-    mbar_wait_acq_cluster(&full[buf], use & 1);
-    const float* pl = planar + buf * PBUF;
-    float* sg = stage + buf * SBUF;                      // free: drained before the last barrier
-    for (int i = threadIdx.x; 4 * i < rlen; i += blockDim.x) {   // interleave 4 pixels per thread
+    if (tg == 0) mbar_arrive_expect_tx(&full[grp], full_bytes);
+    mbar_wait(&full[grp], use & 1);
+    const float* pl = planar + grp * PBUF;
+    float* sg = stage + grp * SBUF;                      // free: drained before the last barrier
+    for (int i = tg; 4 * i < rlen; i += 512) {           // interleave 4 pixels per thread
       const float4 c0 = *reinterpret_cast<const float4*>(pl + 4 * i);
       const float4 c1 = *reinterpret_cast<const float4*>(pl + PLANE + 4 * i);
       const float4 c2 = *reinterpret_cast<const float4*>(pl + 2 * PLANE + 4 * i);
@@ -391,16 +407,16 @@ __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
       d[2] = make_float4(c2.z, c0.w, c1.w, c2.w);
     }
     fence_proxy_async_smem();
-    if (threadIdx.x == 0) bulk_wait_read<0>();           // stage[buf ^ 1] (previous step) drained
-    __syncthreads();                                     // stage written, planar[buf] read
-    if (threadIdx.x == 0) {
+    if (tg == 0) bulk_wait_read<0>();                    // stage[grp] of this group's last step drained
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(512) : "memory");   // stage written, planar read
+    if (tg == 0) {
       bulk_s2g(out + 3 * (step * kLut33Step + r0), sg, (uint32_t)rlen * 12u);
       bulk_commit();
 #pragma unroll
-      for (uint32_t c = 0; c < 3; ++c) mbar_arrive_cluster(mapa_u32(smem_u32(&empty[comp * 2 + buf]), c));
+      for (uint32_t c = 0; c < 3; ++c) mbar_arrive_cluster(mapa_u32(smem_u32(&empty[comp * 2 + grp]), c));
     }
   }
-  if (threadIdx.x == 0) bulk_wait<0>();
+  if (tg == 0) bulk_wait<0>();
   cluster.sync();                                        // partners may still signal / write my smem
 }
 
@@ -457,18 +473,12 @@ static int launch_interp(const float* lat, const uint8_t* rgb, float* out, int64
   Outs outs{{out, nullptr, nullptr}};
   LutParams p{reinterpret_cast<const float4*>(lat)};
   // 17^3: (c0,c1)+c2 smem planes, 59 KB; 9^3: 8 bank-private float4 copies,
-  // 93 KB; 16 compute warps per CTA.  33^3: the component-split cluster wins
-  // for trilinear/prism/pyramidal (60/66/70 vs 42-60 Gpix/s through L2);
-  // tetrahedral's 4 gathers leave the L2 path level with it (74 vs 72), and
-  // the cluster repeats the node selection in all three CTAs (ALU-bound).
-#ifdef MACT_LUT33_TET_CLUSTER
+  // 93 KB; 16 compute warps per CTA.  33^3: the component-split cluster for
+  // every method (64/83/86/88 Gpix/s against 42/52/60/74 gathering from L2);
+  // the L2 streaming kernel remains its fallback for planar output, unaligned
+  // buffers and the tail.
   if constexpr (N == 33)
-#else
-  if constexpr (N == 33 && METHOD != MACT_LUT_TETRAHEDRAL)
-#endif
     return launch_lut33_comp<METHOD>(lat, rgb, out, n, planar, st);
-  else if constexpr (N == 33)
-    return launch_stream_t<OpLut<N, METHOD>, 16, 1, 3, 1>(rgb, outs, n, planar, p, st, "lut_interp");
   else
     return launch_stream_t<OpLut<N, METHOD>, MACT_LUT_NW, (N <= 9 ? 2 : 1), MACT_LUT_SIN, 1>(
         rgb, outs, n, planar, p, st, "lut_interp");
