@@ -39,7 +39,8 @@ enum {
   MACT_ECUDA = 3
 };
 
-enum { MACT_SPACE_LAB = 0, MACT_SPACE_HSI = 1, MACT_SPACE_SCT = 2 };
+enum { MACT_SPACE_LAB = 0, MACT_SPACE_HSI = 1, MACT_SPACE_SCT = 2,
+       MACT_SPACE_HSI_ARCCOS = 3 /* mact_exact only: exact.rgb_to_hsi_arccos (exact.py:104-116) */ };
 enum { MACT_LAYOUT_INTERLEAVED = 0, MACT_LAYOUT_PLANAR = 1 };
 enum { MACT_DTYPE_U8 = 0, MACT_DTYPE_F32 = 1, MACT_DTYPE_F64 = 2 };
 enum {
@@ -162,6 +163,34 @@ size_t mact_err_workspace_bytes(void);
 int mact_err_reduce(const MactErrSpec* spec, const MactCoeffs* c, const uint8_t* rgb,
                     int64_t cube_start, int64_t n, int64_t index_base, MactErrStats* out,
                     void* workspace, void* stream);
+
+/* ---- elementwise building blocks (fp64 device arrays) --------------------- */
+/* The reference's scalar approximant functions, bit-identical to numpy:
+ *   MACT_FN_FORM        out = a(x) (b_deg < 0) or a(x)/b(x)       fast.cbrt_fast, fast.py:81-83
+ *                       (approximants.py:55-82; *degenerate = 1 if any |b(x)| < 1e-300)
+ *   MACT_FN_ATAN_SQRT3  out = sign(x) a(|x|)                      fast.atan_sqrt3_fast, fast.py:118-122
+ *   MACT_FN_ACOS        out = x < 0.5 ? a(x) : b(sqrt(max(1-x,0)))  fast.acos_fast, fast.py:151-162
+ *                       (a = ACOS_HALF, b = ASIN_HALF)
+ *   MACT_FN_ATAN_UNIT   out = atan(x/y) split fits, x = g, y = r;   fast.atan_unit_fast, fast.py:165-185
+ *                       NaN at g = r = 0 (a = ATAN_F, b = ATAN_G)
+ * a[i], b[i] are ascending coefficients; degrees <= 7. */
+enum { MACT_FN_FORM = 0, MACT_FN_ATAN_SQRT3 = 1, MACT_FN_ACOS = 2, MACT_FN_ATAN_UNIT = 3 };
+typedef struct MactApproxSpec {
+  int32_t fn, a_deg, b_deg, _pad;
+  double a[8], b[8];
+} MactApproxSpec;
+int mact_approx_eval(const MactApproxSpec* spec, const double* x, const double* y, double* out,
+                     int64_t n, int32_t* degenerate /* device, may be NULL */, void* stream);
+
+/* exact.py:52-83 elementwise, fp64:
+ *   MACT_ELEM_INVERSE_GAMMA  out0 = inverse_gamma(in0)               (exact.py:52-57)
+ *   MACT_ELEM_RGB_TO_XYZ     (out0, out1, out2) = rgb_to_xyz(in0..2)  (exact.py:60-66)
+ *   MACT_ELEM_LAB_F          out0 = lab_f(in0)                       (exact.py:69-72)
+ *   MACT_ELEM_XYZ_TO_LAB     out0 (n,3) = xyz_to_lab(in0..2)         (exact.py:75-83) */
+enum { MACT_ELEM_INVERSE_GAMMA = 0, MACT_ELEM_RGB_TO_XYZ = 1, MACT_ELEM_LAB_F = 2,
+       MACT_ELEM_XYZ_TO_LAB = 3 };
+int mact_exact_elem(int op, const double* in0, const double* in1, const double* in2,
+                    double* out0, double* out1, double* out2, int64_t n, void* stream);
 
 /* ---- pixel generators ---------------------------------------------------- */
 /* harness.cube_chunk (harness.py:35-46) on device: rgb[i] = cube pixel start+i */

@@ -51,6 +51,13 @@ LAB_LINEAR_OFFSET = 16.0 / 116.0
 # Coefficient tables (approximants.py:168-265), published decimal strings
 # parsed to the nearest double.  Tuples are a_0 .. a_n (ascending powers).
 # ---------------------------------------------------------------------------
+# Cube-root polynomials on [0, 1] (approximants.py:168-177; PAPER Table 1).
+CBRT_POLYS: Dict[int, Tuple[str, ...]] = {
+    2: ("1.268979e-01", "2.393873", "-1.647669"),
+    3: ("9.787826e-02", "4.057495", "-7.388864", "4.331370"),
+    4: ("8.111133e-02", "5.926004", "-2.017165e+01", "2.833070e+01", "-1.324728e+01"),
+    5: ("7.002910e-02", "7.961214", "-4.329352e+01", "1.063182e+02", "-1.135685e+02", "4.358268e+01"),
+}
 CBRT_RATIONALS: Dict[Tuple[int, int], Tuple[Tuple[str, ...], Tuple[str, ...]]] = {
     (2, 2): (("6.309655e-03", "5.785782e-01", "1.591005"),
              ("4.482646e-02", "1.175862", "9.596879e-01")),
@@ -322,6 +329,18 @@ def rgb_to_lab_fast(pixels, cfg: OracleConfig = DEFAULT):
     fy = _lab_f_fast(y / WHITE[1], cfg)
     fz = _lab_f_fast(z / WHITE[2], cfg)
     return stack3(116.0 * fy - 16.0, 500.0 * (fx - fy), 200.0 * (fy - fz))
+
+
+def cbrt_fast(t, num, den=None):
+    """fast.py:81-83 -> approximants.eval_poly / eval_rational (approximants.py:55-82):
+    numerator / denominator Horner, one division (ValueError stands in for
+    DegenerateDenominator on |q| < 1e-300)."""
+    if den is None:
+        return horner(num, t)
+    q = horner(den, t)
+    if np.any(np.abs(q) < 1e-300):
+        raise ValueError("denominator vanished inside evaluation batch")
+    return horner(num, t) / q
 
 
 def atan_sqrt3_fast(x, coeffs):

@@ -51,6 +51,15 @@ class MactErrSpec(C.Structure):
                 ("ref_array", C.c_void_p), ("ref_dtype", C.c_int32), ("_pad", C.c_int32)]
 
 
+class MactApproxSpec(C.Structure):
+    _fields_ = [("fn", C.c_int32), ("a_deg", C.c_int32), ("b_deg", C.c_int32), ("_pad", C.c_int32),
+                ("a", _c_double8), ("b", _c_double8)]
+
+
+FN_FORM, FN_ATAN_SQRT3, FN_ACOS, FN_ATAN_UNIT = 0, 1, 2, 3
+ELEM_INVERSE_GAMMA, ELEM_RGB_TO_XYZ, ELEM_LAB_F, ELEM_XYZ_TO_LAB = 0, 1, 2, 3
+SPACE_HSI_ARCCOS = 3
+
 _vp, _i, _i64, _u64 = C.c_void_p, C.c_int, C.c_int64, C.c_uint64
 _SIGNATURES = {
     "mact_lab_fast": (_i, [_vp, _i, _vp, _i64, C.POINTER(MactCoeffs), _i, _vp]),
@@ -69,6 +78,8 @@ _SIGNATURES = {
                              _i64, _vp, _vp, _vp]),
     "mact_cube_fill": (_i, [_vp, _i64, _i64, _vp]),
     "mact_call_counts": (_i, [_vp, _vp]),
+    "mact_approx_eval": (_i, [C.POINTER(MactApproxSpec), _vp, _vp, _vp, _i64, _vp, _vp]),
+    "mact_exact_elem": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]),
     "mact_probe_expand": (_i, [_vp, _vp, _i64, _vp]),
     "mact_host_ctx_create": (_i, [_i, _i64, _i, C.POINTER(_vp)]),
     "mact_host_ctx_destroy": (_i, [_vp]),

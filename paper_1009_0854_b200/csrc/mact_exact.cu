@@ -22,7 +22,8 @@ __device__ __forceinline__ double load_c(const T* p, int64_t i) { return (double
 __device__ __forceinline__ void exact_px(int space, double r, double g, double b, double* o) {
   if (space == MACT_SPACE_LAB) lab_exact_d(r, g, b, o);
   else if (space == MACT_SPACE_HSI) hsi_exact_d(r, g, b, o);
-  else sct_exact_d(r, g, b, o);
+  else if (space == MACT_SPACE_SCT) sct_exact_d(r, g, b, o);
+  else hsi_arccos_d(r, g, b, o);
 }
 
 template <typename TI, typename TO>
@@ -191,7 +192,7 @@ using namespace mact;
 
 extern "C" int mact_exact(int space, const void* rgb, int in_dtype, void* out, int out_dtype,
                           int64_t n, void* stream) {
-  if (space < 0 || space > 2) return set_error(MACT_EBADARG, "unknown space %d", space);
+  if (space < 0 || space > MACT_SPACE_HSI_ARCCOS) return set_error(MACT_EBADARG, "unknown space %d", space);
   if (n < 0 || (n > 0 && (!rgb || !out))) return set_error(MACT_EBADARG, "bad argument");
   if (n == 0) return MACT_OK;
   cudaStream_t st = (cudaStream_t)stream;

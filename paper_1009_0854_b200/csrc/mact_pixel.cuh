@@ -329,6 +329,21 @@ __device__ __forceinline__ void hsi_exact_d(double r, double g, double b, double
   o[1] = total > 0.0 ? 1.0 - 3.0 * low / total : 0.0;
   o[2] = total / 3.0;
 }
+// exact.rgb_to_hsi_arccos (exact.py:104-116): inverse-cosine hue formula.
+__device__ __forceinline__ void hsi_arccos_d(double r, double g, double b, double* o) {
+  r /= 255.0; g /= 255.0; b /= 255.0;
+  const double num = 0.5 * ((r - g) + (r - b));
+  const double den_sq = (r - g) * (r - g) + (r - b) * (g - b);
+  const double ratio = num / sqrt(den_sq);
+  double h = acos(fmin(fmax(ratio, -1.0), 1.0));
+  if (b > g) h = kTwoPi - h;
+  if (!(den_sq > 0.0)) h = __longlong_as_double(0x7ff8000000000000ll);
+  const double total = r + g + b;
+  const double low = fmin(fmin(r, g), b);
+  o[0] = h;
+  o[1] = total > 0.0 ? 1.0 - 3.0 * low / total : 0.0;
+  o[2] = total / 3.0;
+}
 __device__ __forceinline__ void sct_exact_d(double r, double g, double b, double* o) {
   const double len = sqrt(r * r + g * g + b * b);
   o[0] = len;

@@ -1,6 +1,8 @@
 """Exact (fp64) transforms and distances on B200 — drop-in for ``mact.exact``.
 
     rgb_to_lab_exact / rgb_to_hsi_exact / rgb_to_sct_exact   (exact.py:86-149)
+    rgb_to_hsi_arccos                                        (exact.py:104-116)
+    inverse_gamma / rgb_to_xyz / lab_f / xyz_to_lab          (exact.py:52-83)
     sct_to_rgb                                               (exact.py:152-160)
     lab_distance / hsi_distance / sct_distance_indirect      (exact.py:163-190)
 
@@ -51,13 +53,73 @@ def rgb_to_sct_exact(pixels, *, out_dtype: str = "float64"):
     return _exact("sct", pixels, out_dtype)
 
 
+def rgb_to_hsi_arccos(pixels, *, out_dtype: str = "float64"):
+    """RGB -> HSI via the inverse-cosine hue formula (exact.py:104-116)."""
+    import torch
+
+    t, code, lead, on_dev = _dev.as_device_pixels(pixels)
+    tdt = torch.float64 if out_dtype == "float64" else torch.float32
+    res = torch.empty(lead + (3,), dtype=tdt, device=t.device)
+    _lib.call("mact_exact", _lib.SPACE_HSI_ARCCOS, t.data_ptr(), code, res.data_ptr(),
+              _lib.DTYPE_F64 if out_dtype == "float64" else _lib.DTYPE_F32, t.numel() // 3,
+              _dev.stream_ptr())
+    return _dev.to_caller(res, on_dev)
+
+
+def _f64_args(*xs):
+    """Broadcast fp64 device copies of the arguments; on_dev if the first was a CUDA tensor."""
+    import torch
+
+    on_dev = _dev.is_device_tensor(xs[0])
+    ts = [_as_f64_device(x)[0] for x in xs]
+    if len(ts) > 1:
+        ts = [t.contiguous() for t in torch.broadcast_tensors(*ts)]
+    return ts, on_dev
+
+
+def _elem(op: int, *xs, outs: int = 1, stacked: bool = False):
+    import torch
+
+    ts, on_dev = _f64_args(*xs)
+    shape = ts[0].shape + ((3,) if stacked else ())
+    res = [torch.empty(shape, dtype=torch.float64, device=ts[0].device) for _ in range(outs)]
+    ptr = [t.data_ptr() for t in ts] + [None] * (3 - len(ts))
+    optr = [r.data_ptr() for r in res] + [None] * (3 - len(res))
+    _lib.call("mact_exact_elem", op, *ptr, *optr, ts[0].numel(), _dev.stream_ptr())
+    out = [_dev.to_caller(r, on_dev) for r in res]
+    return out[0] if outs == 1 else tuple(out)
+
+
+def inverse_gamma(k_prime):
+    """Nonlinear 0..1 channel value -> linear intensity, BT.709 (exact.py:52-57)."""
+    return _elem(_lib.ELEM_INVERSE_GAMMA, k_prime)
+
+
+def rgb_to_xyz(r, g, b):
+    """Linear RGB in [0,1] -> (X, Y, Z) (exact.py:60-66)."""
+    return _elem(_lib.ELEM_RGB_TO_XYZ, r, g, b, outs=3)
+
+
+def lab_f(t):
+    """Lightness kernel: cube root above the knee, linear below (exact.py:69-72)."""
+    return _elem(_lib.ELEM_LAB_F, t)
+
+
+def xyz_to_lab(x, y, z):
+    """CIEXYZ -> CIELAB, D65 white, stacked (..., 3) (exact.py:75-83)."""
+    return _elem(_lib.ELEM_XYZ_TO_LAB, x, y, z, stacked=True)
+
+
 def _as_f64_device(x):
     import torch
 
     if _dev.is_device_tensor(x):
         return x.to(torch.float64).contiguous(), True
     _dev.require_cuda()
-    return torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64))).cuda(), False
+    a = np.asarray(x, dtype=np.float64)
+    if not a.flags.c_contiguous:                     # (np.ascontiguousarray would make 0-d arrays 1-d)
+        a = a.copy()
+    return torch.from_numpy(a).cuda(), False
 
 
 def sct_to_rgb(pixels):

@@ -29,6 +29,7 @@ import numpy as np
 
 from . import _dev, _lib
 from .approximants import Rational, TargetFn, hsi_refit, registry_get
+from .errors import DegenerateDenominator, UndefinedAngle
 
 TWO_PI = 2.0 * np.pi
 
@@ -127,6 +128,59 @@ def transform(space: str, pixels, cfg: MactConfig = DEFAULT_CONFIG, *, out=None,
         out[...] = res.cpu().numpy()
         return out
     return _dev.to_caller(res, on_dev)
+
+
+# ------------------------------------------------ scalar approximant functions
+def _approx(fn: int, a, b, x, y=None):
+    """Evaluate one approximant family elementwise on the GPU (mact_approx_eval)."""
+    import torch
+
+    from .exact import _f64_args
+
+    ts, on_dev = _f64_args(x) if y is None else _f64_args(x, y)
+    spec = _lib.MactApproxSpec()
+    spec.fn = fn
+    spec.a_deg = _fill(spec.a, a)
+    spec.b_deg = _fill(spec.b, b) if b is not None else -1
+    out = torch.empty(ts[0].shape, dtype=torch.float64, device=ts[0].device)
+    flag = torch.zeros(1, dtype=torch.int32, device=ts[0].device)
+    _lib.call("mact_approx_eval", spec, ts[0].data_ptr(), ts[1].data_ptr() if y is not None else None,
+              out.data_ptr(), ts[0].numel(), flag.data_ptr(), _dev.stream_ptr())
+    if fn == _lib.FN_FORM and b is not None and int(flag.item()):
+        raise DegenerateDenominator("denominator vanished inside evaluation batch")
+    return _dev.to_caller(out, on_dev)
+
+
+def _form_coeffs(form):
+    if isinstance(form, Rational):
+        return form.numerator.coeffs, form.denominator.coeffs
+    return form.coeffs, None
+
+
+def cbrt_fast(t, approx):
+    """Approximate t**(1/3) with ``approx`` (polynomial or rational) (fast.py:81-83;
+    approximants.eval_poly / eval_rational, approximants.py:55-82)."""
+    a, b = _form_coeffs(approx.form)
+    return _approx(_lib.FN_FORM, a, b, t)
+
+
+def atan_sqrt3_fast(x, approx):
+    """arctan(sqrt(3) x) for |x| <= 1, odd-extended (fast.py:118-122)."""
+    return _approx(_lib.FN_ATAN_SQRT3, approx.form.coeffs, None, x)
+
+
+def acos_fast(x, cfg: MactConfig = DEFAULT_CONFIG):
+    """arccos on [0, 1]: direct fit below 0.5, folded arcsin at and above (fast.py:151-162)."""
+    return _approx(_lib.FN_ACOS, cfg.acos_approx.form.coeffs, cfg.asin_approx.form.coeffs, x)
+
+
+def atan_unit_fast(g, r, cfg: MactConfig = DEFAULT_CONFIG):
+    """arctan(g/r) for g, r >= 0 via the split-domain fits; NaN at g = r = 0, and
+    UndefinedAngle for that scalar input (fast.py:165-185)."""
+    if np.ndim(g) == 0 and np.ndim(r) == 0 and not _dev.is_device_tensor(g) \
+            and float(g) == 0.0 and float(r) == 0.0:
+        raise UndefinedAngle("arctan(g/r) undefined at g = r = 0")
+    return _approx(_lib.FN_ATAN_UNIT, cfg.atan_f_approx.form.coeffs, cfg.atan_g_approx.form.coeffs, g, r)
 
 
 def rgb_to_lab_fast(pixels, cfg: MactConfig = DEFAULT_CONFIG, **kw):

@@ -82,8 +82,45 @@ def call_probs(harness) -> dict:
             for k in names}
 
 
+def elem_vectors() -> dict:
+    """Inputs and reference outputs of the scalar building blocks (fast.py:81-185,
+    exact.py:52-83) -> elem_outputs.npz."""
+    from mact import approximants as A, exact, fast
+    from mact.fast import MactConfig
+
+    t = np.r_[np.linspace(-0.25, 1.25, 3001), 0.008856, np.nextafter(0.008856, 1), 0.0, -0.0, 1.0, np.nan]
+    x = np.r_[np.linspace(-1.25, 1.25, 2501), 0.5, np.nextafter(0.5, 0), 1.0, -0.0, np.nan]
+    rng = np.random.default_rng(41)
+    g = np.r_[rng.random(2000) * 3, 0.0, 0.0, 1.0, 2.0, 0.5, np.nan, 0.0]
+    r = np.r_[rng.random(2000) * 3, 0.0, 1.0, 0.0, 2.0, 0.5, 1.0, np.nan]
+    out = {"t": t, "x": x, "g": g, "r": r}
+    for n, m in [(2, 2), (3, 4), (4, 4)]:
+        out[f"cbrt_{n}{m}"] = fast.cbrt_fast(t, A.registry_get(A.TargetFn.CBRT, (n, m)))
+    for n in (3, 5):
+        out[f"cbrt_poly{n}"] = fast.cbrt_fast(t, A.registry_get(A.TargetFn.CBRT, (n,)))
+    for n in (2, 3, 4, 5):
+        out[f"atan_sqrt3_{n}"] = fast.atan_sqrt3_fast(x, fast._atan_unit_interval(n))
+    for d in [(4, 4, 4), (5, 5, 5), (4, 5, 4)]:
+        cfg = MactConfig(sct_degrees=d)
+        key = "".join(map(str, d))
+        out[f"acos_{key}"] = fast.acos_fast(x, cfg)
+        out[f"atan_unit_{key}"] = fast.atan_unit_fast(g, r, cfg)
+    k = np.r_[np.linspace(0, 1, 2001), 0.081, np.nextafter(0.081, 0)]
+    out["k"] = k
+    out["inverse_gamma"] = exact.inverse_gamma(k)
+    rgb = rng.random((3, 3000))
+    out["rgb_lin"] = rgb
+    out["rgb_to_xyz"] = np.stack(exact.rgb_to_xyz(*rgb))
+    out["lab_f"] = exact.lab_f(t[:-1])
+    out["xyz_to_lab"] = exact.xyz_to_lab(*(rgb * np.array([[0.95], [1.0], [1.09]])))
+    return out
+
+
 def main() -> None:
     sys.path.insert(0, str(REF))
+    if "--elem-only" in sys.argv:
+        np.savez_compressed(OUT / "elem_outputs.npz", **elem_vectors())
+        return
     if "--call-probs-only" in sys.argv:     # refresh one figure without the full sweep
         from mact import harness
         fig = json.loads((OUT / "figures.json").read_text())
@@ -151,6 +188,7 @@ def main() -> None:
     arrays["probe_offsets"] = np.array(offsets)
     lut.save_lut(lut.build_lut("hsi", 9), OUT / "ref_hsi9.mlut")       # MLUT format fixture
     np.savez_compressed(OUT / "reference_outputs.npz", **arrays)
+    np.savez_compressed(OUT / "elem_outputs.npz", **elem_vectors())
     if "--arrays-only" in sys.argv:
         print(f"arrays written in {time.time() - t0:.1f}s")
         return

@@ -50,9 +50,9 @@ def test_struct_layout_matches_c(tmp_path):
 #include <stddef.h>
 #include "mact_cuda.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(MactCoeffs), offsetof(MactCoeffs, atan_g),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu\\n", sizeof(MactCoeffs), offsetof(MactCoeffs, atan_g),
          sizeof(MactErrStats), sizeof(MactErrSpec), offsetof(MactErrSpec, ref_array),
-         offsetof(MactErrSpec, ref_dtype));
+         offsetof(MactErrSpec, ref_dtype), sizeof(MactApproxSpec), offsetof(MactApproxSpec, b));
   return 0;
 }
 """)
@@ -61,7 +61,8 @@ int main(void) {
     vals = list(map(int, subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()))
     assert vals == [C.sizeof(_lib.MactCoeffs), _lib.MactCoeffs.atan_g.offset,
                     C.sizeof(_lib.MactErrStats), C.sizeof(_lib.MactErrSpec),
-                    _lib.MactErrSpec.ref_array.offset, _lib.MactErrSpec.ref_dtype.offset]
+                    _lib.MactErrSpec.ref_array.offset, _lib.MactErrSpec.ref_dtype.offset,
+                    C.sizeof(_lib.MactApproxSpec), _lib.MactApproxSpec.b.offset]
 
 
 def test_bad_arguments_fail_without_touching_the_device(lib):

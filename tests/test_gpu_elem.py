@@ -1,0 +1,90 @@
+"""GPU parity of the reference's scalar building blocks (mact_approx_eval,
+mact_exact_elem, mact_exact HSI-arccos) against the reference's own outputs
+(tests/golden/elem_outputs.npz, reference_outputs.npz)."""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def elem():
+    return np.load(os.path.join(HERE, "golden", "elem_outputs.npz"))
+
+
+@pytest.fixture(scope="module")
+def M():
+    from paper_1009_0854_b200 import _lib, approximants, exact, fast
+    _lib.load()
+    return {"fast": fast, "exact": exact, "A": approximants}
+
+
+def eq(a, b):
+    np.testing.assert_array_equal(np.asarray(a), np.asarray(b))
+
+
+def test_cbrt_fast_bit_exact(M, elem):
+    A, fast = M["A"], M["fast"]
+    for n, m in [(2, 2), (3, 4), (4, 4)]:
+        eq(fast.cbrt_fast(elem["t"], A.registry_get(A.TargetFn.CBRT, (n, m))), elem[f"cbrt_{n}{m}"])
+    for n in (3, 5):
+        eq(fast.cbrt_fast(elem["t"], A.registry_get(A.TargetFn.CBRT, (n,))), elem[f"cbrt_poly{n}"])
+
+
+def test_trig_approximants_bit_exact(M, elem):
+    A, fast = M["A"], M["fast"]
+    for n in (2, 3, 4, 5):
+        eq(fast.atan_sqrt3_fast(elem["x"], A.hsi_refit(n)), elem[f"atan_sqrt3_{n}"])
+    for d in [(4, 4, 4), (5, 5, 5), (4, 5, 4)]:
+        cfg = fast.MactConfig(sct_degrees=d)
+        key = "".join(map(str, d))
+        eq(fast.acos_fast(elem["x"], cfg), elem[f"acos_{key}"])
+        eq(fast.atan_unit_fast(elem["g"], elem["r"], cfg), elem[f"atan_unit_{key}"])
+
+
+def test_device_in_device_out_and_broadcast(M, elem):
+    fast = M["fast"]
+    x = torch.from_numpy(elem["x"]).cuda()
+    y = fast.acos_fast(x)
+    assert isinstance(y, torch.Tensor) and y.is_cuda and y.dtype == torch.float64
+    eq(y.cpu().numpy(), elem["acos_555"])
+    # scalar r broadcast against an array of g
+    g = np.linspace(0, 2, 101)
+    eq(fast.atan_unit_fast(g, 1.0), fast.atan_unit_fast(g, np.ones_like(g)))
+    assert np.asarray(fast.acos_fast(0.25)).shape == ()
+
+
+def test_error_conventions(M):
+    from paper_1009_0854_b200.approximants import Approximant, Polynomial, Rational, TargetFn
+    from paper_1009_0854_b200.errors import DegenerateDenominator, UndefinedAngle
+    fast = M["fast"]
+    bad = Approximant(Rational(Polynomial((1.0,)), Polynomial((1.0, -1.0))), (0.0, 2.0), 0.0, TargetFn.CBRT)
+    with pytest.raises(DegenerateDenominator):
+        fast.cbrt_fast(np.array([0.5, 1.0]), bad)
+    fast.cbrt_fast(np.array([0.5, 0.75]), bad)                     # no vanishing point: fine
+    with pytest.raises(UndefinedAngle):
+        fast.atan_unit_fast(0.0, 0.0)
+    assert np.isnan(fast.atan_unit_fast(np.array([0.0]), np.array([0.0]))[0])
+
+
+def test_exact_building_blocks(M, elem):
+    """libdevice pow/cbrt vs libm: within a few ulp; the rest is bit-exact."""
+    ex = M["exact"]
+    np.testing.assert_allclose(ex.inverse_gamma(elem["k"]), elem["inverse_gamma"], rtol=4e-16, atol=0)
+    eq(np.stack(ex.rgb_to_xyz(*elem["rgb_lin"])), elem["rgb_to_xyz"])
+    np.testing.assert_allclose(ex.lab_f(elem["t"][:-1]), elem["lab_f"], rtol=4e-16, atol=0)
+    xyz = elem["rgb_lin"] * np.array([[0.95], [1.0], [1.09]])
+    np.testing.assert_allclose(ex.xyz_to_lab(*xyz), elem["xyz_to_lab"], rtol=0, atol=1e-12)
+
+
+def test_hsi_arccos_vs_reference(M, golden):
+    got = M["exact"].rgb_to_hsi_arccos(golden["probe"])
+    ref = golden["hsi_arccos"]
+    assert np.array_equal(np.isnan(got), np.isnan(ref))
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-12, equal_nan=True)

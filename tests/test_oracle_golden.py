@@ -138,3 +138,35 @@ def test_call_counts_vs_reference(figures):
     for k, v in figures["call_probabilities"].items():
         assert got[k] == v["count"], k
         assert got[k] / O.CUBE_SIZE == v["p"], k
+
+
+@pytest.fixture(scope="module")
+def elem():
+    return np.load(os.path.join(HERE, "golden", "elem_outputs.npz"))
+
+
+def test_scalar_approximants_vs_reference(elem):
+    """cbrt_fast / atan_sqrt3_fast / acos_fast / atan_unit_fast (fast.py:81-185), bit-exact."""
+    t, x = elem["t"], elem["x"]
+    for n, m in [(2, 2), (3, 4), (4, 4)]:
+        num, den = (O._f(c) for c in O.CBRT_RATIONALS[(n, m)])
+        with np.errstate(all="ignore"):
+            eq(O.cbrt_fast(t, num, den), elem[f"cbrt_{n}{m}"])
+    for n in (3, 5):
+        eq(O.cbrt_fast(t, O._f(O.CBRT_POLYS[n])), elem[f"cbrt_poly{n}"])
+    for n in (2, 3, 4, 5):
+        eq(O.atan_sqrt3_fast(x, O.HSI_REFIT[n]), elem[f"atan_sqrt3_{n}"])
+    for d in [(4, 4, 4), (5, 5, 5), (4, 5, 4)]:
+        cfg = O.OracleConfig(sct_degrees=d)
+        key = "".join(map(str, d))
+        with np.errstate(all="ignore"):
+            eq(O.acos_fast(x, cfg), elem[f"acos_{key}"])
+        eq(O.atan_unit_fast(elem["g"], elem["r"], cfg), elem[f"atan_unit_{key}"])
+
+
+def test_exact_building_blocks_vs_reference(elem):
+    """inverse_gamma / rgb_to_xyz / lab_f / xyz_to_lab (exact.py:52-83), bit-exact."""
+    eq(O.inverse_gamma(elem["k"]), elem["inverse_gamma"])
+    eq(np.stack(O.rgb_to_xyz(*elem["rgb_lin"])), elem["rgb_to_xyz"])
+    eq(O.lab_f(elem["t"][:-1]), elem["lab_f"])
+    eq(O.xyz_to_lab(*(elem["rgb_lin"] * np.array([[0.95], [1.0], [1.09]]))), elem["xyz_to_lab"])
