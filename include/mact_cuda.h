@@ -186,9 +186,10 @@ int mact_approx_eval(const MactApproxSpec* spec, const double* x, const double* 
  *   MACT_ELEM_INVERSE_GAMMA  out0 = inverse_gamma(in0)               (exact.py:52-57)
  *   MACT_ELEM_RGB_TO_XYZ     (out0, out1, out2) = rgb_to_xyz(in0..2)  (exact.py:60-66)
  *   MACT_ELEM_LAB_F          out0 = lab_f(in0)                       (exact.py:69-72)
- *   MACT_ELEM_XYZ_TO_LAB     out0 (n,3) = xyz_to_lab(in0..2)         (exact.py:75-83) */
+ *   MACT_ELEM_XYZ_TO_LAB     out0 (n,3) = xyz_to_lab(in0..2)         (exact.py:75-83)
+ *   MACT_ELEM_ANGULAR_LERP   out0 = lut.angular_lerp(in0, in1, in2)  (lut.py:202-216) */
 enum { MACT_ELEM_INVERSE_GAMMA = 0, MACT_ELEM_RGB_TO_XYZ = 1, MACT_ELEM_LAB_F = 2,
-       MACT_ELEM_XYZ_TO_LAB = 3 };
+       MACT_ELEM_XYZ_TO_LAB = 3, MACT_ELEM_ANGULAR_LERP = 4 };
 int mact_exact_elem(int op, const double* in0, const double* in1, const double* in2,
                     double* out0, double* out1, double* out2, int64_t n, void* stream);
 

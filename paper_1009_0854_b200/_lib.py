@@ -57,7 +57,7 @@ class MactApproxSpec(C.Structure):
 
 
 FN_FORM, FN_ATAN_SQRT3, FN_ACOS, FN_ATAN_UNIT = 0, 1, 2, 3
-ELEM_INVERSE_GAMMA, ELEM_RGB_TO_XYZ, ELEM_LAB_F, ELEM_XYZ_TO_LAB = 0, 1, 2, 3
+ELEM_INVERSE_GAMMA, ELEM_RGB_TO_XYZ, ELEM_LAB_F, ELEM_XYZ_TO_LAB, ELEM_ANGULAR_LERP = 0, 1, 2, 3, 4
 SPACE_HSI_ARCCOS = 3
 
 _vp, _i, _i64, _u64 = C.c_void_p, C.c_int, C.c_int64, C.c_uint64

@@ -3,13 +3,14 @@
 //   mact_approx_eval <- fast.cbrt_fast / atan_sqrt3_fast / acos_fast / atan_unit_fast
 //                       (fast.py:81-83, :118-122, :151-185) over
 //                       approximants.eval_poly / eval_rational (approximants.py:55-82)
-//   mact_exact_elem  <- exact.inverse_gamma / rgb_to_xyz / lab_f / xyz_to_lab (exact.py:52-83)
+//   mact_exact_elem  <- exact.inverse_gamma / rgb_to_xyz / lab_f / xyz_to_lab (exact.py:52-83),
+//                       lut.angular_lerp (lut.py:202-216)
 //
 // Horner runs exactly as numpy evaluates it (acc *= x; acc += c, each rounded:
 // __dmul_rn / __dadd_rn, no FMA contraction), and +, *, /, sqrt are correctly
 // rounded on both sides, so mact_approx_eval is bit-identical to the
 // reference.  mact_exact_elem uses libdevice pow/cbrt (within 1-2 ulp of libm).
-#include "mact_common.cuh"
+#include "mact_lut.cuh"
 
 namespace mact {
 
@@ -84,6 +85,8 @@ __global__ void k_exact_elem(int op, const double* __restrict__ a, const double*
       o0[i] = inverse_gamma_np(a[i]);
     } else if (op == MACT_ELEM_LAB_F) {
       o0[i] = lab_f_np(a[i]);
+    } else if (op == MACT_ELEM_ANGULAR_LERP) {
+      o0[i] = angular_lerp_d(a[i], b[i], c[i]);
     } else if (op == MACT_ELEM_RGB_TO_XYZ) {                       // exact.py:60-66
       const double r = a[i], g = b[i], bb = c[i];
       double* o[3] = {o0, o1, o2};
@@ -131,9 +134,10 @@ extern "C" int mact_approx_eval(const MactApproxSpec* spec, const double* x, con
 
 extern "C" int mact_exact_elem(int op, const double* in0, const double* in1, const double* in2,
                                double* out0, double* out1, double* out2, int64_t n, void* stream) {
-  if (op < MACT_ELEM_INVERSE_GAMMA || op > MACT_ELEM_XYZ_TO_LAB)
+  if (op < MACT_ELEM_INVERSE_GAMMA || op > MACT_ELEM_ANGULAR_LERP)
     return set_error(MACT_EBADARG, "unknown elementwise op %d", op);
-  const bool three_in = op == MACT_ELEM_RGB_TO_XYZ || op == MACT_ELEM_XYZ_TO_LAB;
+  const bool three_in = op == MACT_ELEM_RGB_TO_XYZ || op == MACT_ELEM_XYZ_TO_LAB ||
+                        op == MACT_ELEM_ANGULAR_LERP;
   if (n < 0 || (n > 0 && (!in0 || !out0 || (three_in && (!in1 || !in2)) ||
                           (op == MACT_ELEM_RGB_TO_XYZ && (!out1 || !out2)))))
     return set_error(MACT_EBADARG, "bad argument");

@@ -146,20 +146,6 @@ struct OpLut {
 // vectors, so it is evaluated like the reference: fp64 lattice (n^3, 3),
 // fp64 weights (exact integer products / 255^k), fp64 sincos/atan2.  This
 // destination is not on the throughput metric; a per-pixel kernel suffices.
-__device__ __forceinline__ double fmod2pi_d(double a) {
-  a = fmod(a, kTwoPi);
-  return a < 0.0 ? a + kTwoPi : a;
-}
-__device__ __forceinline__ double angular_lerp_d(double t0, double t1, double a) {
-  double s0, c0, s1, c1;
-  sincos(t0, &s0, &c0);
-  sincos(t1, &s1, &c1);
-  const double c = (1.0 - a) * c0 + a * c1, s = (1.0 - a) * s0 + a * s1;
-  if (hypot(c, s) < 1e-12) return fmod2pi_d(t0);
-  const double out = atan2(s, c);
-  return out < 0.0 ? out + kTwoPi : out;
-}
-
 template <int N, int METHOD>
 __global__ void k_lut_angular(const double* __restrict__ lat, int mask, const uint8_t* __restrict__ rgb,
                               float* __restrict__ out, int64_t n, int planar) {

@@ -99,4 +99,20 @@ __device__ __forceinline__ void lut_nodes(uint32_t pr, uint32_t pg, uint32_t pb,
   }
 }
 
+// lut.angular_lerp (lut.py:202-216): circular interpolation wrapped to
+// [0, 2 pi); a vanishing blended direction resolves to theta0 mod 2 pi.
+__device__ __forceinline__ double fmod2pi_d(double a) {
+  a = fmod(a, kTwoPi);
+  return a < 0.0 ? a + kTwoPi : a;
+}
+__device__ __forceinline__ double angular_lerp_d(double t0, double t1, double a) {
+  double s0, c0, s1, c1;
+  sincos(t0, &s0, &c0);
+  sincos(t1, &s1, &c1);
+  const double c = (1.0 - a) * c0 + a * c1, s = (1.0 - a) * s0 + a * s1;
+  if (hypot(c, s) < 1e-12) return fmod2pi_d(t0);
+  const double out = atan2(s, c);
+  return out < 0.0 ? out + kTwoPi : out;
+}
+
 }  // namespace mact

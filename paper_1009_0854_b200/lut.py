@@ -129,6 +129,14 @@ def build_cache(lut: Lut3D) -> Lut3D:
                  _device=lut._device)
 
 
+def angular_lerp(theta0, theta1, alpha):
+    """Circular interpolation between two angles, wrapped to [0, 2 pi); a
+    vanishing blended direction resolves to theta0 mod 2 pi (lut.py:202-216)."""
+    from .exact import _elem
+
+    return _elem(_lib.ELEM_ANGULAR_LERP, theta0, theta1, alpha)
+
+
 def _host_interp(lut: Lut3D, method_code: int, arr: np.ndarray, out, layout: str):
     """numpy uint8 -> numpy fp32 through the native chunked H2D/kernel/D2H executor."""
     import torch

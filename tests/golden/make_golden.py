@@ -113,6 +113,11 @@ def elem_vectors() -> dict:
     out["rgb_to_xyz"] = np.stack(exact.rgb_to_xyz(*rgb))
     out["lab_f"] = exact.lab_f(t[:-1])
     out["xyz_to_lab"] = exact.xyz_to_lab(*(rgb * np.array([[0.95], [1.0], [1.09]])))
+    from mact import lut
+    th = rng.random((3, 3000)) * np.array([[14.0], [14.0], [1.0]]) - np.array([[7.0], [7.0], [0.0]])
+    th[:, :4] = [[0.0, 1.0, 3.0, -1.0], [np.pi, 1.0 + np.pi, 3.0, -1.0 + 2 * np.pi], [0.5, 0.5, 0.25, 1.0]]
+    out["lerp_in"] = th
+    out["angular_lerp"] = lut.angular_lerp(*th)
     return out
 
 

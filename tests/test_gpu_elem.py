@@ -88,3 +88,13 @@ def test_hsi_arccos_vs_reference(M, golden):
     ref = golden["hsi_arccos"]
     assert np.array_equal(np.isnan(got), np.isnan(ref))
     np.testing.assert_allclose(got, ref, rtol=0, atol=1e-12, equal_nan=True)
+
+
+def test_angular_lerp(elem):
+    from paper_1009_0854_b200 import lut
+    got = lut.angular_lerp(*elem["lerp_in"])
+    ref = elem["angular_lerp"]
+    d = np.abs(got - ref)
+    d = np.minimum(d, 2 * np.pi - d)                 # 0 and 2 pi are the same angle
+    assert d.max() < 1e-12
+    assert np.isclose(got[0], 0.0)                   # antipodal at alpha 0.5 -> theta0

@@ -170,3 +170,7 @@ def test_exact_building_blocks_vs_reference(elem):
     eq(np.stack(O.rgb_to_xyz(*elem["rgb_lin"])), elem["rgb_to_xyz"])
     eq(O.lab_f(elem["t"][:-1]), elem["lab_f"])
     eq(O.xyz_to_lab(*(elem["rgb_lin"] * np.array([[0.95], [1.0], [1.09]]))), elem["xyz_to_lab"])
+
+
+def test_angular_lerp_vs_reference(elem):
+    eq(O.angular_lerp(*elem["lerp_in"]), elem["angular_lerp"])
