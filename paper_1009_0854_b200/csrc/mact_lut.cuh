@@ -23,13 +23,16 @@ template <> struct LutK<MACT_LUT_PRISM> { static constexpr int K = 6; };
 template <> struct LutK<MACT_LUT_PYRAMIDAL> { static constexpr int K = 5; };
 template <> struct LutK<MACT_LUT_TETRAHEDRAL> { static constexpr int K = 4; };
 
+// Unsigned on purpose: a signed x / 255 compiles to a 4-instruction
+// sign-corrected sequence (IMAD.HI + SHF + LEA.HI.SX32 + a zeroed
+// accumulator), the unsigned one to IMAD.HI.U32 + SHF.
 template <int N>
 __device__ __forceinline__ void lut_locate(uint32_t p, int& base, int& rem) {
-  const int x = (int)p * (N - 1);
-  int bse = x / 255;
-  bse = bse > N - 2 ? N - 2 : bse;
-  base = bse;
-  rem = x - 255 * bse;
+  const uint32_t x = p * (uint32_t)(N - 1);
+  uint32_t bse = x / 255u;
+  bse = bse > (uint32_t)(N - 2) ? (uint32_t)(N - 2) : bse;
+  base = (int)bse;
+  rem = (int)(x - 255u * bse);
 }
 
 // Node flat indices and weights of one pixel.  rem values in [0,255].
