@@ -5,6 +5,8 @@
     ErrorStats                                         (harness.py:63-68)
     component_error(...)   per-component |fast - exact|  (not in the reference)
     call_probabilities()  CallProbabilities             (harness.py:125-175)
+    measure_gain(...)     GainStats, device-timed        (harness.py:176-221)
+    synthetic_corpus()                                   (harness.py:224-258)
 
 ``measure_error`` keeps the reference's plugin seam — any callable
 ``pixels -> (..., 3)`` — and fuses the whole evaluation into one kernel
@@ -315,5 +317,93 @@ def call_probabilities() -> CallProbabilities:
     return CallProbabilities(**{k: v / CUBE_SIZE for k, v in c.items()})
 
 
-def measure_gain(*_a, **_k):  # pragma: no cover - out of scope
-    raise CorpusEmpty("measure_gain (CPU wall-clock speed ratios) is out of scope for the GPU path")
+@dataclass(frozen=True)
+class GainStats:
+    """harness.py:176-183."""
+
+    min: float
+    max: float
+    mean: float
+    stdev: float
+    median: float
+    per_image: Tuple[float, ...]
+
+
+def _mean_device_seconds(fn: Callable, image, repeats: int) -> float:
+    """Mean device time of fn(image) over ``repeats`` calls: CUDA events on the
+    current stream around each call (the reference's perf_counter, harness.py:188-194)."""
+    import torch
+
+    st = torch.cuda.current_stream()
+    total = 0.0
+    for _ in range(repeats):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        fn(image)
+        b.record(st)
+        b.synchronize()
+        total += a.elapsed_time(b) / 1e3
+    return total / repeats
+
+
+def measure_gain(space: str, fast: Callable, exact_fn: Callable, corpus, repeats_exact: int = 3,
+                 repeats_fast: int = 3) -> GainStats:
+    """Per-image speedup of ``fast`` over ``exact_fn`` (harness.py:197-221; PAPER Table 4).
+
+    Images are pre-loaded into device memory (the reference pre-loads host
+    arrays), both callables get a warm-up call, then each is timed with CUDA
+    events and the gain is mean exact time / mean fast time.
+    """
+    import torch
+
+    corpus = list(corpus)
+    if len(corpus) == 0:
+        raise CorpusEmpty("gain measurement needs at least one image")
+    if repeats_exact < 3 or repeats_fast < 3:
+        raise ValueError("timing needs at least 3 repeats per transform")
+    _dev.require_cuda()
+    gains = []
+    for image in corpus:
+        img = image if _dev.is_device_tensor(image) else torch.from_numpy(np.ascontiguousarray(image)).cuda()
+        fast(img)
+        exact_fn(img)
+        t_exact = _mean_device_seconds(exact_fn, img, repeats_exact)
+        t_fast = _mean_device_seconds(fast, img, repeats_fast)
+        gains.append(t_exact / t_fast)
+    arr = np.asarray(gains)
+    return GainStats(min=float(arr.min()), max=float(arr.max()), mean=float(arr.mean()),
+                     stdev=float(arr.std(ddof=1)) if arr.size > 1 else 0.0,
+                     median=float(np.median(arr)), per_image=tuple(float(v) for v in arr))
+
+
+def synthetic_corpus(sizes=(512, 1024, 2048), seed: int = 0) -> List[np.ndarray]:
+    """Deterministic benchmark images, one gradient, white-noise, 1/f-noise and
+    flat image per size (harness.py:224-243): host-side input generation with
+    numpy's seeded generator, so the bytes equal the reference's."""
+    rng = np.random.default_rng(seed)
+    images = []
+    for n in sizes:
+        yy, xx = np.mgrid[0:n, 0:n]
+        grad = np.stack([255.0 * xx / (n - 1), 255.0 * yy / (n - 1), 255.0 * (xx + yy) / (2 * n - 2)],
+                        axis=-1)
+        images.append(grad.astype(np.uint8))
+        images.append(rng.integers(0, 256, size=(n, n, 3), dtype=np.uint8))
+        images.append(_pink_noise(rng, n))
+        flat = np.empty((n, n, 3), dtype=np.uint8)
+        flat[..., 0], flat[..., 1], flat[..., 2] = 180, 120, 60
+        images.append(flat)
+    return images
+
+
+def _pink_noise(rng, n: int) -> np.ndarray:
+    """1/f noise per channel, min-max scaled to 0..255 (harness.py:246-258)."""
+    fy = np.fft.fftfreq(n)[:, None]
+    fx = np.fft.rfftfreq(n)[None, :]
+    radial = np.sqrt(fy * fy + fx * fx)
+    radial[0, 0] = 1.0
+    out = np.empty((n, n, 3))
+    for c in range(3):
+        img = np.fft.irfft2(np.fft.rfft2(rng.standard_normal((n, n))) / radial, s=(n, n))
+        lo, hi = img.min(), img.max()
+        out[..., c] = 255.0 * (img - lo) / (hi - lo)
+    return out.astype(np.uint8)

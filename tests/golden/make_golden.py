@@ -121,15 +121,23 @@ def elem_vectors() -> dict:
     return out
 
 
+def corpus_digest(harness) -> list:
+    """sha256 of each image of harness.synthetic_corpus((64, 96), seed=0) (harness.py:224-258)."""
+    import hashlib
+    return [hashlib.sha256(np.ascontiguousarray(im).tobytes()).hexdigest()
+            for im in harness.synthetic_corpus((64, 96), seed=0)]
+
+
 def main() -> None:
     sys.path.insert(0, str(REF))
     if "--elem-only" in sys.argv:
         np.savez_compressed(OUT / "elem_outputs.npz", **elem_vectors())
         return
-    if "--call-probs-only" in sys.argv:     # refresh one figure without the full sweep
+    if "--call-probs-only" in sys.argv:     # refresh small figures without the full sweep
         from mact import harness
         fig = json.loads((OUT / "figures.json").read_text())
         fig["call_probabilities"] = call_probs(harness)
+        fig["synthetic_corpus_64_96"] = corpus_digest(harness)
         (OUT / "figures.json").write_text(json.dumps(fig, indent=1))
         return
     os.environ.setdefault("MACT_THREADS", str(os.cpu_count() or 1))
@@ -278,6 +286,7 @@ def main() -> None:
         comp[space] = acc
     fig["c2_component"] = comp
     fig["call_probabilities"] = call_probs(harness)
+    fig["synthetic_corpus_64_96"] = corpus_digest(harness)
 
     (OUT / "figures.json").write_text(json.dumps(fig, indent=1))
     (OUT / "hsi_refit.json").write_text(json.dumps({"coeffs": refit, "eps": refit_eps}, indent=1))

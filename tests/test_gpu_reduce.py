@@ -150,3 +150,17 @@ def test_call_probabilities(P, figures):
     for k, v in figures["call_probabilities"].items():
         assert counts[k] == v["count"], k
         assert getattr(probs, k) == v["p"], k
+
+
+def test_measure_gain_device_timed(P):
+    """harness.measure_gain (harness.py:197-221) on the GPU: Table 4's shape."""
+    from paper_1009_0854_b200.errors import CorpusEmpty
+    h, fast, exact = P["harness"], P["fast"], P["exact"]
+    corpus = h.synthetic_corpus((256,), seed=0)
+    g = h.measure_gain("lab", fast.rgb_to_lab_fast, exact.rgb_to_lab_exact, corpus)
+    assert len(g.per_image) == 4 and g.min <= g.median <= g.max and g.min > 0
+    assert g.stdev >= 0 and abs(g.mean - np.mean(g.per_image)) < 1e-12
+    with pytest.raises(CorpusEmpty):
+        h.measure_gain("lab", fast.rgb_to_lab_fast, exact.rgb_to_lab_exact, [])
+    with pytest.raises(ValueError):
+        h.measure_gain("lab", fast.rgb_to_lab_fast, exact.rgb_to_lab_exact, corpus, repeats_fast=2)
