@@ -13,7 +13,7 @@ torch = pytest.importorskip("torch")
 hyp = pytest.importorskip("hypothesis")
 from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E402
 
-SETTINGS = settings(max_examples=40, deadline=None, suppress_health_check=list(HealthCheck))
+SETTINGS = settings(max_examples=150, deadline=None, suppress_health_check=list(HealthCheck))
 
 DEGREES = {"lab": [dict(cielab_degrees=d) for d in [(2, 2), (3, 3), (4, 4), (2, 4), (4, 3)]],
            "hsi": [dict(hsi_degree=d) for d in (2, 3, 4, 5)],
