@@ -406,13 +406,91 @@ __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
   cluster.sync();                                        // partners may still signal / write my smem
 }
 
+// Planar output (3, N) needs no exchange at all: component c of a step is a
+// contiguous 16 KB run of plane c.  Independent CTAs (no cluster), CTA b holds
+// component b % 3 and streams steps b / 3, b / 3 + G/3, ...; the two warp
+// groups alternate steps and each drains its staging plane with one bulk store.
+template <int METHOD>
+__global__ void __launch_bounds__(kLut33Threads, 1)
+    k_lut33_planar(const float4* __restrict__ lat4, const uint8_t* __restrict__ rgb,
+                   float* __restrict__ out, int64_t n, int64_t nsteps) {
+  constexpr int N = 33, NN = N * N * N, K = LutK<METHOD>::K;
+  extern __shared__ __align__(128) float sm33[];
+  float* lat_c = sm33;                                   // NN floats
+  float* stage = sm33 + ((NN + 31) / 32) * 32;           // [2][4096]: one plane run per group
+  const int comp = (int)(blockIdx.x % 3);
+  const int64_t cl = blockIdx.x / 3, ncl = gridDim.x / 3;
+  for (int i = threadIdx.x; i < NN; i += blockDim.x) {
+    const float4 v = __ldg(lat4 + i);
+    lat_c[i] = comp == 0 ? v.x : comp == 1 ? v.y : v.z;
+  }
+  __syncthreads();
+  const int grp = (int)(threadIdx.x >> 9), tg = (int)(threadIdx.x & 511);
+  const uint32_t* in_w = reinterpret_cast<const uint32_t*>(rgb);
+  float* sg = stage + grp * kLut33Step;
+  for (int64_t it = grp; cl + it * ncl < nsteps; it += 2) {
+    const int64_t step = cl + it * ncl;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t g = step * kLut33Threads + h * 512 + tg;
+      const uint32_t w0 = __ldg(in_w + 3 * g), w1 = __ldg(in_w + 3 * g + 1), w2 = __ldg(in_w + 3 * g + 2);
+      const uint32_t ch[12] = {byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), byte_of(w0, 3),
+                               byte_of(w1, 0), byte_of(w1, 1), byte_of(w1, 2), byte_of(w1, 3),
+                               byte_of(w2, 0), byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3)};
+      constexpr int PB = K > 6 ? MACT_LUT33_TRI_PB : 4;
+      float a[4];
+#pragma unroll
+      for (int q0 = 0; q0 < 4; q0 += PB) {
+        int idx[PB][K];
+        float w[PB][K], v[PB][K];
+#pragma unroll
+        for (int q = 0; q < PB; ++q)
+          lut_nodes<N, METHOD>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], idx[q], w[q]);
+#pragma unroll
+        for (int q = 0; q < PB; ++q)
+#pragma unroll
+          for (int j = 0; j < K; ++j) v[q][j] = lat_c[idx[q][j]];
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+          a[q0 + q] = w[q][0] * v[q][0];
+#pragma unroll
+          for (int j = 1; j < K; ++j) a[q0 + q] = fmaf(w[q][j], v[q][j], a[q0 + q]);
+        }
+      }
+      if (h == 0 && tg == 0) bulk_wait_read<0>();       // this group's previous plane run drained
+      if (h == 0) asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(512) : "memory");
+      *reinterpret_cast<float4*>(sg + 4 * (h * 512 + tg)) = make_float4(a[0], a[1], a[2], a[3]);
+    }
+    fence_proxy_async_smem();
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(512) : "memory");
+    if (tg == 0) {
+      bulk_s2g(out + comp * n + step * kLut33Step, sg, kLut33Step * 4u);
+      bulk_commit();
+    }
+  }
+  if (tg == 0) bulk_wait<0>();
+}
+
 template <int METHOD>
 static int launch_lut33_comp(const float* lat, const uint8_t* rgb, float* out, int64_t n, int planar,
                              cudaStream_t st) {
   constexpr size_t smem = kLut33Smem;
-  const bool ok = !planar && (uintptr_t)rgb % 16 == 0 && (uintptr_t)out % 16 == 0;
-  const int64_t nsteps = ok ? n / kLut33Step : 0;
-  if (nsteps > 0) {
+  const bool aligned = (uintptr_t)rgb % 16 == 0 && (uintptr_t)out % 16 == 0;
+  const bool ok = !planar && aligned;
+  const int64_t nsteps = aligned && (!planar || n % 4 == 0) ? n / kLut33Step : 0;
+  if (planar && nsteps > 0) {   // planar: independent component CTAs, no exchange
+    constexpr size_t psmem = (((33 * 33 * 33) + 31) / 32 * 32 + 2 * kLut33Step) * sizeof(float);
+    auto pfn = k_lut33_planar<METHOD>;
+    const int64_t cap = persistent_grid((const void*)pfn, kLut33Threads, psmem);
+    if (cap <= 0) return MACT_ECUDA;
+    int64_t groups = cap / 3;
+    if (groups > nsteps) groups = nsteps;
+    if (groups < 1) groups = 1;
+    pfn<<<(unsigned)(3 * groups), kLut33Threads, psmem, st>>>(reinterpret_cast<const float4*>(lat), rgb,
+                                                                   out, n, nsteps);
+    count_launch();
+    if (int rc = check_launch("lut33_planar")) return rc;
+  } else if (ok && nsteps > 0) {
     auto kfn = k_lut33_comp<METHOD>;
     static std::atomic<int> max_clusters{-1};           // per method instantiation (benign race)
     int mc = max_clusters.load();
@@ -435,7 +513,7 @@ static int launch_lut33_comp(const float* lat, const uint8_t* rgb, float* out, i
     if (int rc = check_launch("lut33_comp")) return rc;
   }
   const int64_t done = nsteps * kLut33Step;
-  if (done < n) {   // tail, planar output or unaligned buffers: the L2-gather streaming kernel
+  if (done < n) {   // tail or unaligned buffers: the L2-gather streaming kernel
     Outs outs{{out, nullptr, nullptr}};
     LutParams p{reinterpret_cast<const float4*>(lat)};
     if (done == 0)

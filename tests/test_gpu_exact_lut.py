@@ -165,3 +165,15 @@ def test_lut_interp_host_executor(grid, method):
     lut.interpolate(L, pin_in.numpy(), method, out=pin_out.numpy())
     np.testing.assert_array_equal(pin_out.numpy(), ref)
     np.testing.assert_array_equal(lut.interpolate(L, px[:5000], method, layout="planar").T, ref[:5000])
+
+
+@pytest.mark.parametrize("n", [4096 * 37 + 8, 4096 * 5 + 3, 1000])
+@pytest.mark.parametrize("method", ["trilinear", "tetrahedral"])
+def test_lut33_planar_equals_interleaved(n, method):
+    """33^3 planar output (component CTAs, no exchange) == the interleaved cluster path."""
+    from paper_1009_0854_b200 import lut
+    px = torch.from_numpy(np.random.default_rng(n).integers(0, 256, (n, 3), dtype=np.uint8)).cuda()
+    L = lut.build_lut("lab", 33)
+    inter = lut.interpolate(L, px, method).cpu().numpy()
+    planar = lut.interpolate(L, px, method, layout="planar").cpu().numpy()
+    np.testing.assert_array_equal(planar.T, inter)
