@@ -164,6 +164,12 @@ int mact_err_reduce(const MactErrSpec* spec, const MactCoeffs* c, const uint8_t*
                     int64_t cube_start, int64_t n, int64_t index_base, MactErrStats* out,
                     void* workspace, void* stream);
 
+/* exact.rgb_to_{lab,hsi,sct}_exact formulas (exact.py:60-149) in fp32 with
+ * libdevice cbrtf/atanf/acosf/atan2f/sqrtf, uint8 in, fp32 out, on the
+ * streaming skeleton: the comparator of the paper's Table 4 gain on B200
+ * (SURVEY.md §8(f) item 2).  Not a parity path (fp32 rounding). */
+int mact_exact_f32(int space, const uint8_t* rgb, float* out, int64_t n, int layout, void* stream);
+
 /* ---- elementwise building blocks (fp64 device arrays) --------------------- */
 /* The reference's scalar approximant functions, bit-identical to numpy:
  *   MACT_FN_FORM        out = a(x) (b_deg < 0) or a(x)/b(x)       fast.cbrt_fast, fast.py:81-83

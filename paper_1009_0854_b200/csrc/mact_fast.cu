@@ -160,6 +160,58 @@ struct OpMulti {
 };
 using OpAll = OpMulti<7>;
 
+// The "exact" transforms in fp32 with libdevice cbrtf / atanf / acosf /
+// atan2f / sqrtf on the same streaming skeleton: the B200 comparator of the
+// paper's Table 4 gain.  Formulas as exact.py:60-149.
+template <int SPACE>
+struct OpExactF32 {
+  static constexpr int NOUT = 1;
+  using Params = KCoeffs;
+  struct NoShared { int unused; };
+  using Shared = typename std::conditional<SPACE == MACT_SPACE_LAB, OpLab::Shared, NoShared>::type;
+  static __device__ __forceinline__ void init(Shared* s, const Params& c) {
+    if constexpr (SPACE == MACT_SPACE_LAB) OpLab::init(s, c);
+  }
+  static __device__ __forceinline__ float lab_f(float t) {
+    return t > (float)kLabKnee ? cbrtf(t) : fmaf((float)kLabSlope, t, (float)kLabOffset);
+  }
+  static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
+                                            uint32_t lane, const Params& c, float (*o)[3]) {
+    if constexpr (SPACE == MACT_SPACE_LAB) {
+      const float gr = s->gamma[(r << 5) | lane], gg = s->gamma[(g << 5) | lane], gb = s->gamma[(b << 5) | lane];
+      const float fx = lab_f(fmaf(c.mxyz[2], gb, fmaf(c.mxyz[1], gg, c.mxyz[0] * gr)));
+      const float fy = lab_f(fmaf(c.mxyz[5], gb, fmaf(c.mxyz[4], gg, c.mxyz[3] * gr)));
+      const float fz = lab_f(fmaf(c.mxyz[8], gb, fmaf(c.mxyz[7], gg, c.mxyz[6] * gr)));
+      o[0][0] = fmaf(116.f, fy, -16.f);
+      o[0][1] = 500.f * (fx - fy);
+      o[0][2] = 200.f * (fy - fz);
+    } else if constexpr (SPACE == MACT_SPACE_HSI) {
+      const float rf = u2f_small(r) * (1.f / 255.f), gf = u2f_small(g) * (1.f / 255.f),
+                  bf = u2f_small(b) * (1.f / 255.f);
+      const float s3 = 1.7320508f;
+      float h;
+      if (r > b && g > b) h = (float)(kPi / 3.0) + atanf(s3 * (gf - rf) / ((gf - bf) + (rf - bf)));
+      else if (g > r) h = (float)kPi + atanf(s3 * (bf - gf) / ((bf - rf) + (gf - rf)));
+      else if (b > g) h = (float)(5.0 * kPi / 3.0) + atanf(s3 * (rf - bf) / ((rf - gf) + (bf - gf)));
+      else h = r > b ? 0.f : __int_as_float(0x7fc00000);
+      const float total = rf + gf + bf, low = fminf(fminf(rf, gf), bf);
+      o[0][0] = h;
+      o[0][1] = total > 0.f ? 1.f - 3.f * low / total : 0.f;
+      o[0][2] = total * (1.f / 3.f);
+    } else {
+      const float rf = u2f_small(r), gf = u2f_small(g), bf = u2f_small(b);
+      const float len = sqrtf(fmaf(rf, rf, fmaf(gf, gf, bf * bf)));
+      o[0][0] = len;
+      o[0][1] = len > 0.f ? acosf(fminf(fmaxf(bf / len, -1.f), 1.f)) : 0.f;
+      o[0][2] = (r | g) ? atan2f(gf, rf) : __int_as_float(0x7fc00000);
+    }
+  }
+  static __device__ __forceinline__ void px4w(uint32_t w0, uint32_t w1, uint32_t w2, const Shared* s,
+                                              uint32_t lane, const Params& c, float (*o)[1][3]) {
+    px4_each<OpExactF32>(w0, w1, w2, s, lane, c, o);
+  }
+};
+
 // Real-valued input, fp64, reference formulas verbatim.
 template <typename T>
 __global__ void k_fast_real(int space, const T* __restrict__ in, float* __restrict__ out,
@@ -342,6 +394,28 @@ extern "C" int mact_all_fast(const uint8_t* rgb, float* lab, float* hsi, float* 
     case 6: return launch_stream_t<OpMulti<6>, MACT_HS_CFG>(rgb, Outs{{hsi, sct, nullptr}}, n, planar, kc, st, "multi_fast");
     default: return launch_stream_t<OpAll, MACT_ALL_CFG>(rgb, Outs{{lab, hsi, sct}}, n, planar, kc, st, "all_fast");
   }
+}
+
+extern "C" int mact_exact_f32(int space, const uint8_t* rgb, float* out, int64_t n, int layout, void* stream) {
+  if (space < 0 || space > 2) return set_error(MACT_EBADARG, "unknown space %d", space);
+  if (n < 0 || (n > 0 && (!rgb || !out))) return set_error(MACT_EBADARG, "bad argument");
+  if (layout != MACT_LAYOUT_INTERLEAVED && layout != MACT_LAYOUT_PLANAR)
+    return set_error(MACT_EBADARG, "unknown layout %d", layout);
+  if (n == 0) return MACT_OK;
+  KCoeffs kc;
+  MactCoeffs dflt{};
+  dflt.cbrt_num_deg = dflt.cbrt_den_deg = 2;                // only mxyz is used; any valid degrees
+  dflt.hsi_deg = 2; dflt.asin_deg = dflt.acos_deg = dflt.atan_deg = 4;
+  dflt.cbrt_den[0] = 1.0;
+  if (int rc = make_kcoeffs(&dflt, &kc)) return rc;
+  Outs outs{{out, nullptr, nullptr}};
+  const int planar = layout == MACT_LAYOUT_PLANAR;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (space == MACT_SPACE_LAB)
+    return launch_stream_t<OpExactF32<MACT_SPACE_LAB>, MACT_LAB_CFG>(rgb, outs, n, planar, kc, st, "exact_f32");
+  if (space == MACT_SPACE_HSI)
+    return launch_stream_t<OpExactF32<MACT_SPACE_HSI>, MACT_HSI_CFG>(rgb, outs, n, planar, kc, st, "exact_f32");
+  return launch_stream_t<OpExactF32<MACT_SPACE_SCT>, MACT_SCT_CFG>(rgb, outs, n, planar, kc, st, "exact_f32");
 }
 
 extern "C" int mact_probe_expand(const uint8_t* rgb, float* out, int64_t n, void* stream) {

@@ -53,6 +53,18 @@ def rgb_to_sct_exact(pixels, *, out_dtype: str = "float64"):
     return _exact("sct", pixels, out_dtype)
 
 
+def exact_f32(space: str, pixels, *, layout: str = "interleaved"):
+    """The exact transform formulas in fp32 libdevice arithmetic (mact_exact_f32):
+    the B200 comparator for the paper's Table 4 gain.  uint8 pixels, fp32 out."""
+    t, code, lead, on_dev = _dev.as_device_pixels(pixels)
+    if code != _lib.DTYPE_U8:
+        raise ValueError("exact_f32 takes 8-bit pixels")
+    res = _dev.empty_out(lead, layout, t.device)
+    _lib.call("mact_exact_f32", _lib.SPACES[space], t.data_ptr(), res.data_ptr(), t.numel() // 3,
+              _lib.LAYOUTS[layout], _dev.stream_ptr())
+    return _dev.to_caller(res, on_dev)
+
+
 def rgb_to_hsi_arccos(pixels, *, out_dtype: str = "float64"):
     """RGB -> HSI via the inverse-cosine hue formula (exact.py:104-116)."""
     import torch

@@ -46,6 +46,9 @@ def run():
     if a.op == "all":
         _lib.check(lib.mact_all_fast(x.data_ptr(), outs[0].data_ptr(), outs[1].data_ptr(),
                                      outs[2].data_ptr(), n, cfg.coeffs, 0, st))
+    elif a.op.startswith("exactf32_"):
+        sp = {"exactf32_lab": 0, "exactf32_hsi": 1, "exactf32_sct": 2}[a.op]
+        _lib.check(lib.mact_exact_f32(sp, x.data_ptr(), outs[0].data_ptr(), n, 0, st))
     elif a.op.startswith("exact_"):
         sp = {"exact_lab": 0, "exact_hsi": 1, "exact_sct": 2}[a.op]
         _lib.check(lib.mact_exact(sp, x.data_ptr(), 0, outs[0].data_ptr(), 1, n, st))

@@ -98,3 +98,17 @@ def test_angular_lerp(elem):
     d = np.minimum(d, 2 * np.pi - d)                 # 0 and 2 pi are the same angle
     assert d.max() < 1e-12
     assert np.isclose(got[0], 0.0)                   # antipodal at alpha 0.5 -> theta0
+
+
+@pytest.mark.parametrize("space", ["lab", "hsi", "sct"])
+def test_exact_f32_comparator(M, space):
+    """fp32 libdevice exact transforms (Table 4 comparator) stay inside the
+    north-star tolerance of the fp64 reference on the full cube."""
+    from oracle import mact_oracle as O
+    from tests.parity_util import CHECK
+    from paper_1009_0854_b200 import harness
+    cube = harness.cube_chunk(0, 1 << 24, device="cuda")
+    got = M["exact"].exact_f32(space, cube).cpu().numpy()
+    host = cube.cpu().numpy()
+    for s in range(0, 1 << 24, 1 << 22):
+        CHECK[space](got[s:s + (1 << 22)], O.EXACT[space](host[s:s + (1 << 22)]))
