@@ -118,6 +118,13 @@ def elem_vectors() -> dict:
     th[:, :4] = [[0.0, 1.0, 3.0, -1.0], [np.pi, 1.0 + np.pi, 3.0, -1.0 + 2 * np.pi], [0.5, 0.5, 0.25, 1.0]]
     out["lerp_in"] = th
     out["angular_lerp"] = lut.angular_lerp(*th)
+    # real-valued (float) pixels take the analytic path of every fast transform (fast.py:91-99)
+    fpx = np.r_[rng.random((3000, 3)) * 255.0, [[10.5, 10.5, 10.5], [0.0, 0.0, 3.25], [255.0, 0.0, 0.0],
+                                                [0.0, 0.0, 0.0], [1e-3, 2e-3, 0.0]]]
+    out["float_px"] = fpx
+    for sp in ("lab", "hsi", "sct"):
+        out[f"{sp}_fast_float"] = getattr(fast, f"rgb_to_{sp}_fast")(fpx)
+        out[f"{sp}_exact_float"] = getattr(exact, f"rgb_to_{sp}_exact")(fpx)
     return out
 
 

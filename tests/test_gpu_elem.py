@@ -112,3 +112,19 @@ def test_exact_f32_comparator(M, space):
     host = cube.cpu().numpy()
     for s in range(0, 1 << 24, 1 << 22):
         CHECK[space](got[s:s + (1 << 22)], O.EXACT[space](host[s:s + (1 << 22)]))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("space", ["lab", "hsi", "sct"])
+def test_float_pixels_fast_and_exact(M, elem, space, dtype):
+    """Real-valued pixels: analytic gamma / real-channel formulas (fast.py:91-99, exact.py)."""
+    from tests.parity_util import CHECK
+    px = elem["float_px"].astype(dtype)
+    ref_px = px.astype(np.float64)                      # the reference computes on the fp64 values
+    fast_ref = elem[f"{space}_fast_float"] if dtype == np.float64 else \
+        __import__("oracle.mact_oracle", fromlist=["x"]).FAST[space](ref_px)
+    CHECK[space](getattr(M["fast"], f"rgb_to_{space}_fast")(px), fast_ref)
+    exact_ref = elem[f"{space}_exact_float"] if dtype == np.float64 else \
+        __import__("oracle.mact_oracle", fromlist=["x"]).EXACT[space](ref_px)
+    got = getattr(M["exact"], f"rgb_to_{space}_exact")(px)
+    CHECK[space](got, exact_ref)

@@ -174,3 +174,10 @@ def test_exact_building_blocks_vs_reference(elem):
 
 def test_angular_lerp_vs_reference(elem):
     eq(O.angular_lerp(*elem["lerp_in"]), elem["angular_lerp"])
+
+
+def test_float_pixels_vs_reference(elem):
+    """Oracle fast/exact transforms on real-valued pixels == the reference's (bit-exact)."""
+    for sp in ("lab", "hsi", "sct"):
+        eq(O.FAST[sp](elem["float_px"]), elem[f"{sp}_fast_float"])
+        eq(O.EXACT[sp](elem["float_px"]), elem[f"{sp}_exact_float"])
