@@ -146,34 +146,45 @@ struct OpLut {
 // vectors, so it is evaluated like the reference: fp64 lattice (n^3, 3),
 // fp64 weights (exact integer products / 255^k), fp64 sincos/atan2.  This
 // destination is not on the throughput metric; a per-pixel kernel suffices.
-template <int N, int METHOD>
-__global__ void k_lut_angular(const double* __restrict__ lat, int mask, const uint8_t* __restrict__ rgb,
-                              float* __restrict__ out, int64_t n, int planar) {
+template <typename TI>
+__device__ __forceinline__ double px_chan(const TI* p, int64_t i) { return (double)p[i]; }
+
+// One kernel for every fp64 LUT evaluation: angular destinations (any pixel
+// type) and real-valued pixels (any destination).  uint8 pixels take the
+// integer cell location (bit-exact to the reference); real pixels the fp64
+// one of lut_nodes_real.  Linear components accumulate out += w_j V[node_j]
+// in node order (lut.py:233-236), rounded like numpy.
+template <int N, int METHOD, typename TI>
+__global__ void k_lut_fp64(const double* __restrict__ lat, int mask, const TI* __restrict__ rgb,
+                           float* __restrict__ out, int64_t n, int planar) {
   constexpr int K = LutK<METHOD>::K;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t r = rgb[3 * i], g = rgb[3 * i + 1], b = rgb[3 * i + 2];
     int idx[K];
-    double w[K];
-    lut_nodes<N, METHOD, double>(r, g, b, idx, w);
+    double w[K], d[3];
+    if constexpr (sizeof(TI) == 1) {
+      const uint32_t r = rgb[3 * i], g = rgb[3 * i + 1], b = rgb[3 * i + 2];
+      lut_nodes<N, METHOD, double>(r, g, b, idx, w);
+      int bse, rem;
+      lut_locate<N>(r, bse, rem); d[0] = rem / 255.0;
+      lut_locate<N>(g, bse, rem); d[1] = rem / 255.0;
+      lut_locate<N>(b, bse, rem); d[2] = rem / 255.0;
+    } else {
+      lut_nodes_real<N, METHOD>(px_chan(rgb, 3 * i), px_chan(rgb, 3 * i + 1), px_chan(rgb, 3 * i + 2), idx, w, d);
+    }
     double res[3];
     for (int comp = 0; comp < 3; ++comp) {
       if (!((mask >> comp) & 1)) {
         double a = 0.0;
-        for (int j = 0; j < K; ++j) a += w[j] * lat[3 * idx[j] + comp];
+        for (int j = 0; j < K; ++j) a = __dadd_rn(a, __dmul_rn(w[j], lat[3 * idx[j] + comp]));
         res[comp] = a;
-      } else if (METHOD == MACT_LUT_TRILINEAR) {
-        int br, bg, bb, rr, rg, rb;
-        lut_locate<N>(r, br, rr);
-        lut_locate<N>(g, bg, rg);
-        lut_locate<N>(b, bb, rb);
-        const double dr = rr / 255.0, dg = rg / 255.0, db = rb / 255.0;
+      } else if (METHOD == MACT_LUT_TRILINEAR) {         // lut.py:249-262
         double v[8];
         for (int j = 0; j < 8; ++j) v[j] = lat[3 * idx[j] + comp];   // corner c = r<<2|g<<1|b
-        const double r00 = angular_lerp_d(v[0], v[4], dr), r01 = angular_lerp_d(v[1], v[5], dr);
-        const double r10 = angular_lerp_d(v[2], v[6], dr), r11 = angular_lerp_d(v[3], v[7], dr);
-        res[comp] = angular_lerp_d(angular_lerp_d(r00, r10, dg), angular_lerp_d(r01, r11, dg), db);
-      } else {
+        const double r00 = angular_lerp_d(v[0], v[4], d[0]), r01 = angular_lerp_d(v[1], v[5], d[0]);
+        const double r10 = angular_lerp_d(v[2], v[6], d[0]), r11 = angular_lerp_d(v[3], v[7], d[0]);
+        res[comp] = angular_lerp_d(angular_lerp_d(r00, r10, d[1]), angular_lerp_d(r01, r11, d[1]), d[2]);
+      } else {                                            // _circular_blend, lut.py:219-228
         double c = 0.0, sn = 0.0, wmax = w[0], heavy = lat[3 * idx[0] + comp];
         for (int j = 0; j < K; ++j) {
           const double t = lat[3 * idx[j] + comp];
@@ -560,20 +571,31 @@ static int interp_grid(int method, const float* lat, const uint8_t* rgb, float* 
   return set_error(MACT_EBADARG, "unknown interpolation method %d", method);
 }
 
-template <int N>
-static int interp_ang(int method, int mask, const double* lat, const uint8_t* rgb, float* out,
-                      int64_t n, int planar, cudaStream_t st) {
+template <int N, typename TI>
+static int interp_fp64(int method, int mask, const double* lat, const TI* rgb, float* out,
+                       int64_t n, int planar, cudaStream_t st) {
   int64_t g = (n + 255) / 256;
   if (g > 8LL * num_sms()) g = 8LL * num_sms();
   switch (method) {
-    case MACT_LUT_TRILINEAR: k_lut_angular<N, MACT_LUT_TRILINEAR><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
-    case MACT_LUT_PRISM: k_lut_angular<N, MACT_LUT_PRISM><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
-    case MACT_LUT_PYRAMIDAL: k_lut_angular<N, MACT_LUT_PYRAMIDAL><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
-    case MACT_LUT_TETRAHEDRAL: k_lut_angular<N, MACT_LUT_TETRAHEDRAL><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
+    case MACT_LUT_TRILINEAR: k_lut_fp64<N, MACT_LUT_TRILINEAR, TI><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
+    case MACT_LUT_PRISM: k_lut_fp64<N, MACT_LUT_PRISM, TI><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
+    case MACT_LUT_PYRAMIDAL: k_lut_fp64<N, MACT_LUT_PYRAMIDAL, TI><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
+    case MACT_LUT_TETRAHEDRAL: k_lut_fp64<N, MACT_LUT_TETRAHEDRAL, TI><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
     default: return set_error(MACT_EBADARG, "unknown interpolation method %d", method);
   }
   count_launch();
-  return check_launch("lut_interp_angular");
+  return check_launch("lut_interp_fp64");
+}
+
+template <typename TI>
+static int interp_fp64_grid(int grid_n, int method, int mask, const double* lat, const TI* rgb, float* out,
+                            int64_t n, int planar, cudaStream_t st) {
+  switch (grid_n) {
+    case 9: return interp_fp64<9>(method, mask, lat, rgb, out, n, planar, st);
+    case 17: return interp_fp64<17>(method, mask, lat, rgb, out, n, planar, st);
+    case 33: return interp_fp64<33>(method, mask, lat, rgb, out, n, planar, st);
+  }
+  return set_error(MACT_EBADARG, "grid_n must be one of 9, 17, 33");
 }
 
 template <int N>
@@ -641,17 +663,29 @@ extern "C" int mact_lut_nodes(int grid_n, int method, const uint8_t* rgb, int64_
 extern "C" int mact_lut_interp_angular(const double* lattice64, int grid_n, int method,
                                        int angular_mask, const uint8_t* rgb, float* out, int64_t n,
                                        int layout, void* stream) {
+  return mact_lut_interp_real(lattice64, grid_n, method, angular_mask, rgb, MACT_DTYPE_U8, out, n, layout,
+                              stream);
+}
+
+extern "C" int mact_lut_interp_real(const double* lattice64, int grid_n, int method, int angular_mask,
+                                    const void* rgb, int in_dtype, float* out, int64_t n, int layout,
+                                    void* stream) {
   if (n < 0 || (n > 0 && (!lattice64 || !rgb || !out))) return set_error(MACT_EBADARG, "bad argument");
   if (angular_mask < 0 || angular_mask > 7) return set_error(MACT_EBADARG, "bad angular mask %d", angular_mask);
   if (layout != MACT_LAYOUT_INTERLEAVED && layout != MACT_LAYOUT_PLANAR)
     return set_error(MACT_EBADARG, "unknown layout %d", layout);
+  if (grid_n != 9 && grid_n != 17 && grid_n != 33) return set_error(MACT_EBADARG, "grid_n must be one of 9, 17, 33");
+  if (method < 0 || method > 3) return set_error(MACT_EBADARG, "unknown interpolation method %d", method);
   if (n == 0) return MACT_OK;
   const int planar = layout == MACT_LAYOUT_PLANAR;
   cudaStream_t st = (cudaStream_t)stream;
-  switch (grid_n) {
-    case 9: return interp_ang<9>(method, angular_mask, lattice64, rgb, out, n, planar, st);
-    case 17: return interp_ang<17>(method, angular_mask, lattice64, rgb, out, n, planar, st);
-    case 33: return interp_ang<33>(method, angular_mask, lattice64, rgb, out, n, planar, st);
+  switch (in_dtype) {
+    case MACT_DTYPE_U8:
+      return interp_fp64_grid(grid_n, method, angular_mask, lattice64, (const uint8_t*)rgb, out, n, planar, st);
+    case MACT_DTYPE_F32:
+      return interp_fp64_grid(grid_n, method, angular_mask, lattice64, (const float*)rgb, out, n, planar, st);
+    case MACT_DTYPE_F64:
+      return interp_fp64_grid(grid_n, method, angular_mask, lattice64, (const double*)rgb, out, n, planar, st);
   }
-  return set_error(MACT_EBADARG, "grid_n must be one of 9, 17, 33");
+  return set_error(MACT_EBADARG, "unsupported input dtype %d", in_dtype);
 }

@@ -102,6 +102,82 @@ __device__ __forceinline__ void lut_nodes(uint32_t pr, uint32_t pg, uint32_t pb,
   }
 }
 
+// Real-valued pixels (lut.py:98-105 and :115-199 in fp64, the reference's
+// evaluation order): x = p / spacing, base = clamp(floor(x), 0, n-2),
+// frac = x - base (> 1 or < 0 outside [0, 255]: the reference extrapolates).
+template <int N>
+__device__ __forceinline__ void lut_locate_real(double p, int& base, double& frac) {
+  constexpr double spacing = 255.0 / (N - 1);         // exact for n = 9, 17, 33
+  const double x = __ddiv_rn(p, spacing);
+  double f = floor(x);
+  f = f > (double)(N - 2) ? (double)(N - 2) : f;
+  f = f < 0.0 ? 0.0 : f;
+  base = (int)f;
+  frac = __dadd_rn(x, -f);
+}
+
+template <int N, int METHOD>
+__device__ __forceinline__ void lut_nodes_real(double pr, double pg, double pb,
+                                               int (&idx)[LutK<METHOD>::K], double (&w)[LutK<METHOD>::K],
+                                               double (&d)[3]) {
+  constexpr int SR = N * N, SG = N, SB = 1;
+  int br, bg, bb;
+  lut_locate_real<N>(pr, br, d[0]);
+  lut_locate_real<N>(pg, bg, d[1]);
+  lut_locate_real<N>(pb, bb, d[2]);
+  const double dr = d[0], dg = d[1], db = d[2];
+  const int bf = (br * N + bg) * N + bb;
+  if constexpr (METHOD == MACT_LUT_TRILINEAR) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double wr = (c >> 2) & 1 ? dr : __dadd_rn(1.0, -dr);
+      const double wg = (c >> 1) & 1 ? dg : __dadd_rn(1.0, -dg);
+      const double wb = c & 1 ? db : __dadd_rn(1.0, -db);
+      idx[c] = bf + ((c >> 2) & 1) * SR + ((c >> 1) & 1) * SG + (c & 1) * SB;
+      w[c] = __dmul_rn(__dmul_rn(wr, wg), wb);
+    }
+  } else if constexpr (METHOD == MACT_LUT_PRISM) {
+    const bool up = dg >= db;
+    const double ta = up ? __dadd_rn(1.0, -dg) : __dadd_rn(1.0, -db);
+    const double tb = up ? __dadd_rn(dg, -db) : __dadd_rn(db, -dg);
+    const double tc = up ? db : dg;
+    const int mid = up ? SG : SB, far = SG + SB;
+    const double a0 = __dadd_rn(1.0, -dr);
+    idx[0] = bf; idx[1] = bf + mid; idx[2] = bf + far;
+    idx[3] = bf + SR; idx[4] = bf + mid + SR; idx[5] = bf + far + SR;
+    w[0] = __dmul_rn(ta, a0); w[1] = __dmul_rn(tb, a0); w[2] = __dmul_rn(tc, a0);
+    w[3] = __dmul_rn(ta, dr); w[4] = __dmul_rn(tb, dr); w[5] = __dmul_rn(tc, dr);
+  } else if constexpr (METHOD == MACT_LUT_PYRAMIDAL) {
+    const bool sel_r = (dg > dr) && (db > dr);
+    const bool sel_g = !sel_r && (dr >= dg) && (db >= dg);
+    const double dm = sel_r ? dr : sel_g ? dg : db;
+    const double du = sel_r ? dg : dr;
+    const double dv = sel_r ? db : sel_g ? db : dg;
+    const int nu = sel_r ? SG : SR;
+    const int nv = (sel_r || sel_g) ? SB : SG;
+    idx[0] = bf; idx[1] = bf + nu; idx[2] = bf + nv; idx[3] = bf + nu + nv; idx[4] = bf + SR + SG + SB;
+    w[0] = __dmul_rn(__dadd_rn(1.0, -du), __dadd_rn(1.0, -dv));
+    w[1] = __dmul_rn(du, __dadd_rn(1.0, -dv));
+    w[2] = __dmul_rn(dv, __dadd_rn(1.0, -du));
+    w[3] = __dadd_rn(__dmul_rn(du, dv), -dm);
+    w[4] = dm;
+  } else {
+    // stable argsort of -d (lut.py:185): ties keep r before g before b
+    const int pos_r = (dg > dr) + (db > dr);
+    const int pos_g = (dr >= dg) + (db > dg);
+    const int s1 = pos_r == 0 ? SR : pos_g == 0 ? SG : SB;
+    const double d1 = pos_r == 0 ? dr : pos_g == 0 ? dg : db;
+    const int s2 = pos_r == 1 ? SR : pos_g == 1 ? SG : SB;
+    const double d2 = pos_r == 1 ? dr : pos_g == 1 ? dg : db;
+    const double d3 = pos_r == 2 ? dr : pos_g == 2 ? dg : db;
+    idx[0] = bf; idx[1] = bf + s1; idx[2] = bf + s1 + s2; idx[3] = bf + SR + SG + SB;
+    w[0] = __dadd_rn(1.0, -d1);
+    w[1] = __dadd_rn(d1, -d2);
+    w[2] = __dadd_rn(d2, -d3);
+    w[3] = d3;
+  }
+}
+
 // lut.angular_lerp (lut.py:202-216): circular interpolation wrapped to
 // [0, 2 pi); a vanishing blended direction resolves to theta0 mod 2 pi.
 __device__ __forceinline__ double fmod2pi_d(double a) {

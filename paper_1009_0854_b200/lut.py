@@ -169,10 +169,15 @@ def interpolate(lut: Lut3D, pixels, method: str = "tetrahedral", variant: str = 
         arr = np.asarray(pixels)
         if arr.dtype == np.uint8 and arr.ndim >= 1 and arr.shape[-1] == 3:
             return _host_interp(lut, m, arr, out, layout)
-    t, lead, on_dev = _u8_pixels(pixels)
+    t, code, lead, on_dev = _dev.as_device_pixels(pixels)
     res = (_dev.check_out(out, lead, layout, t.device) if (out is not None and on_dev)
            else _dev.empty_out(lead, layout, t.device))
-    if mask:
+    if code != _lib.DTYPE_U8:
+        # real-valued pixels: fp64 cell location and weights (lut.py:98-199)
+        lat = lut.lattice64(t.device)
+        _lib.call("mact_lut_interp_real", lat.data_ptr(), lut.grid_n, m, mask, t.data_ptr(), code,
+                  res.data_ptr(), t.numel() // 3, _lib.LAYOUTS[layout], _dev.stream_ptr())
+    elif mask:
         lat = lut.lattice64(t.device)
         _lib.call("mact_lut_interp_angular", lat.data_ptr(), lut.grid_n, m, mask, t.data_ptr(),
                   res.data_ptr(), t.numel() // 3, _lib.LAYOUTS[layout], _dev.stream_ptr())

@@ -125,6 +125,17 @@ def elem_vectors() -> dict:
     for sp in ("lab", "hsi", "sct"):
         out[f"{sp}_fast_float"] = getattr(fast, f"rgb_to_{sp}_fast")(fpx)
         out[f"{sp}_exact_float"] = getattr(exact, f"rgb_to_{sp}_exact")(fpx)
+    # LUT interpolation of real-valued pixels: lattice coordinates, faces,
+    # ties and points just outside [0, 255] (the reference extrapolates)
+    lpx = np.r_[rng.random((400, 3)) * 255.0, [[255.0, 255.0, 255.0], [0.0, 0.0, 0.0], [255.5, -0.5, 128.0],
+                                               [15.9375, 31.875, 7.96875], [100.0, 100.0, 100.0],
+                                               [12.0, 12.0, 200.0], [200.0, 12.0, 12.0]]]
+    out["lut_px"] = lpx
+    for sp in ("lab", "hsi", "sct"):
+        for n in (9, 17, 33):
+            L = lut.build_lut(sp, n)
+            for m in lut.METHODS:
+                out[f"lutf_{sp}_{n}_{m}"] = lut.interpolate(L, lpx, m)
     return out
 
 

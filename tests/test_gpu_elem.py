@@ -128,3 +128,23 @@ def test_float_pixels_fast_and_exact(M, elem, space, dtype):
         __import__("oracle.mact_oracle", fromlist=["x"]).EXACT[space](ref_px)
     got = getattr(M["exact"], f"rgb_to_{space}_exact")(px)
     CHECK[space](got, exact_ref)
+
+
+@pytest.mark.parametrize("grid", [9, 17, 33])
+@pytest.mark.parametrize("space", ["lab", "hsi", "sct"])
+def test_lut_real_valued_pixels(elem, space, grid):
+    """lut.interpolate on float pixels (fp64 cell location, lut.py:98-199), every
+    method, linear and angular destinations, including extrapolation outside [0, 255]."""
+    from tests.parity_util import CHECK
+    from paper_1009_0854_b200 import lut
+    L = lut.build_lut(space, grid)
+    for dtype in (np.float64, np.float32):
+        px = elem["lut_px"].astype(dtype)
+        for m in ("trilinear", "prism", "pyramidal", "tetrahedral"):
+            if dtype == np.float64:
+                ref = elem[f"lutf_{space}_{grid}_{m}"]          # the reference itself
+            else:                                               # fp32 pixels: oracle on their fp64 values
+                from oracle import mact_oracle as O
+                ref = O.interpolate(O.build_lut_values(space, grid), px.astype(np.float64), m,
+                                    angular_mask=O.ANGULAR_MASKS[space])
+            CHECK[space](lut.interpolate(L, px, m), ref)

@@ -181,3 +181,12 @@ def test_float_pixels_vs_reference(elem):
     for sp in ("lab", "hsi", "sct"):
         eq(O.FAST[sp](elem["float_px"]), elem[f"{sp}_fast_float"])
         eq(O.EXACT[sp](elem["float_px"]), elem[f"{sp}_exact_float"])
+
+
+@pytest.mark.parametrize("space", ["lab", "hsi", "sct"])
+def test_lut_real_pixels_vs_reference(elem, space):
+    for n in (9, 17, 33):
+        vals = O.build_lut_values(space, n)
+        for m in O.METHODS:
+            got = O.interpolate(vals, elem["lut_px"], m, angular_mask=O.ANGULAR_MASKS[space])
+            eq(got, elem[f"lutf_{space}_{n}_{m}"])
