@@ -158,6 +158,11 @@ int mact_lut_interp_real(const double* lattice64, int grid_n, int method, int an
  * and weights (n,k), k = 8/6/5/4; indices bit-exact with the reference. */
 int mact_lut_nodes(int grid_n, int method, const uint8_t* rgb, int64_t n,
                    int32_t* nodes, float* weights, void* stream);
+/* the same for any pixel dtype (MACT_DTYPE_U8/F32/F64) with fp64 weights,
+ * computed exactly as lut.node_weights does (lut.py:98-199): bit-identical
+ * indices and weights */
+int mact_lut_nodes_real(int grid_n, int method, const void* rgb, int in_dtype, int64_t n,
+                        int32_t* nodes, double* weights, void* stream);
 
 /* ---- error reduction (K6) ------------------------------------------------ */
 /* Fused candidate + exact + metric + reduction over pixels rgb[0..n)

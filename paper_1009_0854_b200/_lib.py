@@ -74,6 +74,7 @@ _SIGNATURES = {
     "mact_lut_interp_angular": (_i, [_vp, _i, _i, _i, _vp, _vp, _i64, _i, _vp]),
     "mact_lut_interp_real": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _i64, _i, _vp]),
     "mact_lut_nodes": (_i, [_i, _i, _vp, _i64, _vp, _vp, _vp]),
+    "mact_lut_nodes_real": (_i, [_i, _i, _vp, _i, _i64, _vp, _vp, _vp]),
     "mact_err_workspace_bytes": (C.c_size_t, []),
     "mact_err_reduce": (_i, [C.POINTER(MactErrSpec), C.POINTER(MactCoeffs), _vp, _i64, _i64,
                              _i64, _vp, _vp, _vp]),

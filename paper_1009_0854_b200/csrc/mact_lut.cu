@@ -248,6 +248,25 @@ __global__ void k_lut_nodes(const uint8_t* __restrict__ rgb, int64_t n, int32_t*
   }
 }
 
+// Real-valued pixels: fp64 nodes and weights exactly as lut.node_weights
+// computes them (lut.py:115-199).
+template <int N, int METHOD, typename TI>
+__global__ void k_lut_nodes_real(const TI* __restrict__ rgb, int64_t n, int32_t* __restrict__ nodes,
+                                 double* __restrict__ weights) {
+  constexpr int K = LutK<METHOD>::K;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int idx[K];
+    double w[K], d[3];
+    lut_nodes_real<N, METHOD>((double)rgb[3 * i], (double)rgb[3 * i + 1], (double)rgb[3 * i + 2], idx, w, d);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      nodes[i * K + j] = idx[j];
+      weights[i * K + j] = w[j];
+    }
+  }
+}
+
 // ------------------------------------------------- 33^3: component-split clusters
 // The 33^3 lattice (35937 nodes) does not fit one CTA's shared memory as
 // float4 nodes (575 KB), but ONE component of it does (144 KB).  A cluster of
@@ -614,9 +633,46 @@ static int nodes_grid(int method, const uint8_t* rgb, int64_t n, int32_t* nodes,
   return check_launch("lut_nodes");
 }
 
+template <int N, typename TI>
+static int nodes_real_grid(int method, const TI* rgb, int64_t n, int32_t* nodes, double* w, cudaStream_t st) {
+  int64_t g = (n + 255) / 256;
+  if (g > 8LL * num_sms()) g = 8LL * num_sms();
+  switch (method) {
+    case MACT_LUT_TRILINEAR: k_lut_nodes_real<N, MACT_LUT_TRILINEAR, TI><<<(unsigned)g, 256, 0, st>>>(rgb, n, nodes, w); break;
+    case MACT_LUT_PRISM: k_lut_nodes_real<N, MACT_LUT_PRISM, TI><<<(unsigned)g, 256, 0, st>>>(rgb, n, nodes, w); break;
+    case MACT_LUT_PYRAMIDAL: k_lut_nodes_real<N, MACT_LUT_PYRAMIDAL, TI><<<(unsigned)g, 256, 0, st>>>(rgb, n, nodes, w); break;
+    case MACT_LUT_TETRAHEDRAL: k_lut_nodes_real<N, MACT_LUT_TETRAHEDRAL, TI><<<(unsigned)g, 256, 0, st>>>(rgb, n, nodes, w); break;
+    default: return set_error(MACT_EBADARG, "unknown interpolation method %d", method);
+  }
+  count_launch();
+  return check_launch("lut_nodes_real");
+}
+
+template <typename TI>
+static int nodes_real(int grid_n, int method, const TI* rgb, int64_t n, int32_t* nodes, double* w,
+                      cudaStream_t st) {
+  switch (grid_n) {
+    case 9: return nodes_real_grid<9>(method, rgb, n, nodes, w, st);
+    case 17: return nodes_real_grid<17>(method, rgb, n, nodes, w, st);
+    case 33: return nodes_real_grid<33>(method, rgb, n, nodes, w, st);
+  }
+  return set_error(MACT_EBADARG, "grid_n must be one of 9, 17, 33");
+}
+
 }  // namespace mact
 
 using namespace mact;
+
+extern "C" int mact_lut_nodes_real(int grid_n, int method, const void* rgb, int in_dtype, int64_t n,
+                                   int32_t* nodes, double* weights, void* stream) {
+  if (n < 0 || (n > 0 && (!rgb || !nodes || !weights))) return set_error(MACT_EBADARG, "bad argument");
+  if (n == 0) return MACT_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (in_dtype == MACT_DTYPE_U8) return nodes_real(grid_n, method, (const uint8_t*)rgb, n, nodes, weights, st);
+  if (in_dtype == MACT_DTYPE_F32) return nodes_real(grid_n, method, (const float*)rgb, n, nodes, weights, st);
+  if (in_dtype == MACT_DTYPE_F64) return nodes_real(grid_n, method, (const double*)rgb, n, nodes, weights, st);
+  return set_error(MACT_EBADARG, "unsupported input dtype %d", in_dtype);
+}
 
 extern "C" int mact_lut_build(int space, int grid_n, double* lattice_f64, float* lattice_f32,
                               void* stream) {

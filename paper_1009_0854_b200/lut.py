@@ -106,16 +106,17 @@ def _u8_pixels(pixels):
 
 
 def node_weights(lut: Lut3D, pixels, method: str):
-    """(flat node indices int32 (..., k), weights float32 (..., k)) (lut.py:115-199)."""
+    """(flat node indices int32 (..., k), float64 weights (..., k)), bit-identical to
+    the reference for every pixel dtype (lut.py:115-199)."""
     import torch
 
     m = _method_code(method)
-    t, lead, on_dev = _u8_pixels(pixels)
+    t, code, lead, on_dev = _dev.as_device_pixels(pixels)
     k = NEIGHBOR_COUNT[method]
     nodes = torch.empty(lead + (k,), dtype=torch.int32, device=t.device)
-    w = torch.empty(lead + (k,), dtype=torch.float32, device=t.device)
-    _lib.call("mact_lut_nodes", lut.grid_n, m, t.data_ptr(), t.numel() // 3, nodes.data_ptr(),
-              w.data_ptr(), _dev.stream_ptr())
+    w = torch.empty(lead + (k,), dtype=torch.float64, device=t.device)   # the reference's fp64 weights
+    _lib.call("mact_lut_nodes_real", lut.grid_n, m, t.data_ptr(), code, t.numel() // 3,
+              nodes.data_ptr(), w.data_ptr(), _dev.stream_ptr())
     return _dev.to_caller(nodes, on_dev), _dev.to_caller(w, on_dev)
 
 

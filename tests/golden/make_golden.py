@@ -136,6 +136,9 @@ def elem_vectors() -> dict:
             L = lut.build_lut(sp, n)
             for m in lut.METHODS:
                 out[f"lutf_{sp}_{n}_{m}"] = lut.interpolate(L, lpx, m)
+                if sp == "lab":
+                    nodes, w = lut.node_weights(L, lpx, m)
+                    out[f"nodesf_{n}_{m}"], out[f"weightsf_{n}_{m}"] = nodes.astype(np.int32), w
     return out
 
 

@@ -148,3 +148,14 @@ def test_lut_real_valued_pixels(elem, space, grid):
                 ref = O.interpolate(O.build_lut_values(space, grid), px.astype(np.float64), m,
                                     angular_mask=O.ANGULAR_MASKS[space])
             CHECK[space](lut.interpolate(L, px, m), ref)
+
+
+@pytest.mark.parametrize("grid", [9, 17, 33])
+def test_lut_node_weights_real_pixels_bit_exact(elem, grid):
+    """node_weights on float pixels: indices and fp64 weights bit-identical to the reference."""
+    from paper_1009_0854_b200 import lut
+    L = lut.build_lut("lab", grid)
+    for m in ("trilinear", "prism", "pyramidal", "tetrahedral"):
+        nodes, w = lut.node_weights(L, elem["lut_px"], m)
+        eq(nodes, elem[f"nodesf_{grid}_{m}"])
+        eq(w, elem[f"weightsf_{grid}_{m}"])

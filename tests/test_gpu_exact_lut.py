@@ -66,22 +66,35 @@ def test_lut_nodes_bit_exact(P, golden, n, method):
     lt = P["lut"].build_lut("lab", n)
     nodes, w = P["lut"].node_weights(lt, golden["small"], method)
     np.testing.assert_array_equal(nodes, golden[f"nodes_{n}_{method}"])
-    np.testing.assert_allclose(w, golden[f"weights_{n}_{method}"], atol=2e-7)
+    np.testing.assert_array_equal(w, golden[f"weights_{n}_{method}"])     # fp64, bit-identical
 
 
 @pytest.mark.parametrize("n", [9, 17, 33])
 @pytest.mark.parametrize("method", O.METHODS)
 def test_lut_nodes_full_cube(P, n, method):
-    """Every cube colour: node indices bit-exact against the oracle (C3 rows)."""
+    """Every cube colour: node indices bit-exact against the oracle (C3 rows), both
+    for the integer cell location the interpolation kernels use (mact_lut_nodes)
+    and for node_weights (fp64 weights, bit-identical)."""
+    from paper_1009_0854_b200 import _lib
     lt = P["lut"].build_lut("lab", n)
     cube = P["harness"].cube_chunk(0, 1 << 24, device="cuda")
+    k = P["lut"].NEIGHBOR_COUNT[method]
+    inodes = torch.empty((1 << 24, k), dtype=torch.int32, device="cuda")
+    iw = torch.empty((1 << 24, k), dtype=torch.float32, device="cuda")
+    _lib.call("mact_lut_nodes", n, _lib.METHODS[method], cube.data_ptr(), 1 << 24, inodes.data_ptr(),
+              iw.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    inodes = inodes.cpu().numpy()
+    iw = iw.cpu().numpy()
     nodes, w = P["lut"].node_weights(lt, cube, method)
-    nodes = nodes.cpu().numpy()
+    nodes, w = nodes.cpu().numpy(), w.cpu().numpy()
     host = cube.cpu().numpy()
     step = 1 << 22
     for s in range(0, 1 << 24, step):
         on, ow = O.node_weights(n, host[s:s + step], method)
+        np.testing.assert_array_equal(inodes[s:s + step], on)
         np.testing.assert_array_equal(nodes[s:s + step], on)
+        np.testing.assert_array_equal(w[s:s + step], ow)
+        np.testing.assert_allclose(iw[s:s + step], ow, rtol=0, atol=2e-7)
 
 
 @pytest.mark.parametrize("n", [9, 17, 33])

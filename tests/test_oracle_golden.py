@@ -190,3 +190,11 @@ def test_lut_real_pixels_vs_reference(elem, space):
         for m in O.METHODS:
             got = O.interpolate(vals, elem["lut_px"], m, angular_mask=O.ANGULAR_MASKS[space])
             eq(got, elem[f"lutf_{space}_{n}_{m}"])
+
+
+def test_lut_node_weights_real_pixels_vs_reference(elem):
+    for n in (9, 17, 33):
+        for m in O.METHODS:
+            nodes, w = O.node_weights(n, elem["lut_px"], m)
+            eq(nodes, elem[f"nodesf_{n}_{m}"])
+            eq(w, elem[f"weightsf_{n}_{m}"])
