@@ -111,6 +111,13 @@ int mact_hsi_fast(const void* rgb, int in_dtype, float* out, int64_t n,
 /* replaces mact.fast.rgb_to_sct_fast (fast.py:188-203) */
 int mact_sct_fast(const void* rgb, int in_dtype, float* out, int64_t n,
                   const MactCoeffs* c, int layout, void* stream);
+/* The fast transforms in the reference's own arithmetic: fp64 out, numpy's
+ * operation order, every operation rounded once, the fp64 GAMMA_TABLE.
+ * Bit-identical to mact.fast.rgb_to_*_fast (fast.py:86-203) for uint8 pixels
+ * (and for real-valued HSI/SCT pixels).  space = MACT_SPACE_*; the fidelity
+ * mode next to the fp32 throughput path above. */
+int mact_fast_f64(int space, const void* rgb, int in_dtype, double* out, int64_t n,
+                  const MactCoeffs* c, int layout, void* stream);
 /* all three from one read of the pixels (BASELINE config 5); any output may be NULL */
 int mact_all_fast(const uint8_t* rgb, float* lab, float* hsi, float* sct, int64_t n,
                   const MactCoeffs* c, int layout, void* stream);

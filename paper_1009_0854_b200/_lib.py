@@ -83,6 +83,7 @@ _SIGNATURES = {
     "mact_approx_eval": (_i, [C.POINTER(MactApproxSpec), _vp, _vp, _vp, _i64, _vp, _vp]),
     "mact_exact_elem": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]),
     "mact_exact_f32": (_i, [_i, _vp, _vp, _i64, _i, _vp]),
+    "mact_fast_f64": (_i, [_i, _vp, _i, _vp, _i64, C.POINTER(MactCoeffs), _i, _vp]),
     "mact_probe_expand": (_i, [_vp, _vp, _i64, _vp]),
     "mact_host_ctx_create": (_i, [_i, _i64, _i, C.POINTER(_vp)]),
     "mact_host_ctx_destroy": (_i, [_vp]),

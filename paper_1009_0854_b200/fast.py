@@ -107,13 +107,28 @@ def _host_u8(space: str, arr: np.ndarray, cfg: MactConfig, out, layout: str):
 
 
 def transform(space: str, pixels, cfg: MactConfig = DEFAULT_CONFIG, *, out=None,
-              layout: str = "interleaved"):
-    """Run one MACT fast transform (space in lab/hsi/sct) on the GPU."""
+              layout: str = "interleaved", out_dtype: str = "float32"):
+    """Run one MACT fast transform (space in lab/hsi/sct) on the GPU.
+
+    out_dtype "float32" (default) is the throughput path; "float64" evaluates
+    in the reference's own fp64 arithmetic (mact_fast_f64) and returns what
+    mact.fast returns, bit for bit for 8-bit pixels.
+    """
     if space not in _ENTRY:
         raise ValueError(f"unknown space {space!r}")
     if layout not in _lib.LAYOUTS:
         raise ValueError(f"unknown layout {layout!r}")
+    if out_dtype not in ("float32", "float64"):
+        raise ValueError(f"out_dtype must be float32 or float64, got {out_dtype!r}")
     _dev.require_cuda()
+    if out_dtype == "float64":
+        import torch
+
+        t, code, lead, on_dev = _dev.as_device_pixels(pixels)
+        res = _dev.empty_out(lead, layout, t.device, dtype=torch.float64)
+        _lib.call("mact_fast_f64", _lib.SPACES[space], t.data_ptr(), code, res.data_ptr(), t.numel() // 3,
+                  cfg.coeffs, _lib.LAYOUTS[layout], _dev.stream_ptr())
+        return _dev.to_caller(res, on_dev)
     if not _dev.is_device_tensor(pixels):
         arr = np.asarray(pixels)
         if arr.dtype == np.uint8 and arr.ndim >= 1 and arr.shape[-1] == 3:

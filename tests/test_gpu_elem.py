@@ -159,3 +159,46 @@ def test_lut_node_weights_real_pixels_bit_exact(elem, grid):
         nodes, w = lut.node_weights(L, elem["lut_px"], m)
         eq(nodes, elem[f"nodesf_{grid}_{m}"])
         eq(w, elem[f"weightsf_{grid}_{m}"])
+
+
+@pytest.mark.parametrize("space", ["lab", "hsi", "sct"])
+def test_fast_f64_bit_identical_to_reference(M, golden, space):
+    """out_dtype="float64": the reference's own arithmetic, bit for bit on the probe set."""
+    got = getattr(M["fast"], f"rgb_to_{space}_fast")(golden["probe"], out_dtype="float64")
+    assert got.dtype == np.float64
+    eq(got, golden[f"{space}_fast"])
+
+
+def test_fast_f64_other_degrees_and_layouts(M, golden):
+    fast = M["fast"]
+    s = golden["small"]
+    for n, m in [(2, 2), (3, 4), (4, 3)]:
+        eq(fast.rgb_to_lab_fast(s, fast.MactConfig(cielab_degrees=(n, m)), out_dtype="float64"),
+           golden[f"lab_fast_{n}{m}"])
+    for n in (2, 3, 4):
+        eq(fast.rgb_to_hsi_fast(s, fast.MactConfig(hsi_degree=n), out_dtype="float64"), golden[f"hsi_fast_{n}"])
+    for d in [(4, 4, 4), (4, 5, 5)]:
+        eq(fast.rgb_to_sct_fast(s, fast.MactConfig(sct_degrees=d), out_dtype="float64"),
+           golden["sct_fast_" + "".join(map(str, d))])
+    planar = fast.rgb_to_hsi_fast(torch.from_numpy(s).cuda(), out_dtype="float64", layout="planar")
+    eq(planar.cpu().numpy().T, fast.rgb_to_hsi_fast(s, out_dtype="float64"))
+
+
+def test_fast_f64_real_valued_pixels(M, elem):
+    fast = M["fast"]
+    for sp in ("hsi", "sct"):                    # basic operations only: bit-identical
+        eq(getattr(fast, f"rgb_to_{sp}_fast")(elem["float_px"], out_dtype="float64"), elem[f"{sp}_fast_float"])
+    lab = fast.rgb_to_lab_fast(elem["float_px"], out_dtype="float64")   # libdevice pow: within ulps
+    np.testing.assert_allclose(lab, elem["lab_fast_float"], rtol=0, atol=1e-12)
+
+
+def test_fast_f64_full_cube_vs_oracle(M):
+    """All 2^24 colours, fp64 mode, bit-identical to the oracle (itself pinned to the reference)."""
+    from oracle import mact_oracle as O
+    from paper_1009_0854_b200 import harness
+    cube = harness.cube_chunk(0, 1 << 24, device="cuda")
+    host = cube.cpu().numpy()
+    for sp in ("lab", "hsi", "sct"):
+        got = getattr(M["fast"], f"rgb_to_{sp}_fast")(cube, out_dtype="float64").cpu().numpy()
+        for s in range(0, 1 << 24, 1 << 22):
+            eq(got[s:s + (1 << 22)], O.FAST[sp](host[s:s + (1 << 22)]))
