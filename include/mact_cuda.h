@@ -155,12 +155,16 @@ int mact_lut_interp(const float* lattice, int grid_n, int method, const uint8_t*
 int mact_lut_interp_angular(const double* lattice64, int grid_n, int method, int angular_mask,
                             const uint8_t* rgb, float* out, int64_t n, int layout, void* stream);
 /* mact.lut.interpolate on any pixel dtype (MACT_DTYPE_U8/F32/F64) and any
- * destination, evaluated in fp64 on the fp64 (n^3,3) lattice: real-valued
- * pixels follow lut._locate / node_weights in fp64 (lut.py:98-199; pixels
- * outside [0, 255] extrapolate like the reference), angular components blend
- * on the circle (lut.py:202-262).  mact_lut_interp_angular is its uint8 case. */
+ * destination, evaluated in fp64 on the fp64 (n^3,3) lattice: cell location
+ * and weights follow lut._locate / node_weights in fp64 (lut.py:98-199;
+ * pixels outside [0, 255] extrapolate like the reference), linear
+ * components accumulate in the reference's order, angular ones blend on the
+ * circle (lut.py:202-262).  out_dtype MACT_DTYPE_F64 on a linear destination
+ * is bit-identical to the reference.  mact_lut_interp_angular is its uint8 /
+ * fp32-out case. */
 int mact_lut_interp_real(const double* lattice64, int grid_n, int method, int angular_mask,
-                         const void* rgb, int in_dtype, float* out, int64_t n, int layout, void* stream);
+                         const void* rgb, int in_dtype, void* out, int out_dtype, int64_t n, int layout,
+                         void* stream);
 /* replaces mact.lut.node_weights (lut.py:115-199): flat node indices (n,k)
  * and weights (n,k), k = 8/6/5/4; indices bit-exact with the reference. */
 int mact_lut_nodes(int grid_n, int method, const uint8_t* rgb, int64_t n,

@@ -149,29 +149,21 @@ struct OpLut {
 template <typename TI>
 __device__ __forceinline__ double px_chan(const TI* p, int64_t i) { return (double)p[i]; }
 
-// One kernel for every fp64 LUT evaluation: angular destinations (any pixel
-// type) and real-valued pixels (any destination).  uint8 pixels take the
-// integer cell location (bit-exact to the reference); real pixels the fp64
-// one of lut_nodes_real.  Linear components accumulate out += w_j V[node_j]
-// in node order (lut.py:233-236), rounded like numpy.
-template <int N, int METHOD, typename TI>
+// One kernel for every fp64 LUT evaluation: angular destinations, real-valued
+// pixels and the float64 fidelity mode.  Cell location and weights follow
+// lut._locate / node_weights in fp64 (lut_nodes_real, bit-identical to the
+// reference); linear components accumulate out += w_j V[node_j] in node order
+// (lut.py:233-236), rounded like numpy, so a linear destination with fp64
+// output reproduces the reference bit for bit.
+template <int N, int METHOD, typename TI, typename TO>
 __global__ void k_lut_fp64(const double* __restrict__ lat, int mask, const TI* __restrict__ rgb,
-                           float* __restrict__ out, int64_t n, int planar) {
+                           TO* __restrict__ out, int64_t n, int planar) {
   constexpr int K = LutK<METHOD>::K;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     int idx[K];
     double w[K], d[3];
-    if constexpr (sizeof(TI) == 1) {
-      const uint32_t r = rgb[3 * i], g = rgb[3 * i + 1], b = rgb[3 * i + 2];
-      lut_nodes<N, METHOD, double>(r, g, b, idx, w);
-      int bse, rem;
-      lut_locate<N>(r, bse, rem); d[0] = rem / 255.0;
-      lut_locate<N>(g, bse, rem); d[1] = rem / 255.0;
-      lut_locate<N>(b, bse, rem); d[2] = rem / 255.0;
-    } else {
-      lut_nodes_real<N, METHOD>(px_chan(rgb, 3 * i), px_chan(rgb, 3 * i + 1), px_chan(rgb, 3 * i + 2), idx, w, d);
-    }
+    lut_nodes_real<N, METHOD>(px_chan(rgb, 3 * i), px_chan(rgb, 3 * i + 1), px_chan(rgb, 3 * i + 2), idx, w, d);
     double res[3];
     for (int comp = 0; comp < 3; ++comp) {
       if (!((mask >> comp) & 1)) {
@@ -203,8 +195,8 @@ __global__ void k_lut_fp64(const double* __restrict__ lat, int mask, const TI* _
       }
     }
     for (int comp = 0; comp < 3; ++comp) {
-      if (planar) out[comp * n + i] = (float)res[comp];
-      else out[3 * i + comp] = (float)res[comp];
+      if (planar) out[comp * n + i] = (TO)res[comp];
+      else out[3 * i + comp] = (TO)res[comp];
     }
   }
 }
@@ -590,24 +582,24 @@ static int interp_grid(int method, const float* lat, const uint8_t* rgb, float* 
   return set_error(MACT_EBADARG, "unknown interpolation method %d", method);
 }
 
-template <int N, typename TI>
-static int interp_fp64(int method, int mask, const double* lat, const TI* rgb, float* out,
+template <int N, typename TI, typename TO>
+static int interp_fp64(int method, int mask, const double* lat, const TI* rgb, TO* out,
                        int64_t n, int planar, cudaStream_t st) {
   int64_t g = (n + 255) / 256;
   if (g > 8LL * num_sms()) g = 8LL * num_sms();
   switch (method) {
-    case MACT_LUT_TRILINEAR: k_lut_fp64<N, MACT_LUT_TRILINEAR, TI><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
-    case MACT_LUT_PRISM: k_lut_fp64<N, MACT_LUT_PRISM, TI><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
-    case MACT_LUT_PYRAMIDAL: k_lut_fp64<N, MACT_LUT_PYRAMIDAL, TI><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
-    case MACT_LUT_TETRAHEDRAL: k_lut_fp64<N, MACT_LUT_TETRAHEDRAL, TI><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
+    case MACT_LUT_TRILINEAR: k_lut_fp64<N, MACT_LUT_TRILINEAR, TI, TO><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
+    case MACT_LUT_PRISM: k_lut_fp64<N, MACT_LUT_PRISM, TI, TO><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
+    case MACT_LUT_PYRAMIDAL: k_lut_fp64<N, MACT_LUT_PYRAMIDAL, TI, TO><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
+    case MACT_LUT_TETRAHEDRAL: k_lut_fp64<N, MACT_LUT_TETRAHEDRAL, TI, TO><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
     default: return set_error(MACT_EBADARG, "unknown interpolation method %d", method);
   }
   count_launch();
   return check_launch("lut_interp_fp64");
 }
 
-template <typename TI>
-static int interp_fp64_grid(int grid_n, int method, int mask, const double* lat, const TI* rgb, float* out,
+template <typename TI, typename TO>
+static int interp_fp64_grid(int grid_n, int method, int mask, const double* lat, const TI* rgb, TO* out,
                             int64_t n, int planar, cudaStream_t st) {
   switch (grid_n) {
     case 9: return interp_fp64<9>(method, mask, lat, rgb, out, n, planar, st);
@@ -615,6 +607,14 @@ static int interp_fp64_grid(int grid_n, int method, int mask, const double* lat,
     case 33: return interp_fp64<33>(method, mask, lat, rgb, out, n, planar, st);
   }
   return set_error(MACT_EBADARG, "grid_n must be one of 9, 17, 33");
+}
+
+template <typename TI>
+static int interp_fp64_out(int out_dtype, int grid_n, int method, int mask, const double* lat, const TI* rgb,
+                           void* out, int64_t n, int planar, cudaStream_t st) {
+  if (out_dtype == MACT_DTYPE_F64)
+    return interp_fp64_grid(grid_n, method, mask, lat, rgb, (double*)out, n, planar, st);
+  return interp_fp64_grid(grid_n, method, mask, lat, rgb, (float*)out, n, planar, st);
 }
 
 template <int N>
@@ -719,17 +719,19 @@ extern "C" int mact_lut_nodes(int grid_n, int method, const uint8_t* rgb, int64_
 extern "C" int mact_lut_interp_angular(const double* lattice64, int grid_n, int method,
                                        int angular_mask, const uint8_t* rgb, float* out, int64_t n,
                                        int layout, void* stream) {
-  return mact_lut_interp_real(lattice64, grid_n, method, angular_mask, rgb, MACT_DTYPE_U8, out, n, layout,
-                              stream);
+  return mact_lut_interp_real(lattice64, grid_n, method, angular_mask, rgb, MACT_DTYPE_U8, out,
+                              MACT_DTYPE_F32, n, layout, stream);
 }
 
 extern "C" int mact_lut_interp_real(const double* lattice64, int grid_n, int method, int angular_mask,
-                                    const void* rgb, int in_dtype, float* out, int64_t n, int layout,
-                                    void* stream) {
+                                    const void* rgb, int in_dtype, void* out, int out_dtype, int64_t n,
+                                    int layout, void* stream) {
   if (n < 0 || (n > 0 && (!lattice64 || !rgb || !out))) return set_error(MACT_EBADARG, "bad argument");
   if (angular_mask < 0 || angular_mask > 7) return set_error(MACT_EBADARG, "bad angular mask %d", angular_mask);
   if (layout != MACT_LAYOUT_INTERLEAVED && layout != MACT_LAYOUT_PLANAR)
     return set_error(MACT_EBADARG, "unknown layout %d", layout);
+  if (out_dtype != MACT_DTYPE_F32 && out_dtype != MACT_DTYPE_F64)
+    return set_error(MACT_EBADARG, "out_dtype must be f32 or f64 (%d)", out_dtype);
   if (grid_n != 9 && grid_n != 17 && grid_n != 33) return set_error(MACT_EBADARG, "grid_n must be one of 9, 17, 33");
   if (method < 0 || method > 3) return set_error(MACT_EBADARG, "unknown interpolation method %d", method);
   if (n == 0) return MACT_OK;
@@ -737,11 +739,11 @@ extern "C" int mact_lut_interp_real(const double* lattice64, int grid_n, int met
   cudaStream_t st = (cudaStream_t)stream;
   switch (in_dtype) {
     case MACT_DTYPE_U8:
-      return interp_fp64_grid(grid_n, method, angular_mask, lattice64, (const uint8_t*)rgb, out, n, planar, st);
+      return interp_fp64_out(out_dtype, grid_n, method, angular_mask, lattice64, (const uint8_t*)rgb, out, n, planar, st);
     case MACT_DTYPE_F32:
-      return interp_fp64_grid(grid_n, method, angular_mask, lattice64, (const float*)rgb, out, n, planar, st);
+      return interp_fp64_out(out_dtype, grid_n, method, angular_mask, lattice64, (const float*)rgb, out, n, planar, st);
     case MACT_DTYPE_F64:
-      return interp_fp64_grid(grid_n, method, angular_mask, lattice64, (const double*)rgb, out, n, planar, st);
+      return interp_fp64_out(out_dtype, grid_n, method, angular_mask, lattice64, (const double*)rgb, out, n, planar, st);
   }
   return set_error(MACT_EBADARG, "unsupported input dtype %d", in_dtype);
 }

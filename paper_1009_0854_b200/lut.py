@@ -156,9 +156,16 @@ def _host_interp(lut: Lut3D, method_code: int, arr: np.ndarray, out, layout: str
 
 
 def interpolate(lut: Lut3D, pixels, method: str = "tetrahedral", variant: str = "standard", *,
-                out=None, layout: str = "interleaved"):
-    """Interpolate destination triples for RGB in [0, 255] (lut.py:341-350)."""
+                out=None, layout: str = "interleaved", out_dtype: str = "float32"):
+    """Interpolate destination triples for RGB in [0, 255] (lut.py:341-350).
+
+    out_dtype "float32" (default) is the throughput path (fp32 lattice in
+    shared memory); "float64" evaluates on the fp64 lattice in the reference's
+    arithmetic, bit-identical for linear destinations.
+    """
     m = _method_code(method)
+    if out_dtype not in ("float32", "float64"):
+        raise ValueError(f"out_dtype must be float32 or float64, got {out_dtype!r}")
     if variant not in VARIANTS:
         raise ValueError(f"unknown variant {variant!r}")
     if variant == "caching" and lut.cache is None:
@@ -166,6 +173,15 @@ def interpolate(lut: Lut3D, pixels, method: str = "tetrahedral", variant: str = 
     if layout not in _lib.LAYOUTS:
         raise ValueError(f"unknown layout {layout!r}")
     mask = sum(1 << c for c, ang in enumerate(lut.angular_mask) if ang)
+    if out_dtype == "float64":
+        import torch
+
+        t, code, lead, on_dev = _dev.as_device_pixels(pixels)
+        res = _dev.empty_out(lead, layout, t.device, dtype=torch.float64)
+        lat = lut.lattice64(t.device)
+        _lib.call("mact_lut_interp_real", lat.data_ptr(), lut.grid_n, m, mask, t.data_ptr(), code,
+                  res.data_ptr(), _lib.DTYPE_F64, t.numel() // 3, _lib.LAYOUTS[layout], _dev.stream_ptr())
+        return _dev.to_caller(res, on_dev)
     if not mask and not _dev.is_device_tensor(pixels):
         arr = np.asarray(pixels)
         if arr.dtype == np.uint8 and arr.ndim >= 1 and arr.shape[-1] == 3:
@@ -177,7 +193,7 @@ def interpolate(lut: Lut3D, pixels, method: str = "tetrahedral", variant: str = 
         # real-valued pixels: fp64 cell location and weights (lut.py:98-199)
         lat = lut.lattice64(t.device)
         _lib.call("mact_lut_interp_real", lat.data_ptr(), lut.grid_n, m, mask, t.data_ptr(), code,
-                  res.data_ptr(), t.numel() // 3, _lib.LAYOUTS[layout], _dev.stream_ptr())
+                  res.data_ptr(), _lib.DTYPE_F32, t.numel() // 3, _lib.LAYOUTS[layout], _dev.stream_ptr())
     elif mask:
         lat = lut.lattice64(t.device)
         _lib.call("mact_lut_interp_angular", lat.data_ptr(), lut.grid_n, m, mask, t.data_ptr(),

@@ -202,3 +202,19 @@ def test_fast_f64_full_cube_vs_oracle(M):
         got = getattr(M["fast"], f"rgb_to_{sp}_fast")(cube, out_dtype="float64").cpu().numpy()
         for s in range(0, 1 << 24, 1 << 22):
             eq(got[s:s + (1 << 22)], O.FAST[sp](host[s:s + (1 << 22)]))
+
+
+@pytest.mark.parametrize("grid", [9, 17, 33])
+def test_lut_f64_bit_identical_to_reference(golden, elem, grid):
+    """interpolate(out_dtype="float64"): linear destination bit-identical to lut.interpolate,
+    for 8-bit and real-valued pixels."""
+    from paper_1009_0854_b200 import lut
+    L = lut.build_lut("lab", grid)
+    for m in ("trilinear", "prism", "pyramidal", "tetrahedral"):
+        got = lut.interpolate(L, golden["small"], m, out_dtype="float64")
+        assert got.dtype == np.float64
+        # the lattice is built on the GPU (libdevice cbrt/pow): compare against the oracle on OUR lattice
+        from oracle import mact_oracle as O
+        vals = L.values
+        eq(got, O.interpolate(vals, golden["small"], m))
+        eq(lut.interpolate(L, elem["lut_px"], m, out_dtype="float64"), O.interpolate(vals, elem["lut_px"], m))
