@@ -50,7 +50,8 @@ enum {
   MACT_LUT_TETRAHEDRAL = 3
 };
 enum { MACT_METRIC_DISTANCE = 0, MACT_METRIC_COMPONENT = 1 };
-enum { MACT_CAND_FAST = 0, MACT_CAND_LUT = 1, MACT_CAND_ARRAY = 2 };
+enum { MACT_CAND_FAST = 0, MACT_CAND_LUT = 1, MACT_CAND_ARRAY = 2,
+       MACT_CAND_FAST_F64 = 3 /* fast transform in the reference's fp64 arithmetic */ };
 
 #define MACT_MAX_COEFFS 8
 

@@ -24,7 +24,7 @@ LAYOUTS = {"interleaved": 0, "planar": 1}
 DTYPE_U8, DTYPE_F32, DTYPE_F64 = 0, 1, 2
 METHODS = {"trilinear": 0, "prism": 1, "pyramidal": 2, "tetrahedral": 3}
 METRIC_DISTANCE, METRIC_COMPONENT = 0, 1
-CAND_FAST, CAND_LUT, CAND_ARRAY = 0, 1, 2
+CAND_FAST, CAND_LUT, CAND_ARRAY, CAND_FAST_F64 = 0, 1, 2, 3
 MAX_COEFFS = 8
 
 _c_double8 = C.c_double * MAX_COEFFS

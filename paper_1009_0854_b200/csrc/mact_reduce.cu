@@ -14,6 +14,7 @@
 
 #include "mact_lut.cuh"
 #include "mact_pixel.cuh"
+#include "mact_ref.cuh"
 
 namespace mact {
 
@@ -108,11 +109,11 @@ __device__ __forceinline__ void load3(const void* p, int64_t i, double* o) {
 template <int NC>
 __global__ void __launch_bounds__(kRedThreads) k_err(const __grid_constant__ RedParams p,
                                                      MactErrStats* __restrict__ parts) {
+  // the reference's fp64 GAMMA_TABLE (fast.py:35, exact.py:52-57 at i/255) and its fp32 rounding
   __shared__ float gamma_rep[256 * 32];
   __shared__ double gamma_d[256];
-  for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x)
-    gamma_rep[i] = (float)inverse_gamma_d((double)(i >> 5) / 255.0);
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) gamma_d[i] = inverse_gamma_d(i / 255.0);
+  for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) gamma_rep[i] = (float)ref::kGammaF64[i >> 5];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) gamma_d[i] = ref::kGammaF64[i];
   __syncthreads();
   const MactErrSpec& s = p.spec;
   const uint32_t lane = threadIdx.x & 31;
@@ -135,6 +136,10 @@ __global__ void __launch_bounds__(kRedThreads) k_err(const __grid_constant__ Red
       else if (s.space == MACT_SPACE_HSI) v = hsi_fast_u8(r, g, b, p.c);
       else v = sct_fast_u8(r, g, b, p.c);
       cand[0] = v.c0; cand[1] = v.c1; cand[2] = v.c2;
+    } else if (s.candidate == MACT_CAND_FAST_F64) {        // the reference's own arithmetic
+      if (s.space == MACT_SPACE_LAB) ref::lab_fast(gamma_d[r], gamma_d[g], gamma_d[b], p.c, cand);
+      else if (s.space == MACT_SPACE_HSI) ref::hsi_fast((double)r, (double)g, (double)b, p.c, cand);
+      else ref::sct_fast((double)r, (double)g, (double)b, p.c, cand);
     } else if (s.candidate == MACT_CAND_LUT) {
       if (s.lut_grid_n == 9) lut_value<9>(s.lut_lattice, s.lut_method, r, g, b, cand);
       else if (s.lut_grid_n == 17) lut_value<17>(s.lut_lattice, s.lut_method, r, g, b, cand);
@@ -230,14 +235,14 @@ extern "C" int mact_err_reduce(const MactErrSpec* spec, const MactCoeffs* c, con
       return set_error(MACT_EBADARG, "unknown interpolation method %d", spec->lut_method);
   } else if (spec->candidate == MACT_CAND_ARRAY) {
     if (!spec->cand_array) return set_error(MACT_EBADARG, "array candidate without data");
-  } else if (spec->candidate != MACT_CAND_FAST) {
+  } else if (spec->candidate != MACT_CAND_FAST && spec->candidate != MACT_CAND_FAST_F64) {
     return set_error(MACT_EBADARG, "unknown candidate kind %d", spec->candidate);
   }
   if (spec->candidate != MACT_CAND_ARRAY && !rgb && cube_start < 0)
     return set_error(MACT_EBADARG, "candidate needs pixels");
   RedParams p;
   p.spec = *spec;
-  if (spec->candidate == MACT_CAND_FAST) {
+  if (spec->candidate == MACT_CAND_FAST || spec->candidate == MACT_CAND_FAST_F64) {
     if (int rc = make_kcoeffs(c, &p.c)) return rc;
   } else {
     memset(&p.c, 0, sizeof p.c);

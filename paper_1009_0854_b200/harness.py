@@ -94,9 +94,12 @@ class LutCandidate:
         return _lut.interpolate(self.lut, pixels, self.method)
 
 
-def fast_candidate(space: str, cfg: "fast.MactConfig" = None):
-    """The fast transform of ``space`` bound to ``cfg`` (fusable by measure_error)."""
+def fast_candidate(space: str, cfg: "fast.MactConfig" = None, *, out_dtype: str = "float32"):
+    """The fast transform of ``space`` bound to ``cfg`` (fusable by measure_error).
+    out_dtype "float64" scores the reference's own fp64 arithmetic."""
     fn = {"lab": fast.rgb_to_lab_fast, "hsi": fast.rgb_to_hsi_fast, "sct": fast.rgb_to_sct_fast}[space]
+    if out_dtype == "float64":
+        return functools.partial(fn, cfg=cfg or fast.DEFAULT_CONFIG, out_dtype="float64")
     return functools.partial(fn, cfg=cfg or fast.DEFAULT_CONFIG)
 
 
@@ -107,14 +110,18 @@ _EXACT_FN = {exact.rgb_to_lab_exact: "lab", exact.rgb_to_hsi_exact: "hsi",
 
 def _classify(space: str, candidate):
     """-> (kind, payload) with kind in fast/lut/array."""
-    fn, cfg = candidate, fast.DEFAULT_CONFIG
+    fn, cfg, odt = candidate, fast.DEFAULT_CONFIG, "float32"
     if isinstance(candidate, functools.partial):
         fn = candidate.func
         if candidate.args:
             cfg = candidate.args[0]
         cfg = candidate.keywords.get("cfg", cfg)
+        odt = candidate.keywords.get("out_dtype", odt)
+        extra = set(candidate.keywords) - {"cfg", "out_dtype"}
+        if extra or len(candidate.args) > 1:
+            fn = None                                     # other bound arguments: evaluate as-is
     if _FAST_FN.get(fn) == space and isinstance(cfg, fast.MactConfig):
-        return "fast", cfg
+        return ("fast64" if odt == "float64" else "fast"), cfg
     if (isinstance(candidate, LutCandidate) and space == candidate.lut.destination_space
             and not any(candidate.lut.angular_mask)):
         return "lut", candidate                # fused (linear destinations); angular -> array path
@@ -152,8 +159,8 @@ def reduce_partials(space: str, candidate, reference, pixels=None, *, cube_start
         raise ValueError("empty population")
     device = t.device if t is not None else torch.device("cuda", torch.cuda.current_device())
     cfg = fast.DEFAULT_CONFIG
-    if kind == "fast":
-        spec.candidate = _lib.CAND_FAST
+    if kind in ("fast", "fast64"):
+        spec.candidate = _lib.CAND_FAST_F64 if kind == "fast64" else _lib.CAND_FAST
         cfg = payload
     elif kind == "lut":
         spec.candidate = _lib.CAND_LUT

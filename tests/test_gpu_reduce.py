@@ -164,3 +164,21 @@ def test_measure_gain_device_timed(P):
         h.measure_gain("lab", fast.rgb_to_lab_fast, exact.rgb_to_lab_exact, [])
     with pytest.raises(ValueError):
         h.measure_gain("lab", fast.rgb_to_lab_fast, exact.rgb_to_lab_exact, corpus, repeats_fast=2)
+
+
+@pytest.mark.parametrize("key,space,kw", [("lab_44", "lab", {}), ("lab_22", "lab", dict(cielab_degrees=(2, 2))),
+                                          ("hsi_5", "hsi", {}), ("sct_555", "sct", {})])
+def test_cube_figures_fidelity_mode(P, figures, key, space, kw):
+    """With the fp64 candidate (the reference's own arithmetic) the fused reduction
+    reproduces the reference's Tables 9-11 figures to 1e-10 (Lab) / 1e-8 instead of ~1e-4."""
+    h = P["harness"]
+    cfg = P["fast"].MactConfig(**kw)
+    st = h.measure_error(space, h.fast_candidate(space, cfg, out_dtype="float64"),
+                         getattr(P["exact"], f"rgb_to_{space}_exact"))
+    ref = figures["cube"][key]
+    assert st.count == ref["count"] and list(st.argmax_pixel) == ref["argmax_pixel"]
+    # Lab's distance is a plain Euclidean norm; the HSI cylinder and the SCT indirect
+    # distance go through libdevice sin/cos/cbrt/pow, a few ulps from numpy's libm.
+    rtol = 1e-10 if space == "lab" else 1e-8
+    assert abs(st.avg - ref["avg"]) <= rtol * ref["avg"], (st.avg, ref["avg"])
+    assert abs(st.max - ref["max"]) <= rtol * ref["max"], (st.max, ref["max"])
