@@ -105,3 +105,38 @@ def test_gamma_table_header_is_current():
     for bits, name in gen.FILES.items():
         with open(os.path.join(root, "paper_1009_0854_b200", "csrc", name)) as fh:
             assert fh.read() == gen.render(bits), name
+
+
+def test_plain_c_client_links_and_gets_status_codes(tmp_path, lib):
+    """A C program (no Python, no torch) links libmact_cuda.so through the header
+    alone and gets the documented status codes for argument errors, which are
+    decided before any CUDA call (so this runs without a GPU)."""
+    from paper_1009_0854_b200 import _lib
+    src = tmp_path / "client.c"
+    src.write_text(r'''
+#include <stdio.h>
+#include <string.h>
+#include "mact_cuda.h"
+int main(void) {
+  MactCoeffs c; memset(&c, 0, sizeof c);
+  c.cbrt_num_deg = 4; c.cbrt_den_deg = 4; c.hsi_deg = 5; c.asin_deg = 5; c.acos_deg = 5; c.atan_deg = 5;
+  int ok = 1;
+  ok &= mact_version() == 100;
+  ok &= mact_lab_fast(NULL, MACT_DTYPE_U8, NULL, -1, &c, MACT_LAYOUT_INTERLEAVED, NULL) == MACT_EBADARG;
+  ok &= strlen(mact_last_error()) > 0;
+  ok &= mact_lab_fast(NULL, MACT_DTYPE_U8, NULL, 0, &c, 7, NULL) == MACT_EBADARG;        /* bad layout */
+  c.cbrt_num_deg = 5;                                                                   /* no such set */
+  ok &= mact_hsi_fast(NULL, MACT_DTYPE_U8, NULL, 0, &c, MACT_LAYOUT_INTERLEAVED, NULL) == MACT_EUNKNOWN_APPROX;
+  ok &= mact_lut_interp(NULL, 17, MACT_LUT_TETRAHEDRAL, NULL, NULL, 0, 0, NULL) == MACT_OK;  /* n = 0: no-op */
+  ok &= mact_lut_interp(NULL, 17, 9, NULL, NULL, 0, 0, NULL) == MACT_EBADARG;          /* unknown method */
+  ok &= mact_exact(5, NULL, MACT_DTYPE_U8, NULL, MACT_DTYPE_F64, 0, NULL) == MACT_EBADARG;
+  printf("%s\n", ok ? "ok" : "FAIL");
+  return ok ? 0 : 1;
+}
+''')
+    exe = tmp_path / "client"
+    libdir = str(_lib.LIB_PATH.parent)
+    subprocess.run(["gcc", "-std=c99", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+                    "-L", libdir, "-l:" + _lib.LIB_PATH.name, "-Wl,-rpath," + libdir], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stdout + r.stderr
