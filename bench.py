@@ -260,6 +260,10 @@ def run_ours(args, wl):
         tot = parallel.combine(parallel.all_gather_partials(parts, dev))[0]
         err = {"dE_mean": tot["sum"] / tot["count"], "dE_max": tot["max"],
                "dE_argmax_index": tot["argmax"], "pixels": tot["count"]}
+        if space == "lut":   # config 3: "compared with MACT on the same pixels"
+            parts = harness.reduce_partials("lab", harness.fast_candidate("lab"), None, xf, index_base=base)
+            m = parallel.combine(parallel.all_gather_partials(parts, dev))[0]
+            err["mact_dE_mean"], err["mact_dE_max"] = m["sum"] / m["count"], m["max"]
     if space in ("all", "hsi+sct"):   # configs 2 and 5: per-component |fast - exact|
         err = err or {}
         for sp in ("hsi", "sct"):
