@@ -236,7 +236,8 @@ int mact_call_counts(unsigned long long* counts, void* stream);
 /* Runs a fast transform over HOST buffers: chunked H2D -> kernel -> D2H on
  * `nstreams` CUDA streams so both copy engines and the SMs overlap.  Host
  * buffers should be pinned (cudaHostAlloc / registered); pageable buffers are
- * staged through pinned bounce buffers.  op = MACT_SPACE_* (fast transform). */
+ * staged through pinned bounce buffers.  op = MACT_SPACE_* (fast transform).
+ * Calls on one context are serialised internally (thread-safe). */
 typedef struct MactHostCtx MactHostCtx;
 int mact_host_ctx_create(int device, int64_t chunk_px, int nstreams, MactHostCtx** ctx);
 int mact_host_ctx_destroy(MactHostCtx* ctx);

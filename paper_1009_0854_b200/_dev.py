@@ -118,8 +118,18 @@ def host_ctx(device: int, chunk_px: int = 1 << 23, nstreams: int = 3):
         if key not in _ctx:
             h = C.c_void_p()
             _lib.call("mact_host_ctx_create", device, chunk_px, nstreams, C.byref(h))
-            _ctx[key] = h
-        return _ctx[key]
+            _ctx[key] = (h, threading.Lock())
+        return _ctx[key][0]
+
+
+def host_call(name: str, device: int, *args):
+    """Call a host-executor entry point on the device's shared context.  A context
+    owns streams and staging buffers, so concurrent callers (the reference's
+    harness uses a thread pool, harness.py:99-101) are serialised on it; one
+    call already keeps both copy engines and the SMs busy."""
+    ctx = host_ctx(device)
+    with _ctx[(device, 1 << 23, 3)][1]:
+        return _lib.call(name, ctx, *args)
 
 
 def np_ptr(a: np.ndarray) -> int:

@@ -10,6 +10,7 @@
 // memcpy of chunk k overlapping the DMA of chunk k-1.
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -25,6 +26,7 @@ struct MactHostCtx {
   std::vector<float*> d_out;
   std::vector<uint8_t*> h_in;           // pinned bounce buffers (pageable callers)
   std::vector<float*> h_out;
+  std::mutex mu;                        // one call at a time owns the streams and staging buffers
 };
 
 using namespace mact;
@@ -148,6 +150,7 @@ static cudaError_t copy_out(float* host_out, const float* dout, int64_t off, int
 template <class Launch>
 static int stream_host(MactHostCtx* c, const uint8_t* host_rgb, float* host_out, int64_t n,
                        int layout, Launch&& launch) {
+  std::lock_guard<std::mutex> guard(c->mu);
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(c->device);

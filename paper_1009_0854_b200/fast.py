@@ -99,10 +99,8 @@ def _host_u8(space: str, arr: np.ndarray, cfg: MactConfig, out, layout: str):
     lead = src.shape[:-1]
     n = int(np.prod(lead, dtype=np.int64)) if lead else 1
     out = _dev.host_out(out, lead, layout)
-    dev = torch.cuda.current_device()
-    ctx = _dev.host_ctx(dev)
-    _lib.call("mact_transform_host", ctx, _lib.SPACES[space], _dev.np_ptr(src), _dev.np_ptr(out),
-              n, cfg.coeffs, _lib.LAYOUTS[layout])
+    _dev.host_call("mact_transform_host", torch.cuda.current_device(), _lib.SPACES[space], _dev.np_ptr(src),
+                   _dev.np_ptr(out), n, cfg.coeffs, _lib.LAYOUTS[layout])
     return out
 
 

@@ -150,8 +150,8 @@ def _host_interp(lut: Lut3D, method_code: int, arr: np.ndarray, out, layout: str
     dev = torch.cuda.current_device()
     lat = lut.lattice(torch.device("cuda", dev))
     torch.cuda.current_stream().synchronize()          # the executor runs on its own streams
-    _lib.call("mact_lut_interp_host", _dev.host_ctx(dev), lat.data_ptr(), lut.grid_n, method_code,
-              _dev.np_ptr(src), _dev.np_ptr(out), n, _lib.LAYOUTS[layout])
+    _dev.host_call("mact_lut_interp_host", dev, lat.data_ptr(), lut.grid_n, method_code,
+                   _dev.np_ptr(src), _dev.np_ptr(out), n, _lib.LAYOUTS[layout])
     return out
 
 

@@ -117,3 +117,16 @@ def test_cuda_graph_capture_and_replay(P):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(o1.cpu().numpy(), eager1.cpu().numpy())
     np.testing.assert_array_equal(o2.cpu().numpy(), eager2.cpu().numpy())
+
+
+def test_concurrent_host_callers(P):
+    """numpy callers from a thread pool (harness.py:99-101) share the host executor safely."""
+    from concurrent.futures import ThreadPoolExecutor
+    fast = P["fast"]
+    rng = np.random.default_rng(21)
+    imgs = [rng.integers(0, 256, ((1 << 22) + 17 * k, 3), dtype=np.uint8) for k in range(6)]
+    ref = [fast.rgb_to_lab_fast(torch.from_numpy(im).cuda()).cpu().numpy() for im in imgs]
+    with ThreadPoolExecutor(max_workers=6) as pool:
+        got = list(pool.map(fast.rgb_to_lab_fast, imgs))
+    for a, b in zip(got, ref):
+        np.testing.assert_array_equal(a, b)
