@@ -77,8 +77,10 @@ def test_combine_matches_single_and_first_argmax():
     assert math.isclose(tot["sum"], single["sum"], rel_tol=1e-14)
 
 
-@pytest.mark.timeout(120)
-def test_gloo_world2_combine():
+@pytest.mark.timeout(180)
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_combine(world):
+    """world 2 and an uneven world 3: every rank folds the same statistics as one process."""
     import multiprocessing as mp
 
     ctx = mp.get_context("spawn")
@@ -88,17 +90,19 @@ def test_gloo_world2_combine():
     data[5] = np.nan
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, data, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, data, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=90) for _ in range(2)]
+    res = [q.get(timeout=120) for _ in range(world)]
     for p in procs:
         p.join(timeout=30)
         assert p.exitcode == 0
     single = _partials_for(data, 0)
+    starts = [parallel.shard_range(len(data), world, r).start for r in range(world)]
     for rank, tot, t, argmaxes in res:
         assert tot["argmax"] == 20 == single["argmax"]
         assert tot["max"] == 3.0 and tot["count"] == single["count"] and tot["nan"] == 1
         assert math.isclose(tot["sum"], single["sum"], rel_tol=1e-14)
-        assert t == 2.0                                   # max over ranks
-        assert argmaxes[0] < 5001 <= argmaxes[1]          # rank order = index order
+        assert t == float(world)                          # max over ranks
+        assert all(starts[r] <= argmaxes[r] < (starts[r + 1] if r + 1 < world else len(data))
+                   for r in range(world))                 # rank order = index order
