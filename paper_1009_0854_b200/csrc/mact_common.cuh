@@ -183,6 +183,14 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 
 // ------------------------------------------------------------- host side
 void count_launch(int k = 1);
+// NVTX range around a library call (visible in Nsight Systems / `ncu --nvtx`);
+// a few ns when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name);
+  ~NvtxRange();
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 int set_error(int code, const char* fmt, ...);
 int check_launch(const char* what);
 int num_sms();

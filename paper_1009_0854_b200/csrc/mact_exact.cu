@@ -192,6 +192,7 @@ using namespace mact;
 
 extern "C" int mact_exact(int space, const void* rgb, int in_dtype, void* out, int out_dtype,
                           int64_t n, void* stream) {
+  NvtxRange range("mact_exact");
   if (space < 0 || space > MACT_SPACE_HSI_ARCCOS) return set_error(MACT_EBADARG, "unknown space %d", space);
   if (n < 0 || (n > 0 && (!rgb || !out))) return set_error(MACT_EBADARG, "bad argument");
   if (n == 0) return MACT_OK;

@@ -151,6 +151,7 @@ template <class Launch>
 static int stream_host(MactHostCtx* c, const uint8_t* host_rgb, float* host_out, int64_t n,
                        int layout, Launch&& launch) {
   std::lock_guard<std::mutex> guard(c->mu);
+  NvtxRange range("mact_host_stream");
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(c->device);

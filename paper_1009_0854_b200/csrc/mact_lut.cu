@@ -496,6 +496,7 @@ __global__ void __launch_bounds__(kLut33Threads, 1)
 template <int METHOD>
 static int launch_lut33_comp(const float* lat, const uint8_t* rgb, float* out, int64_t n, int planar,
                              cudaStream_t st) {
+  NvtxRange range("lut33_interp");
   constexpr size_t smem = kLut33Smem;
   const bool aligned = (uintptr_t)rgb % 16 == 0 && (uintptr_t)out % 16 == 0;
   const bool ok = !planar && aligned;

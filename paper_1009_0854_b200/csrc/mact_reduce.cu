@@ -223,6 +223,7 @@ extern "C" size_t mact_err_workspace_bytes(void) {
 extern "C" int mact_err_reduce(const MactErrSpec* spec, const MactCoeffs* c, const uint8_t* rgb,
                                int64_t cube_start, int64_t n, int64_t index_base,
                                MactErrStats* out, void* workspace, void* stream) {
+  NvtxRange range("mact_err_reduce");
   if (!spec || !out || !workspace) return set_error(MACT_EBADARG, "bad argument");
   if (spec->space < 0 || spec->space > 2) return set_error(MACT_EBADARG, "unknown space %d", spec->space);
   if (n <= 0) return set_error(MACT_EBADARG, "empty population");

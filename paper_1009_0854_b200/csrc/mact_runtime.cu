@@ -10,12 +10,17 @@
 #include <string>
 #include <tuple>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "mact_common.cuh"
 
 namespace mact {
 
 static thread_local std::string g_last_error;
 static std::atomic<uint64_t> g_launches{0};
+
+NvtxRange::NvtxRange(const char* name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
 
 void count_launch(int k) { g_launches.fetch_add((uint64_t)k, std::memory_order_relaxed); }
 

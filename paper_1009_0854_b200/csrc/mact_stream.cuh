@@ -206,6 +206,7 @@ template <class Op, int NW, int G, int SIN, int NOB>
 inline int launch_stream_t(const uint8_t* in, Outs outs, int64_t n, int planar,
                            const typename Op::Params& p, cudaStream_t st, const char* name) {
   if (n <= 0) return MACT_OK;
+  NvtxRange range(name);
   using L = WsLayout<Op, NW, G, SIN, NOB>;
   bool aligned = ((uintptr_t)in % 16) == 0;
   for (int k = 0; k < Op::NOUT; ++k)
