@@ -1,14 +1,18 @@
 """Benchmark of the B200 MACT path — one JSON line on rank 0.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c4|c1|c2|c3|c5] [--e2e-steps E] [--no-cpu-baseline]
+                    [--workload c4|c1|c2|c3|c5] [--lut-grid 9|17|33] [--lut-method M]
+                    [--e2e-steps E] [--no-cpu-baseline] [--graph | --no-graph]
 
 Default workload = BASELINE.json config 4 (the config the metric is quoted on
 "at 1/2/4/8 B200"): 64 images of 3840x2160 uint8 RGB, spatially correlated
 synthetic content, RGB->CIELAB via MACT (4,4), sharded by image across ranks
 (fixed 64-image batch -> strong scaling).  A step = one pass of the transform
 over the rank's images, inputs and outputs resident in HBM (1.59 GB in +
-6.37 GB out at N=1, far larger than the 126 MB L2, so no flush is needed).
+6.37 GB out at N=1, far larger than the 126 MB L2, so no flush is needed;
+smaller workloads rotate over enough buffer copies to exceed 2x L2).
+roofline.achieved counts the algorithmic bytes of the step's one launch:
+3 B in + 12 B out per pixel and transform (27 B fused C2, 39 B fused C5).
 
 Under torchrun (N>1) every rank processes its shard; time = max over ranks
 of the CUDA-event time between barriers.  --impl reference times the
@@ -32,7 +36,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
 HBM_FALLBACK = 6650.0          # GB/s, B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
-BYTES_PER_PX = 15              # 3 B uint8 in + 12 B fp32 out
 L2_POOL_BYTES = 512 << 20      # per-step footprint below this rotates over buffer copies
 
 WORKLOADS = {
