@@ -236,6 +236,12 @@ __global__ void k_fast_real(int space, const T* __restrict__ in, float* __restri
 // NOB output buffers per warp> (DESIGN.md §Kernels has the smem/occupancy math).
 // Overridable at build time for tuning (MACT_NVCC_DEFS, see build.py).
 // CIELAB: 16+1 warps, G=4, 2 stages: 176 KB smem (32 KB bank-replicated gamma) -> 1 CTA/SM (R01 sweep: 250 Gpix/s)
+#ifndef MACT_DIRECT_N
+#define MACT_DIRECT_N (1 << 21)
+#endif
+#ifndef MACT_DIRECT_N_LAB
+#define MACT_DIRECT_N_LAB (1 << 23)
+#endif
 #ifndef MACT_LAB_SMALL_N
 #define MACT_LAB_SMALL_N (1 << 21)
 #endif
@@ -336,18 +342,28 @@ static int fast_entry(int space, const void* rgb, int in_dtype, float* out, int6
   const int planar = layout == MACT_LAYOUT_PLANAR;
   Outs outs{{out, nullptr, nullptr}};
   const uint8_t* in = (const uint8_t*)rgb;
+  // small interleaved inputs (one image of up to a few Mpx): the direct kernel,
+  // whose latency is one DRAM round trip (C1: 60 -> 70 Gpix/s; Lab 1-4 Mpx:
+  // 1.1-1.4x).  Crossovers measured on B200: Lab 8 Mpx, HSI / SCT 2 Mpx.
+  const int64_t direct_n = space == MACT_SPACE_LAB ? (int64_t)MACT_DIRECT_N_LAB : (int64_t)MACT_DIRECT_N;
+  const bool direct = n < direct_n && !planar && n % 4 == 0 && (uintptr_t)in % 16 == 0 &&
+                      (uintptr_t)out % 16 == 0;
   switch (in_dtype) {
     case MACT_DTYPE_U8:
       if (space == MACT_SPACE_LAB) {
         // images below ~one tile per SM (C1: 512^2 = 32 tiles of 8192) take
         // 4x smaller tiles so the work spreads over 4x more SMs
+        if (direct)
+          return launch_direct<OpLab, 256>(in, outs, n, kc, st, "lab_fast");
         if (n < (int64_t)MACT_LAB_SMALL_N)
           return launch_stream_t<OpLab, MACT_LAB_SNW, 1, 2, 1>(in, outs, n, planar, kc, st, "lab_fast");
         return launch_stream_t<OpLab, MACT_LAB_CFG>(in, outs, n, planar, kc, st, "lab_fast");
       }
       if (space == MACT_SPACE_HSI)
-        return launch_stream_t<OpHsi, MACT_HSI_CFG>(in, outs, n, planar, kc, st, "hsi_fast");
-      return launch_stream_t<OpSct, MACT_SCT_CFG>(in, outs, n, planar, kc, st, "sct_fast");
+        return direct ? launch_direct<OpHsi, 256>(in, outs, n, kc, st, "hsi_fast")
+                      : launch_stream_t<OpHsi, MACT_HSI_CFG>(in, outs, n, planar, kc, st, "hsi_fast");
+      return direct ? launch_direct<OpSct, 256>(in, outs, n, kc, st, "sct_fast")
+                    : launch_stream_t<OpSct, MACT_SCT_CFG>(in, outs, n, planar, kc, st, "sct_fast");
     case MACT_DTYPE_F32:
       return launch_real<float>(space, (const float*)rgb, out, n, planar, kc, st);
     case MACT_DTYPE_F64:

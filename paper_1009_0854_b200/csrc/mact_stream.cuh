@@ -200,6 +200,50 @@ __global__ void __launch_bounds__(NT) k_generic(const uint8_t* __restrict__ in, 
   }
 }
 
+// Small inputs (one image of a few Mpx): no producer warp, no mbarriers, no
+// staging -- each thread loads its 4 pixels (3 words), runs Op::px4w and
+// stores 3 float4, so the latency of a launch is one DRAM round trip plus
+// the arithmetic.  Interleaved output, 16-byte aligned buffers, n % 4 == 0.
+template <class Op, int NT>
+__global__ void __launch_bounds__(NT) k_direct(const uint8_t* __restrict__ in, Outs outs, int64_t ngroups,
+                                               const __grid_constant__ typename Op::Params p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  auto* sh = reinterpret_cast<typename Op::Shared*>(smem);
+  Op::init(sh, p);
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(in);
+  for (int64_t gi = blockIdx.x * (int64_t)NT + threadIdx.x; gi < ngroups; gi += (int64_t)gridDim.x * NT) {
+    float o[4][Op::NOUT][3];
+    Op::px4w(__ldg(w + 3 * gi), __ldg(w + 3 * gi + 1), __ldg(w + 3 * gi + 2), sh, lane, p, o);
+#pragma unroll
+    for (int k = 0; k < Op::NOUT; ++k) {
+      if (outs.o[k] == nullptr) continue;
+      float4* d = reinterpret_cast<float4*>(outs.o[k] + 12 * gi);
+      d[0] = make_float4(o[0][k][0], o[0][k][1], o[0][k][2], o[1][k][0]);
+      d[1] = make_float4(o[1][k][1], o[1][k][2], o[2][k][0], o[2][k][1]);
+      d[2] = make_float4(o[2][k][2], o[3][k][0], o[3][k][1], o[3][k][2]);
+    }
+  }
+}
+
+template <class Op, int NT>
+inline int launch_direct(const uint8_t* in, Outs outs, int64_t n, const typename Op::Params& p,
+                         cudaStream_t st, const char* name) {
+  NvtxRange range(name);
+  auto kfn = k_direct<Op, NT>;
+  const size_t sb = sizeof(typename Op::Shared);
+  const int64_t cap = persistent_grid((const void*)kfn, NT, sb);
+  if (cap <= 0) return MACT_ECUDA;
+  const int64_t ngroups = n / 4;
+  int64_t grid = (ngroups + NT - 1) / NT;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  kfn<<<(unsigned)grid, NT, sb, st>>>(in, outs, ngroups, p);
+  count_launch();
+  return check_launch(name);
+}
+
 // Host launcher: whole tiles on k_ws, the remainder (or everything, when a
 // buffer is not 16-byte aligned) on k_generic.
 template <class Op, int NW, int G, int SIN, int NOB>
