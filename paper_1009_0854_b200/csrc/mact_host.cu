@@ -158,7 +158,16 @@ static int stream_host(MactHostCtx* c, const uint8_t* host_rgb, float* host_out,
   const bool direct = is_pinned(host_rgb) && is_pinned(host_out);
   int rc = MACT_OK;
   if (!direct) rc = ensure_bounce(c);
-  const int64_t nchunks = (n + c->chunk - 1) / c->chunk;
+  // Small inputs are cut into at least 2 x nstreams chunks (>= 64 Ki px, multiple
+  // of 2048) so their H2D, kernel and D2H still overlap; large ones use the
+  // context's chunk size.
+  int64_t chunk = c->chunk;
+  if (n < c->chunk * 2 * c->nstreams) {
+    chunk = (n + 2 * c->nstreams - 1) / (2 * c->nstreams);
+    chunk = std::max<int64_t>(65536, (chunk + 2047) / 2048 * 2048);
+    chunk = std::min<int64_t>(chunk, c->chunk);
+  }
+  const int64_t nchunks = (n + chunk - 1) / chunk;
   // slot bookkeeping for pageable callers: chunk that last used each slot
   std::vector<int64_t> pending(c->nstreams, -1);
   auto drain = [&](int s) -> int {
@@ -166,7 +175,7 @@ static int stream_host(MactHostCtx* c, const uint8_t* host_rgb, float* host_out,
     if (k < 0) return MACT_OK;
     cudaError_t e = cudaEventSynchronize(c->done[s]);
     if (e != cudaSuccess) return set_error(MACT_ECUDA, "d2h: %s", cudaGetErrorString(e));
-    const int64_t off = k * c->chunk, m = std::min<int64_t>(c->chunk, n - off);
+    const int64_t off = k * chunk, m = std::min<int64_t>(chunk, n - off);
     if (layout == MACT_LAYOUT_INTERLEAVED) {
       par_memcpy(host_out + 3 * off, c->h_out[s], (size_t)m * 12);
     } else {
@@ -178,7 +187,7 @@ static int stream_host(MactHostCtx* c, const uint8_t* host_rgb, float* host_out,
   for (int64_t k = 0; k < nchunks && rc == MACT_OK; ++k) {
     const int s = (int)(k % c->nstreams);
     cudaStream_t st = c->streams[s];
-    const int64_t off = k * c->chunk, m = std::min<int64_t>(c->chunk, n - off);
+    const int64_t off = k * chunk, m = std::min<int64_t>(chunk, n - off);
     cudaError_t e;
     if (direct) {
       e = cudaMemcpyAsync(c->d_in[s], host_rgb + 3 * off, (size_t)m * 3, cudaMemcpyHostToDevice, st);
