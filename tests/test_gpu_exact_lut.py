@@ -190,3 +190,36 @@ def test_lut33_planar_equals_interleaved(n, method):
     inter = lut.interpolate(L, px, method).cpu().numpy()
     planar = lut.interpolate(L, px, method, layout="planar").cpu().numpy()
     np.testing.assert_array_equal(planar.T, inter)
+
+
+@pytest.mark.parametrize("grid", [9, 17, 33])
+def test_lut_unaligned_views_and_step_edges(grid):
+    """Unaligned buffers take the generic kernel, step-multiple edges the tails:
+    every path agrees bit for bit with the aligned interleaved result."""
+    from paper_1009_0854_b200 import lut
+    L = lut.build_lut("lab", grid)
+    px = torch.from_numpy(np.random.default_rng(grid).integers(0, 256, (4096 * 8 + 7, 3), dtype=np.uint8)).cuda()
+    full = lut.interpolate(L, px, "tetrahedral").cpu().numpy()
+    sub = lut.interpolate(L, px[1:], "tetrahedral").cpu().numpy()          # 3-byte offset input
+    np.testing.assert_array_equal(sub, full[1:])
+    for n in (4096 * 8 - 1, 4096 * 8 + 1, 4096 * 3, 4095):
+        np.testing.assert_array_equal(lut.interpolate(L, px[:n], "tetrahedral").cpu().numpy(), full[:n])
+    out = torch.empty((px.shape[0] + 1, 3), dtype=torch.float32, device="cuda")[1:]   # 12-byte offset output
+    lut.interpolate(L, px, "tetrahedral", out=out)
+    np.testing.assert_array_equal(out.cpu().numpy(), full)
+
+
+@pytest.mark.parametrize("grid", [17, 33])
+def test_lut_beyond_int32_pixel_count(grid):
+    """One interpolation over 2^31 + 4099 pixels (64-bit step and tile indexing)."""
+    from paper_1009_0854_b200 import harness, lut
+    L = lut.build_lut("lab", grid)
+    n = (1 << 31) + 4099
+    cube = harness.cube_chunk(0, 1 << 24, device="cuda")
+    ref = lut.interpolate(L, cube, "tetrahedral")
+    x = cube.repeat((n >> 24) + 1, 1)[:n]
+    out = lut.interpolate(L, x, "tetrahedral")
+    idx = torch.from_numpy(np.r_[0:64, (1 << 31) - 64:(1 << 31) + 64, n - 4099 - 64:n]).cuda()
+    np.testing.assert_array_equal(out[idx].cpu().numpy(), ref[idx % (1 << 24)].cpu().numpy())
+    del out, x
+    torch.cuda.empty_cache()
