@@ -201,9 +201,10 @@ def run_ours(args, wl):
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize(dev)
-    # Small workloads are launch-latency bound (C1: 262 K px = ~1 us of HBM time):
-    # the K steps are captured once into a CUDA graph and replayed in the timed region.
-    use_graph = args.graph or (args.graph is None and n_local < (1 << 22))
+    # Short steps are launch-latency bound (C1: 262 K px = ~1 us of HBM time; C2/C3:
+    # ~0.1 ms steps lose ~9 us each to launch gaps): below 128 Mpx per rank the K steps are
+    # captured once into a CUDA graph and replayed in the timed region (also C4 at N >= 4).
+    use_graph = args.graph or (args.graph is None and n_local < (1 << 27))
     graph = None
     if use_graph:
         graph = torch.cuda.CUDAGraph()
@@ -418,7 +419,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=None,
-                    help="capture the K steps in a CUDA graph (default: only for workloads < 4 Mpx)")
+                    help="capture the K steps in a CUDA graph (default: only below 128 Mpx per rank)")
     args = ap.parse_args()
     wl = dict(WORKLOADS[args.workload])
     wl["desc"] = wl["desc"].format(grid=args.lut_grid, method=args.lut_method)
