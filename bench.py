@@ -201,10 +201,11 @@ def run_ours(args, wl):
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize(dev)
-    # Short steps are launch-latency bound (C1: 262 K px = ~1 us of HBM time; C2/C3:
-    # ~0.1 ms steps lose ~9 us each to launch gaps): below 128 Mpx per rank the K steps are
-    # captured once into a CUDA graph and replayed in the timed region (also C4 at N >= 4).
-    use_graph = args.graph or (args.graph is None and n_local < (1 << 27))
+    # The K steps are captured once into a CUDA graph and replayed in the timed
+    # region: short steps are launch-latency bound (C1: 262 K px = ~1 us of HBM
+    # time; the ~0.1 ms C2/C3 steps lose ~9 us each to launch gaps), and even C4's
+    # 1.8 ms steps gain 0.6 %.  --no-graph times stream launches with per-step events.
+    use_graph = args.graph is not False
     graph = None
     if use_graph:
         graph = torch.cuda.CUDAGraph()
@@ -419,7 +420,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=None,
-                    help="capture the K steps in a CUDA graph (default: only below 128 Mpx per rank)")
+                    help="capture the K steps in a CUDA graph (default: on)")
     args = ap.parse_args()
     wl = dict(WORKLOADS[args.workload])
     wl["desc"] = wl["desc"].format(grid=args.lut_grid, method=args.lut_method)
