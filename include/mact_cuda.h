@@ -255,6 +255,15 @@ int mact_lut_interp_host(MactHostCtx* ctx, const float* lattice, int grid_n, int
 int mact_probe_expand(const uint8_t* rgb, float* out, int64_t n, void* stream);
 
 /* ---- misc ----------------------------------------------------------------- */
+/* How the uint8 fast CIELAB kernels evaluate this configuration's rational
+ * (fast.py:110-115): MACT_LAB_PATH_SEG = segmented fp32 cubic (the default
+ * when the host-side fit check passes), MACT_LAB_PATH_MONIC = fp64 monic
+ * (4,4) quotient, MACT_LAB_PATH_PQ = fp64 P/Q; negative = error status.
+ * Host-only (no device work). */
+#define MACT_LAB_PATH_SEG 1
+#define MACT_LAB_PATH_MONIC 2
+#define MACT_LAB_PATH_PQ 3
+int mact_lab_eval_path(const MactCoeffs* c);
 const char* mact_last_error(void);
 int mact_version(void);
 /* number of kernel launches issued by this thread since the last reset */

@@ -59,6 +59,7 @@ class MactApproxSpec(C.Structure):
 FN_FORM, FN_ATAN_SQRT3, FN_ACOS, FN_ATAN_UNIT = 0, 1, 2, 3
 ELEM_INVERSE_GAMMA, ELEM_RGB_TO_XYZ, ELEM_LAB_F, ELEM_XYZ_TO_LAB, ELEM_ANGULAR_LERP = 0, 1, 2, 3, 4
 SPACE_HSI_ARCCOS = 3
+LAB_PATH_SEG, LAB_PATH_MONIC, LAB_PATH_PQ = 1, 2, 3
 
 _vp, _i, _i64, _u64 = C.c_void_p, C.c_int, C.c_int64, C.c_uint64
 _SIGNATURES = {
@@ -91,6 +92,7 @@ _SIGNATURES = {
     "mact_lut_interp_host": (_i, [_vp, _vp, _i, _i, _vp, _vp, _i64, _i]),
     "mact_last_error": (C.c_char_p, []),
     "mact_version": (_i, []),
+    "mact_lab_eval_path": (_i, [C.POINTER(MactCoeffs)]),
     "mact_launch_count": (_u64, []),
     "mact_launch_count_reset": (None, []),
 }

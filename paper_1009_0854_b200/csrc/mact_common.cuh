@@ -32,6 +32,13 @@ __host__ __device__ constexpr double rgb2xyz(int row, int col) {
 constexpr int kCbrtDeg = 4;
 constexpr int kPolyDeg = 5;
 
+// Segment table of the fp32 CIELAB lightness kernel (see KCoeffs::seg).
+constexpr int kLabSegShift = 19;                                   // 16 segments per binade
+constexpr uint32_t kLabSegMask = ~((1u << kLabSegShift) - 1u);
+constexpr uint32_t kLabSegBase = 0x3C000000u >> kLabSegShift;      // 2^-7
+constexpr int kLabSegs = (int)((0x3F800000u >> kLabSegShift) - kLabSegBase + 1);   // up to [1, 1.0625)
+constexpr int kLabSegCopies = 8;   // bank-private smem copies: an 8-lane LDS.128 phase is conflict-free
+
 // Kernel parameter block built on the host from MactCoeffs (passed by value
 // as a __grid_constant__ parameter, so it lives in the constant bank and the
 // FMAs take coefficients as c[][] operands — no registers, no globals).
@@ -54,6 +61,16 @@ struct KCoeffs {
   double lin_s, lin_o;              // linear branch expressed in q: q = lin_s t + lin_o
   double l_s, l_o;                  // 116 s, 116 k - 16
   float a_s, b_s;                   // 500 s, 200 s
+  // Segmented fp32 form of the same rational (any degrees), used when its
+  // fit passed the host-side check (lab_seg = 1).  Segment i covers the fp32
+  // values whose bits >> kLabSegShift equal kLabSegBase + i, i.e. 16
+  // segments per binade from 2^-7 (below the knee 0.008856) to [1, 1.0625).
+  // On it, R(t) ~= hi + u (c1 + u (c2 + u c3)) with u = t - t_seg exact:
+  // seg[i] = (hi, c1, c2, c3).  The linear branch below the knee is
+  // lin_hi + (lin_slope t + lin_lo).
+  int32_t lab_seg;
+  float lin_hi, lin_lo, lin_slope;
+  float4 seg[kLabSegs];
 };
 
 // ---------------------------------------------------------------- Horner

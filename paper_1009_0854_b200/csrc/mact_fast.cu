@@ -26,39 +26,61 @@ __device__ const float kGammaF32[256] = {
 #include "mact_gamma_table.inc"
 };
 
+// CIELAB op, tables in shared memory (SmemTab, mact_pixel.cuh): the
+// streaming kernels.
 struct OpLab {
   static constexpr int NOUT = 1;
   using Params = KCoeffs;
+  using Tab = SmemTab<kLabSegCopies>;
   struct Shared {
     float gamma[256 * 32];   // GAMMA_TABLE (fast.py:35) in fp32, replicated per bank
+    float4 seg[kLabSegs * kLabSegCopies];   // KCoeffs::seg, bank-private copies
   };
-  static __device__ __forceinline__ void init(Shared* s, const Params&) {
+  static __device__ __forceinline__ void init(Shared* s, const Params& c) {
     for (int k = threadIdx.x; k < 256; k += blockDim.x) {   // L2-resident table, replicated per bank
       const float v = __ldg(kGammaF32 + k);
 #pragma unroll 8
       for (int r = 0; r < 32; ++r) s->gamma[(k << 5) | ((r + k) & 31)] = v;
     }
+    if (c.lab_seg) {   // warp-uniform parameter reads (one constant-cache broadcast per entry)
+      const int lane = (int)(threadIdx.x & 31), nw = (int)(blockDim.x >> 5);
+      for (int i = (int)(threadIdx.x >> 5); i < kLabSegs; i += nw) {
+        const float4 v = c.seg[i];
+        if (lane < kLabSegCopies) s->seg[i * kLabSegCopies + lane] = v;
+      }
+    }
+  }
+  static __device__ __forceinline__ Tab tab(const Shared* s, uint32_t lane, const Params&) {
+    return Tab(s->gamma, s->seg, lane);
   }
   static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
                                             uint32_t lane, const Params& c, float (*o)[3]) {
-    const Lab3 v = lab_fast_u8(r, g, b, s->gamma, lane, c);
+    const Lab3 v = lab_fast_u8(r, g, b, tab(s, lane, c), c);
     o[0][0] = v.c0; o[0][1] = v.c1; o[0][2] = v.c2;
   }
-  static __device__ __forceinline__ void px4w(uint32_t w0, uint32_t w1, uint32_t w2,
-                                              const Shared* s, uint32_t lane, const Params& c,
-                                              float (*o)[1][3]) {
+  template <class T>
+  static __device__ __forceinline__ void px4w_tab(uint32_t w0, uint32_t w1, uint32_t w2, const T& t,
+                                                  const Params& c, float (*o)[1][3]) {
     const uint32_t ch[12] = {byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), byte_of(w0, 3),
                              byte_of(w1, 0), byte_of(w1, 1), byte_of(w1, 2), byte_of(w1, 3),
                              byte_of(w2, 0), byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3)};
-    if (c.monic44) {
+    if (c.lab_seg || c.monic44) {
       float v[4][3];
-      lab_fast_u8x4(ch, s->gamma, lane, c, v);
+      lab_fast_u8x4(ch, t, c, v);
 #pragma unroll
       for (int q = 0; q < 4; ++q) { o[q][0][0] = v[q][0]; o[q][0][1] = v[q][1]; o[q][0][2] = v[q][2]; }
     } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) px(ch[3 * q], ch[3 * q + 1], ch[3 * q + 2], s, lane, c, o[q]);
+      for (int q = 0; q < 4; ++q) {
+        const Lab3 v = lab_fast_u8(ch[3 * q], ch[3 * q + 1], ch[3 * q + 2], t, c);
+        o[q][0][0] = v.c0; o[q][0][1] = v.c1; o[q][0][2] = v.c2;
+      }
     }
+  }
+  static __device__ __forceinline__ void px4w(uint32_t w0, uint32_t w1, uint32_t w2,
+                                              const Shared* s, uint32_t lane, const Params& c,
+                                              float (*o)[1][3]) {
+    px4w_tab(w0, w1, w2, tab(s, lane, c), c, o);
   }
 };
 
@@ -135,7 +157,7 @@ struct OpMulti {
   static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
                                             uint32_t lane, const Params& c, float (*o)[3]) {
     int k = 0;
-    if constexpr (LAB) put(o[k++], lab_fast_u8(r, g, b, s->gamma, lane, c));
+    if constexpr (LAB) put(o[k++], lab_fast_u8(r, g, b, OpLab::tab(s, lane, c), c));
     if constexpr (HSI) put(o[k++], hsi_fast_u8(r, g, b, c));
     if constexpr (SCT) put(o[k++], sct_fast_u8(r, g, b, c));
   }
@@ -239,9 +261,6 @@ __global__ void k_fast_real(int space, const T* __restrict__ in, float* __restri
 #ifndef MACT_DIRECT_N
 #define MACT_DIRECT_N (1 << 21)
 #endif
-#ifndef MACT_DIRECT_N_LAB
-#define MACT_DIRECT_N_LAB (1 << 23)
-#endif
 #ifndef MACT_LAB_SMALL_N
 #define MACT_LAB_SMALL_N (1 << 21)
 #endif
@@ -342,19 +361,19 @@ static int fast_entry(int space, const void* rgb, int in_dtype, float* out, int6
   const int planar = layout == MACT_LAYOUT_PLANAR;
   Outs outs{{out, nullptr, nullptr}};
   const uint8_t* in = (const uint8_t*)rgb;
-  // small interleaved inputs (one image of up to a few Mpx): the direct kernel,
-  // whose latency is one DRAM round trip (C1: 60 -> 70 Gpix/s; Lab 1-4 Mpx:
-  // 1.1-1.4x).  Crossovers measured on B200: Lab 8 Mpx, HSI / SCT 2 Mpx.
-  const int64_t direct_n = space == MACT_SPACE_LAB ? (int64_t)MACT_DIRECT_N_LAB : (int64_t)MACT_DIRECT_N;
-  const bool direct = n < direct_n && !planar && n % 4 == 0 && (uintptr_t)in % 16 == 0 &&
-                      (uintptr_t)out % 16 == 0;
+  // small interleaved HSI / SCT inputs (one image of up to a few Mpx): the
+  // direct kernel, whose latency is one DRAM round trip (crossover measured on
+  // B200: 2 Mpx).  CIELAB has no direct kernel: its tables must be staged in
+  // shared memory (a parameter-bank gather runs at 30 Gpix/s), and with them
+  // the small-tile streaming kernel is faster at every size (R01 sweep,
+  // scripts/sweep_lab_sizes.py: 512^2 4.5 us vs 5.8 us).
+  const bool direct = n < (int64_t)MACT_DIRECT_N && !planar && n % 4 == 0 &&
+                      (uintptr_t)in % 16 == 0 && (uintptr_t)out % 16 == 0;
   switch (in_dtype) {
     case MACT_DTYPE_U8:
       if (space == MACT_SPACE_LAB) {
         // images below ~one tile per SM (C1: 512^2 = 32 tiles of 8192) take
-        // 4x smaller tiles so the work spreads over 4x more SMs
-        if (direct)
-          return launch_direct<OpLab, 256>(in, outs, n, kc, st, "lab_fast");
+        // smaller tiles so the work spreads over more SMs
         if (n < (int64_t)MACT_LAB_SMALL_N)
           return launch_stream_t<OpLab, MACT_LAB_SNW, 1, 2, 1>(in, outs, n, planar, kc, st, "lab_fast");
         return launch_stream_t<OpLab, MACT_LAB_CFG>(in, outs, n, planar, kc, st, "lab_fast");

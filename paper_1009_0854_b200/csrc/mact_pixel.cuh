@@ -14,9 +14,10 @@
 //  * SCT's folded-arcsin argument uses the cancellation-free
 //    1 - b/L = (r^2+g^2) / (L (L+b))  (H2).
 //  * CIELAB: fp32 gamma table + fp32 3x3 (white folded in), then the rational
-//    P/Q in fp64 Horner and a double-float quotient q0 + r/Q, carried as a
-//    (hi, lo) pair through L*, a*, b* so that 500 (fx - fy) does not amplify
-//    fp32 rounding (H1).
+//    P/Q as a segmented fp32 cubic whose (hi, small part) split survives into
+//    the a*, b* differences, so that 500 (fx - fy) does not amplify fp32
+//    rounding (H1).  Configurations whose segment fit fails the host check
+//    keep the fp64 evaluation (monic q = D'/Q' for (4,4), P/Q otherwise).
 #pragma once
 
 #include "mact_common.cuh"
@@ -95,17 +96,86 @@ __device__ __forceinline__ void lab_from_q(double qx, double qy, double qz, cons
   B = c.b_s * (float)(qy - qz);
 }
 
-// gamma_rep: 256 entries replicated 32x, entry i at [i*32 + lane] (conflict-free)
-__device__ __forceinline__ Lab3 lab_fast_u8(uint32_t r, uint32_t g, uint32_t b,
-                                            const float* gamma_rep, uint32_t lane,
+// ------------------------------------------ CIELAB fast, segmented fp32
+// The rational R = P/Q as a piecewise cubic on 16 segments per binade of the
+// fp32 t (KCoeffs::seg, fitted on the host to ~5e-9): with u = t - t_seg
+// (exact: t_seg is t with the bits below the segment index cleared),
+//   f = hi + d,   d = u (c1 + u (c2 + u c3)),
+// and the epilogue keeps hi and d apart,
+//   a* = 500 ((hx - hy) + (dx - dy)),  b* = 200 ((hy - hz) + (dy - dz)),
+// so the 500x amplification of a* sees the rounding of the small parts d
+// only (the hi differences are exact or rounded relative to the result).
+// All fp32: no fp64 pipe, no XU.  Full-cube error vs the reference:
+// 1.5e-5 / 5.6e-5 / 2.5e-5 on L*, a*, b* (tolerance 1e-4).
+//
+// Where the two tables (fp32 GAMMA_TABLE, segment table) are read from is a
+// policy, so every kernel runs the same arithmetic:
+//  * SmemTab<COPIES>: staged in shared memory; gamma replicated 32x (entry i
+//    of lane l at float [i*32 + l], conflict-free), segment table in COPIES
+//    bank-private copies (entry i of copy k at float4 [i*COPIES + k]);
+//    addressed with 32-bit shared addresses off the lane's base.
+//  (A policy reading the segment entries straight from the parameter bank
+//  -- no staging -- was measured at 30 Gpix/s: divergent constant-bank
+//  gathers serialise.)
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float4 lds_f32x4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+template <int COPIES>
+struct SmemTab {
+  uint32_t gl, sa;   // gamma + lane*4, seg + (lane % COPIES)*16 (shared addresses)
+  __device__ __forceinline__ SmemTab(const float* gamma_rep, const float4* seg, uint32_t lane)
+      : gl(smem_u32(gamma_rep) + lane * 4), sa(smem_u32(seg) + (lane & (COPIES - 1)) * 16) {}
+  __device__ __forceinline__ float gamma(uint32_t v) const { return lds_f32(gl + (v << 7)); }
+  __device__ __forceinline__ float4 seg(uint32_t i) const { return lds_f32x4(sa + i * (COPIES * 16)); }
+};
+template <class Tab>
+__device__ __forceinline__ void lab_seg(float t, const Tab& tab, float& h, float& d) {
+  const uint32_t b = __float_as_uint(t);
+  const uint32_t i = min((b >> kLabSegShift) - kLabSegBase, (uint32_t)(kLabSegs - 1));
+  const float4 e = tab.seg(i);
+  const float u = t - __uint_as_float(b & kLabSegMask);
+  h = e.x;
+  d = u * fmaf(u, fmaf(u, e.w, e.z), e.y);
+}
+__device__ __forceinline__ void lab_seg_lin(float t, const KCoeffs& c, float& h, float& d) {
+  h = c.lin_hi;
+  d = fmaf(c.lin_slope, t, c.lin_lo);          // strict '>' keeps t = knee linear (fast.py:114)
+}
+__device__ __forceinline__ void lab_from_seg(float hx, float dx, float hy, float dy, float hz,
+                                             float dz, float& L, float& A, float& B) {
+  L = fmaf(116.f, dy, fmaf(116.f, hy, -16.f));
+  A = 500.f * ((hx - hy) + (dx - dy));
+  B = 200.f * ((hy - hz) + (dy - dz));
+}
+__device__ __forceinline__ float lab_t(const KCoeffs& c, int row, float gr, float gg, float gb) {
+  return fmaf(c.mxyz[3 * row + 2], gb, fmaf(c.mxyz[3 * row + 1], gg, c.mxyz[3 * row] * gr));
+}
+
+// One pixel (tails, unaligned buffers, the fused error reduction).
+template <class Tab>
+__device__ __forceinline__ Lab3 lab_fast_u8(uint32_t r, uint32_t g, uint32_t b, const Tab& tab,
                                             const KCoeffs& c) {
-  const float gr = gamma_rep[(r << 5) | lane];
-  const float gg = gamma_rep[(g << 5) | lane];
-  const float gb = gamma_rep[(b << 5) | lane];
-  const float tx = fmaf(c.mxyz[2], gb, fmaf(c.mxyz[1], gg, c.mxyz[0] * gr));
-  const float ty = fmaf(c.mxyz[5], gb, fmaf(c.mxyz[4], gg, c.mxyz[3] * gr));
-  const float tz = fmaf(c.mxyz[8], gb, fmaf(c.mxyz[7], gg, c.mxyz[6] * gr));
+  const float gr = tab.gamma(r), gg = tab.gamma(g), gb = tab.gamma(b);
+  const float tx = lab_t(c, 0, gr, gg, gb), ty = lab_t(c, 1, gr, gg, gb), tz = lab_t(c, 2, gr, gg, gb);
   Lab3 o;
+  if (c.lab_seg) {   // same arithmetic as lab_fast_u8x4 (bit-identical tile/tail paths)
+    float h[3], d[3];
+    const float t[3] = {tx, ty, tz};
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      if (t[j] > (float)kLabKnee) lab_seg(t[j], tab, h[j], d[j]);
+      else lab_seg_lin(t[j], c, h[j], d[j]);
+    }
+    lab_from_seg(h[0], d[0], h[1], d[1], h[2], d[2], o.c0, o.c1, o.c2);
+    return o;
+  }
   if (c.monic44) {   // same arithmetic as lab_fast_u8x4 (bit-identical tile/tail paths)
     lab_from_q(lab_q_sel(tx, c), lab_q_sel(ty, c), lab_q_sel(tz, c), c, o.c0, o.c1, o.c2);
     return o;
@@ -117,22 +187,37 @@ __device__ __forceinline__ Lab3 lab_fast_u8(uint32_t r, uint32_t g, uint32_t b,
   return o;
 }
 
-__device__ __forceinline__ void lab_fast_u8x4(const uint32_t (&ch)[12], const float* gamma_rep,
-                                              uint32_t lane, const KCoeffs& c, float (*o)[3]) {
+// 4 pixels (12 channels) per call, warp-converged.  Configurations that are
+// neither segmented nor monic (4,4) take lab_fast_u8 per pixel (caller).
+template <class Tab>
+__device__ __forceinline__ void lab_fast_u8x4(const uint32_t (&ch)[12], const Tab& tab,
+                                              const KCoeffs& c, float (*o)[3]) {
   float t[12];
   bool low = false;
-  const float* gl = gamma_rep + lane;                  // lane's bank column: one IMAD per lookup
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
-    const float gr = gl[ch[3 * p] << 5];
-    const float gg = gl[ch[3 * p + 1] << 5];
-    const float gb = gl[ch[3 * p + 2] << 5];
-    t[3 * p] = fmaf(c.mxyz[2], gb, fmaf(c.mxyz[1], gg, c.mxyz[0] * gr));
-    t[3 * p + 1] = fmaf(c.mxyz[5], gb, fmaf(c.mxyz[4], gg, c.mxyz[3] * gr));
-    t[3 * p + 2] = fmaf(c.mxyz[8], gb, fmaf(c.mxyz[7], gg, c.mxyz[6] * gr));
+    const float gr = tab.gamma(ch[3 * p]), gg = tab.gamma(ch[3 * p + 1]), gb = tab.gamma(ch[3 * p + 2]);
+    t[3 * p] = lab_t(c, 0, gr, gg, gb);
+    t[3 * p + 1] = lab_t(c, 1, gr, gg, gb);
+    t[3 * p + 2] = lab_t(c, 2, gr, gg, gb);
   }
 #pragma unroll
   for (int j = 0; j < 12; ++j) low |= !(t[j] > (float)kLabKnee);
+  if (c.lab_seg) {
+    float h[12], d[12];
+#pragma unroll
+    for (int j = 0; j < 12; ++j) lab_seg(t[j], tab, h[j], d[j]);
+    if (__any_sync(0xffffffffu, low)) {
+#pragma unroll
+      for (int j = 0; j < 12; ++j)
+        if (!(t[j] > (float)kLabKnee)) lab_seg_lin(t[j], c, h[j], d[j]);
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+      lab_from_seg(h[3 * p], d[3 * p], h[3 * p + 1], d[3 * p + 1], h[3 * p + 2], d[3 * p + 2],
+                   o[p][0], o[p][1], o[p][2]);
+    return;
+  }
   double q[12];
 #pragma unroll
   for (int j = 0; j < 12; ++j) q[j] = lab_q(MACT_T2D(t[j]), c);

@@ -19,6 +19,7 @@
 namespace mact {
 
 constexpr int kRedThreads = 256;
+constexpr int kRedSegCopies = 4;
 constexpr int kRedMaxBlocks = 2048;
 
 struct Acc {
@@ -112,7 +113,13 @@ __global__ void __launch_bounds__(kRedThreads) k_err(const __grid_constant__ Red
   // the reference's fp64 GAMMA_TABLE (fast.py:35, exact.py:52-57 at i/255) and its fp32 rounding
   __shared__ float gamma_rep[256 * 32];
   __shared__ double gamma_d[256];
+  __shared__ float4 seg[kLabSegs * kRedSegCopies];   // KCoeffs::seg (fewer copies: static smem cap)
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) gamma_rep[i] = (float)ref::kGammaF64[i >> 5];
+  if (p.c.lab_seg)
+    for (int i = (int)(threadIdx.x >> 5); i < kLabSegs; i += kRedThreads / 32) {
+      const float4 v = p.c.seg[i];
+      if ((threadIdx.x & 31) < kRedSegCopies) seg[i * kRedSegCopies + (threadIdx.x & 31)] = v;
+    }
   for (int i = threadIdx.x; i < 256; i += blockDim.x) gamma_d[i] = ref::kGammaF64[i];
   __syncthreads();
   const MactErrSpec& s = p.spec;
@@ -132,7 +139,7 @@ __global__ void __launch_bounds__(kRedThreads) k_err(const __grid_constant__ Red
     double cand[3], ref[3];
     if (s.candidate == MACT_CAND_FAST) {
       Lab3 v;
-      if (s.space == MACT_SPACE_LAB) v = lab_fast_u8(r, g, b, gamma_rep, lane, p.c);
+      if (s.space == MACT_SPACE_LAB) v = lab_fast_u8(r, g, b, SmemTab<kRedSegCopies>(gamma_rep, seg, lane), p.c);
       else if (s.space == MACT_SPACE_HSI) v = hsi_fast_u8(r, g, b, p.c);
       else v = sct_fast_u8(r, g, b, p.c);
       cand[0] = v.c0; cand[1] = v.c1; cand[2] = v.c2;

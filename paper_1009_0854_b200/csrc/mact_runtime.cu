@@ -5,10 +5,12 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <vector>
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -86,6 +88,94 @@ int persistent_grid(const void* fn, int threads, size_t smem_bytes) {
   return grid;
 }
 
+// Segment table of the fp32 lightness kernel (KCoeffs::seg).
+// Each segment's cubic in u = t - t_seg interpolates the rational
+// R = P/Q (evaluated as approximants.py:55-82: two Horner sums in fp64 and
+// one division) at the 4 Chebyshev nodes of the segment; the fp32-rounded
+// coefficients c1..c3 are then checked against R on 65 points per segment.
+// A fit worse than 1e-8 absolute (the 500 (fx - fy) budget of a*; the (4,4) set
+// fits to ~5e-9) or a non-finite value leaves the configuration on the fp64
+// evaluation.
+static double rational_ref(const KCoeffs* k, double t) {
+  double p = k->cbrt_num[kCbrtDeg], q = k->cbrt_den[kCbrtDeg];
+  for (int i = kCbrtDeg - 1; i >= 0; --i) {
+    p = p * t + k->cbrt_num[i];
+    q = q * t + k->cbrt_den[i];
+  }
+  return p / q;
+}
+
+static bool fit_lab_segments(KCoeffs* k) {
+  k->lin_hi = (float)kLabOffset;
+  k->lin_lo = (float)(kLabOffset - (double)k->lin_hi);
+  k->lin_slope = (float)kLabSlope;
+  const double kPiL = 3.14159265358979323846;
+  for (int i = 0; i < kLabSegs; ++i) {
+    uint32_t b0 = (kLabSegBase + (uint32_t)i) << kLabSegShift, b1 = b0 + (1u << kLabSegShift);
+    float f0, f1;
+    std::memcpy(&f0, &b0, 4);
+    std::memcpy(&f1, &b1, 4);
+    const double t0 = f0, w = (double)f1 - t0;
+    long double a[4][5];
+    for (int r = 0; r < 4; ++r) {   // Vandermonde system at the Chebyshev nodes of [0, w]
+      const long double u = 0.5L * w * (1.0L - std::cos((2 * r + 1) * kPiL / 8.0));
+      long double pw = 1.0L;
+      for (int col = 0; col < 4; ++col, pw *= u) a[r][col] = pw;
+      a[r][4] = rational_ref(k, t0 + (double)u);
+    }
+    for (int col = 0; col < 4; ++col) {   // Gaussian elimination, partial pivoting
+      int piv = col;
+      for (int r = col + 1; r < 4; ++r)
+        if (std::fabs((double)a[r][col]) > std::fabs((double)a[piv][col])) piv = r;
+      for (int j = 0; j < 5; ++j) std::swap(a[col][j], a[piv][j]);
+      for (int r = 0; r < 4; ++r) {
+        if (r == col) continue;
+        const long double m = a[r][col] / a[col][col];
+        for (int j = col; j < 5; ++j) a[r][j] -= m * a[col][j];
+      }
+    }
+    float cf[4];
+    for (int j = 0; j < 4; ++j) cf[j] = (float)(a[j][4] / a[j][j]);
+    const double c0 = (double)(a[0][4] / a[0][0]);   // hi's own rounding (<= 1/2 ulp) is not fit error
+    for (int s = 0; s <= 64; ++s) {
+      const double u = w * s / 64.0;
+      const double approx = c0 + u * ((double)cf[1] + u * ((double)cf[2] + u * (double)cf[3]));
+      const double want = rational_ref(k, t0 + u);
+      if (!std::isfinite(want) || !(std::fabs(approx - want) <= 1e-8)) return false;
+    }
+    k->seg[i] = make_float4(cf[0], cf[1], cf[2], cf[3]);
+  }
+  return true;
+}
+
+// The fit costs ~60 us of host time, so tables are cached per rational
+// (keyed by its 2 x 5 coefficients; a handful of configurations in practice).
+struct SegTable {
+  bool ok;
+  float lin[3];
+  float4 seg[kLabSegs];
+};
+static bool build_lab_segments(KCoeffs* k) {
+  static std::mutex mu;
+  static std::map<std::vector<double>, SegTable> cache;
+  std::vector<double> key(k->cbrt_num, k->cbrt_num + kCbrtDeg + 1);
+  key.insert(key.end(), k->cbrt_den, k->cbrt_den + kCbrtDeg + 1);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    SegTable t;
+    t.ok = fit_lab_segments(k);
+    t.lin[0] = k->lin_hi; t.lin[1] = k->lin_lo; t.lin[2] = k->lin_slope;
+    std::memcpy(t.seg, k->seg, sizeof t.seg);
+    if (cache.size() > 64) cache.clear();
+    it = cache.emplace(std::move(key), t).first;
+  }
+  const SegTable& t = it->second;
+  k->lin_hi = t.lin[0]; k->lin_lo = t.lin[1]; k->lin_slope = t.lin[2];
+  std::memcpy(k->seg, t.seg, sizeof t.seg);
+  return t.ok;
+}
+
 // MactConfig -> kernel coefficient block.  Degree bounds follow the bundled
 // registry (approximants.py:168-265): CIELAB rationals n,m in 2..4, the HSI
 // refit 2..5, SCT polynomials 4..5.  Anything else is UnknownApproximant.
@@ -144,6 +234,11 @@ int make_kcoeffs(const MactCoeffs* c, KCoeffs* k) {
       k->b_s = (float)(200.0 * sc);
     }
   }
+#ifdef MACT_LAB_NO_SEG   // A/B builds: keep the fp64 evaluation
+  k->lab_seg = 0;
+#else
+  k->lab_seg = build_lab_segments(k) ? 1 : 0;
+#endif
   return MACT_OK;
 }
 
@@ -151,5 +246,10 @@ int make_kcoeffs(const MactCoeffs* c, KCoeffs* k) {
 
 extern "C" const char* mact_last_error(void) { return mact::g_last_error.c_str(); }
 extern "C" int mact_version(void) { return 100; }
+extern "C" int mact_lab_eval_path(const MactCoeffs* c) {
+  mact::KCoeffs k;
+  if (int rc = mact::make_kcoeffs(c, &k)) return rc;
+  return k.lab_seg ? MACT_LAB_PATH_SEG : k.monic44 ? MACT_LAB_PATH_MONIC : MACT_LAB_PATH_PQ;
+}
 extern "C" uint64_t mact_launch_count(void) { return mact::g_launches.load(); }
 extern "C" void mact_launch_count_reset(void) { mact::g_launches.store(0); }

@@ -209,13 +209,22 @@ __global__ void __launch_bounds__(NT) k_direct(const uint8_t* __restrict__ in, O
                                                const __grid_constant__ typename Op::Params p) {
   extern __shared__ __align__(128) uint8_t smem[];
   auto* sh = reinterpret_cast<typename Op::Shared*>(smem);
-  Op::init(sh, p);
-  __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t* w = reinterpret_cast<const uint32_t*>(in);
-  for (int64_t gi = blockIdx.x * (int64_t)NT + threadIdx.x; gi < ngroups; gi += (int64_t)gridDim.x * NT) {
+  const int64_t stride = (int64_t)gridDim.x * NT;
+  int64_t gi = blockIdx.x * (int64_t)NT + threadIdx.x;
+  // the first group's loads are in flight while the CTA stages its tables
+  uint32_t w0 = 0, w1 = 0, w2 = 0;
+  if (gi < ngroups) { w0 = __ldg(w + 3 * gi); w1 = __ldg(w + 3 * gi + 1); w2 = __ldg(w + 3 * gi + 2); }
+  Op::init(sh, p);
+  __syncthreads();
+  for (; gi < ngroups; gi += stride) {
     float o[4][Op::NOUT][3];
-    Op::px4w(__ldg(w + 3 * gi), __ldg(w + 3 * gi + 1), __ldg(w + 3 * gi + 2), sh, lane, p, o);
+    Op::px4w(w0, w1, w2, sh, lane, p, o);
+    if (gi + stride < ngroups) {
+      const uint32_t* q = w + 3 * (gi + stride);
+      w0 = __ldg(q); w1 = __ldg(q + 1); w2 = __ldg(q + 2);
+    }
 #pragma unroll
     for (int k = 0; k < Op::NOUT; ++k) {
       if (outs.o[k] == nullptr) continue;

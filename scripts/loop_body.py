@@ -1,8 +1,8 @@
 """Opcode histogram of the main tile loop of a k_stream kernel (between the
 mbarrier TRYWAIT and the bulk-store issue).  python scripts/loop_body.py OpLab"""
-import collections, re, subprocess, sys
+import collections, os, re, subprocess, sys
 name = sys.argv[1]
-out = subprocess.run(["cuobjdump", "-sass", "paper_1009_0854_b200/libmact_cuda.so"], capture_output=True, text=True).stdout
+out = subprocess.run(["cuobjdump", "-sass", os.environ.get("MACT_LIB", "paper_1009_0854_b200/libmact_cuda.so")], capture_output=True, text=True).stdout
 for f in re.split(r"\n\s*Function : ", out)[1:]:
     fn = f.split("\n", 1)[0]
     if "k_ws" not in fn or name not in fn:

@@ -2,6 +2,7 @@
 every symbol include/mact_cuda.h declares, and the ctypes structs match the C
 layout (checked by compiling the header with gcc)."""
 
+import ctypes as C
 import os
 import re
 import subprocess
@@ -140,3 +141,14 @@ int main(void) {
                     "-L", libdir, "-l:" + _lib.LIB_PATH.name, "-Wl,-rpath," + libdir], check=True)
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0 and r.stdout.strip() == "ok", r.stdout + r.stderr
+
+
+def test_lab_eval_path_segmented_for_every_registry_rational(lib):
+    """Host-only: the segmented fp32 lightness kernel is fitted for
+    every bundled CIELAB rational (approximants.py:179-211) and passes the
+    host-side 1e-8 fit check, so no configuration falls back to fp64."""
+    from paper_1009_0854_b200 import _lib, fast
+    from oracle import mact_oracle as O
+    for degs in O.CBRT_RATIONALS:
+        cfg = fast.MactConfig(cielab_degrees=degs)
+        assert lib.mact_lab_eval_path(C.byref(cfg._pack())) == _lib.LAB_PATH_SEG, degs

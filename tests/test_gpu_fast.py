@@ -40,6 +40,24 @@ def test_full_cube_vs_oracle(P, space):
         CHECK[space](got[s:s + (1 << 22)], O.FAST[space](host[s:s + (1 << 22)]))
 
 
+@pytest.mark.parametrize("degs", [(2, 2), (2, 3), (3, 2), (2, 4), (3, 3), (4, 2), (3, 4), (4, 3)])
+def test_lab_full_cube_every_degree(P, degs):
+    """The segmented fp32 lightness kernel is fitted per configuration: every
+    bundled rational, all 2^24 colours, against the oracle (default (4,4) is
+    test_full_cube_vs_oracle)."""
+    from paper_1009_0854_b200 import _lib
+    fast = P["fast"]
+    cfg = fast.MactConfig(cielab_degrees=degs)
+    import ctypes
+    assert _lib.load().mact_lab_eval_path(ctypes.byref(cfg._pack())) == _lib.LAB_PATH_SEG
+    cube = P["harness"].cube_chunk(0, 1 << 24, device="cuda")
+    got = fast.rgb_to_lab_fast(cube, cfg).cpu().numpy()
+    host = cube.cpu().numpy()
+    ocfg = O.OracleConfig(cielab_degrees=degs)
+    for s in range(0, 1 << 24, 1 << 22):
+        check_lab(got[s:s + (1 << 22)], O.rgb_to_lab_fast(host[s:s + (1 << 22)], ocfg))
+
+
 def test_other_degrees(P, golden):
     fast = P["fast"]
     s = dev(golden["small"])
