@@ -322,7 +322,7 @@ def run_ours(args, wl):
             "metric": METRIC, "value": round(value, 3), "unit": "Gpixels/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(total_ms / args.steps, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "u8->f32 (fp32 + fp64 rational)" if space in ("lab", "all") else "u8->f32",
+            "dtype": "u8->f32",
             "data": "synthetic (generated on device, seeded per image)",
             "config": {"workload": f"{args.workload}: {wl['desc']}", "pixels": n_total,
                        "transforms_per_step": transforms, "layout": "interleaved (N,3) fp32",

@@ -313,7 +313,7 @@ __global__ void k_fast_real(int space, const T* __restrict__ in, float* __restri
 #define MACT_ALL_G 1
 #endif
 #ifndef MACT_ALL_SIN
-#define MACT_ALL_SIN 2
+#define MACT_ALL_SIN 8
 #endif
 #ifndef MACT_ALL_NOB
 #define MACT_ALL_NOB 1
