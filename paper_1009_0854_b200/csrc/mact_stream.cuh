@@ -89,23 +89,31 @@ __global__ void __launch_bounds__(32 * (NW + 1)) k_ws(const uint8_t* __restrict_
   auto* sh = reinterpret_cast<typename Op::Shared*>(smem + L::sh_off);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  if (threadIdx.x == 0) {
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int64_t my_tiles = ntiles > first ? (ntiles - first + stride - 1) / stride : 0;
+  // The producer lane initialises the mbarriers and issues the first SIN tile
+  // loads before the CTA stages its tables, so the DRAM latency of the first
+  // tiles overlaps Op::init (one-tile-per-CTA launches: small images).
+  const bool producer = warp == NW && lane == 0;
+  const int64_t pre = my_tiles < SIN ? my_tiles : SIN;
+  if (producer) {
 #pragma unroll
     for (int s = 0; s < SIN; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NW);
     }
     fence_mbar_init();
+    for (int64_t i = 0; i < pre; ++i) {
+      mbar_arrive_expect_tx(&full[i], L::IN_BYTES);
+      bulk_g2s(in_s + (size_t)i * L::IN_BYTES, in + (first + i * stride) * L::IN_BYTES, L::IN_BYTES, &full[i]);
+    }
   }
   Op::init(sh, p);
   __syncthreads();
 
-  const int64_t first = blockIdx.x, stride = gridDim.x;
-  const int64_t my_tiles = ntiles > first ? (ntiles - first + stride - 1) / stride : 0;
-
   if (warp == NW) {                                       // ---- producer warp
     if (lane == 0) {
-      for (int64_t i = 0; i < my_tiles; ++i) {
+      for (int64_t i = pre; i < my_tiles; ++i) {
         const int s = (int)(i % SIN);
         if (i >= SIN) mbar_wait(&empty[s], (uint32_t)(((i / SIN) - 1) & 1));
         mbar_arrive_expect_tx(&full[s], L::IN_BYTES);
