@@ -26,6 +26,14 @@ __host__ __device__ constexpr double rgb2xyz(int row, int col) {
                   : (col == 0 ? 0.019331 : col == 1 ? 0.119195 : 0.950532);
 }
 
+// RGB->XYZ rows pre-divided by the D65 white point, rounded once to fp32 --
+// compile-time immediates (exact.py:21-66 fixes them; MactConfig cannot), so
+// the FMAs take them as instruction operands instead of registers reloaded
+// from the parameter bank.  KCoeffs::mxyz holds the same values (host check).
+__host__ __device__ constexpr float kMxyz(int row, int col) {
+  return (float)(rgb2xyz(row, col) / (row == 0 ? kWhiteX : row == 1 ? kWhiteY : kWhiteZ));
+}
+
 // Degree caps of the bundled sets: CIELAB rationals up to (4,4), the HSI
 // refit and SCT polynomials up to 5.  Unused high coefficients are zero,
 // which leaves Horner bit-identical (0*x + 0 = 0, then 0*x + a_n = a_n).

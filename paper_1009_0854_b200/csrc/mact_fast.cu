@@ -26,61 +26,58 @@ __device__ const float kGammaF32[256] = {
 #include "mact_gamma_table.inc"
 };
 
-// CIELAB op, tables in shared memory (SmemTab, mact_pixel.cuh): the
-// streaming kernels.
+// CIELAB op: both tables in one 64 KB-aligned shared block (PackedTab,
+// mact_pixel.cuh), which the skeleton places at an aligned offset.
 struct OpLab {
   static constexpr int NOUT = 1;
   using Params = KCoeffs;
-  using Tab = SmemTab<kLabSegCopies>;
-  struct Shared {
-    float gamma[256 * 32];   // GAMMA_TABLE (fast.py:35) in fp32, replicated per bank
-    float4 seg[kLabSegs * kLabSegCopies];   // KCoeffs::seg, bank-private copies
+  using Tab = PackedTab;
+  struct alignas(128) Shared {
+    static constexpr uint32_t kAlign = PackedTab::kBytes;
+    float rows[256 * 64];   // row r: GAMMA_TABLE[r] (fast.py:35, fp32) x 32 lanes | segment r x 8 copies
   };
+  static_assert(sizeof(Shared) == PackedTab::kBytes, "packed table is 256 rows of 256 B");
   static __device__ __forceinline__ void init(Shared* s, const Params& c) {
-    for (int k = threadIdx.x; k < 256; k += blockDim.x) {   // L2-resident table, replicated per bank
+    for (int k = threadIdx.x; k < 256; k += blockDim.x) {   // L2-resident table, one row per thread
       const float v = __ldg(kGammaF32 + k);
 #pragma unroll 8
-      for (int r = 0; r < 32; ++r) s->gamma[(k << 5) | ((r + k) & 31)] = v;
+      for (int r = 0; r < 32; ++r) s->rows[(k << 6) | ((r + k) & 31)] = v;
     }
     if (c.lab_seg) {   // warp-uniform parameter reads (one constant-cache broadcast per entry)
       const int lane = (int)(threadIdx.x & 31), nw = (int)(blockDim.x >> 5);
       for (int i = (int)(threadIdx.x >> 5); i < kLabSegs; i += nw) {
         const float4 v = c.seg[i];
-        if (lane < kLabSegCopies) s->seg[i * kLabSegCopies + lane] = v;
+        if (lane < 8) reinterpret_cast<float4*>(s->rows)[i * 16 + 8 + lane] = v;
       }
     }
   }
   static __device__ __forceinline__ Tab tab(const Shared* s, uint32_t lane, const Params&) {
-    return Tab(s->gamma, s->seg, lane);
+    return Tab(s->rows, lane);
   }
   static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
                                             uint32_t lane, const Params& c, float (*o)[3]) {
     const Lab3 v = lab_fast_u8(r, g, b, tab(s, lane, c), c);
     o[0][0] = v.c0; o[0][1] = v.c1; o[0][2] = v.c2;
   }
-  template <class T>
-  static __device__ __forceinline__ void px4w_tab(uint32_t w0, uint32_t w1, uint32_t w2, const T& t,
-                                                  const Params& c, float (*o)[1][3]) {
-    const uint32_t ch[12] = {byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), byte_of(w0, 3),
-                             byte_of(w1, 0), byte_of(w1, 1), byte_of(w1, 2), byte_of(w1, 3),
-                             byte_of(w2, 0), byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3)};
+  static __device__ __forceinline__ void px4w(uint32_t w0, uint32_t w1, uint32_t w2,
+                                              const Shared* s, uint32_t lane, const Params& c,
+                                              float (*o)[1][3]) {
+    const Tab t = tab(s, lane, c);
     if (c.lab_seg || c.monic44) {
       float v[4][3];
-      lab_fast_u8x4(ch, t, c, v);
+      lab_fast_u8x4(w0, w1, w2, t, c, v);
 #pragma unroll
       for (int q = 0; q < 4; ++q) { o[q][0][0] = v[q][0]; o[q][0][1] = v[q][1]; o[q][0][2] = v[q][2]; }
     } else {
+      const uint32_t ch[12] = {byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), byte_of(w0, 3),
+                               byte_of(w1, 0), byte_of(w1, 1), byte_of(w1, 2), byte_of(w1, 3),
+                               byte_of(w2, 0), byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3)};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const Lab3 v = lab_fast_u8(ch[3 * q], ch[3 * q + 1], ch[3 * q + 2], t, c);
         o[q][0][0] = v.c0; o[q][0][1] = v.c1; o[q][0][2] = v.c2;
       }
     }
-  }
-  static __device__ __forceinline__ void px4w(uint32_t w0, uint32_t w1, uint32_t w2,
-                                              const Shared* s, uint32_t lane, const Params& c,
-                                              float (*o)[1][3]) {
-    px4w_tab(w0, w1, w2, tab(s, lane, c), c, o);
   }
 };
 
@@ -200,10 +197,11 @@ struct OpExactF32 {
   static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
                                             uint32_t lane, const Params& c, float (*o)[3]) {
     if constexpr (SPACE == MACT_SPACE_LAB) {
-      const float gr = s->gamma[(r << 5) | lane], gg = s->gamma[(g << 5) | lane], gb = s->gamma[(b << 5) | lane];
-      const float fx = lab_f(fmaf(c.mxyz[2], gb, fmaf(c.mxyz[1], gg, c.mxyz[0] * gr)));
-      const float fy = lab_f(fmaf(c.mxyz[5], gb, fmaf(c.mxyz[4], gg, c.mxyz[3] * gr)));
-      const float fz = lab_f(fmaf(c.mxyz[8], gb, fmaf(c.mxyz[7], gg, c.mxyz[6] * gr)));
+      const PackedTab t(s->rows, lane);
+      const float gr = t.gamma(r), gg = t.gamma(g), gb = t.gamma(b);
+      const float fx = lab_f(lab_t(c, 0, gr, gg, gb));
+      const float fy = lab_f(lab_t(c, 1, gr, gg, gb));
+      const float fz = lab_f(lab_t(c, 2, gr, gg, gb));
       o[0][0] = fmaf(116.f, fy, -16.f);
       o[0][1] = 500.f * (fx - fy);
       o[0][2] = 200.f * (fy - fz);

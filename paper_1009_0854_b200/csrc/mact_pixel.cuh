@@ -113,7 +113,8 @@ __device__ __forceinline__ void lab_from_q(double qx, double qy, double qz, cons
 //  * SmemTab<COPIES>: staged in shared memory; gamma replicated 32x (entry i
 //    of lane l at float [i*32 + l], conflict-free), segment table in COPIES
 //    bank-private copies (entry i of copy k at float4 [i*COPIES + k]);
-//    addressed with 32-bit shared addresses off the lane's base.
+//    addressed with 32-bit shared addresses off the lane's base.  The error
+//    reduction kernel (static smem).
 //  (A policy reading the segment entries straight from the parameter bank
 //  -- no staging -- was measured at 30 Gpix/s: divergent constant-bank
 //  gathers serialise.)
@@ -127,19 +128,44 @@ __device__ __forceinline__ float4 lds_f32x4(uint32_t a) {
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
   return v;
 }
+//  * PackedTab: both tables in ONE 64 KB block aligned to 64 KB in the
+//    shared window, rows of 256 B: row r holds gamma entry r for the 32 lanes
+//    in its first 128 B, and (rows 0..127) the 8 copies of segment entry r in
+//    its last 128 B.  The gamma address of byte k of an input word is then
+//    one PRMT (the byte lands in address bits 8..15 of the lane's base), and
+//    the segment address of t one SHF + LOP3 (no clamp: t < 2^-7 wraps onto a
+//    row the linear branch overrides).  The streaming CIELAB kernels.
 template <int COPIES>
 struct SmemTab {
   uint32_t gl, sa;   // gamma + lane*4, seg + (lane % COPIES)*16 (shared addresses)
   __device__ __forceinline__ SmemTab(const float* gamma_rep, const float4* seg, uint32_t lane)
       : gl(smem_u32(gamma_rep) + lane * 4), sa(smem_u32(seg) + (lane & (COPIES - 1)) * 16) {}
   __device__ __forceinline__ float gamma(uint32_t v) const { return lds_f32(gl + (v << 7)); }
-  __device__ __forceinline__ float4 seg(uint32_t i) const { return lds_f32x4(sa + i * (COPIES * 16)); }
+  __device__ __forceinline__ float gamma_w(uint32_t w, int k) const { return gamma(byte_of(w, k)); }
+  __device__ __forceinline__ float4 seg_t(uint32_t b) const {
+    const uint32_t i = min((b >> kLabSegShift) - kLabSegBase, (uint32_t)(kLabSegs - 1));
+    return lds_f32x4(sa + i * (COPIES * 16));
+  }
 };
+struct PackedTab {
+  static constexpr uint32_t kBytes = 65536;
+  uint32_t gl, sa;   // table + lane*4, table + 128 + (lane % 8)*16 (shared addresses, table % 64K == 0)
+  __device__ __forceinline__ PackedTab(const void* table, uint32_t lane)
+      : gl(smem_u32(table) + lane * 4), sa(smem_u32(table) + 128 + (lane & 7) * 16) {}
+  __device__ __forceinline__ float gamma(uint32_t v) const { return lds_f32(gl + (v << 8)); }
+  __device__ __forceinline__ float gamma_w(uint32_t w, int k) const {
+    return lds_f32(__byte_perm(w, gl, 0x7604u | ((uint32_t)k << 4)));
+  }
+  __device__ __forceinline__ float4 seg_t(uint32_t b) const {
+    static_assert((kLabSegBase & 127u) == 0 && kLabSegs <= 128, "segment rows wrap mod 128");
+    return lds_f32x4(((b >> (kLabSegShift - 8)) & 0x7F00u) | sa);
+  }
+};
+
 template <class Tab>
 __device__ __forceinline__ void lab_seg(float t, const Tab& tab, float& h, float& d) {
   const uint32_t b = __float_as_uint(t);
-  const uint32_t i = min((b >> kLabSegShift) - kLabSegBase, (uint32_t)(kLabSegs - 1));
-  const float4 e = tab.seg(i);
+  const float4 e = tab.seg_t(b);
   const float u = t - __uint_as_float(b & kLabSegMask);
   h = e.x;
   d = u * fmaf(u, fmaf(u, e.w, e.z), e.y);
@@ -154,8 +180,8 @@ __device__ __forceinline__ void lab_from_seg(float hx, float dx, float hy, float
   A = 500.f * ((hx - hy) + (dx - dy));
   B = 200.f * ((hy - hz) + (dy - dz));
 }
-__device__ __forceinline__ float lab_t(const KCoeffs& c, int row, float gr, float gg, float gb) {
-  return fmaf(c.mxyz[3 * row + 2], gb, fmaf(c.mxyz[3 * row + 1], gg, c.mxyz[3 * row] * gr));
+__device__ __forceinline__ float lab_t(const KCoeffs&, int row, float gr, float gg, float gb) {
+  return fmaf(kMxyz(row, 2), gb, fmaf(kMxyz(row, 1), gg, kMxyz(row, 0) * gr));
 }
 
 // One pixel (tails, unaligned buffers, the fused error reduction).
@@ -190,13 +216,16 @@ __device__ __forceinline__ Lab3 lab_fast_u8(uint32_t r, uint32_t g, uint32_t b, 
 // 4 pixels (12 channels) per call, warp-converged.  Configurations that are
 // neither segmented nor monic (4,4) take lab_fast_u8 per pixel (caller).
 template <class Tab>
-__device__ __forceinline__ void lab_fast_u8x4(const uint32_t (&ch)[12], const Tab& tab,
+__device__ __forceinline__ void lab_fast_u8x4(uint32_t w0, uint32_t w1, uint32_t w2, const Tab& tab,
                                               const KCoeffs& c, float (*o)[3]) {
   float t[12];
   bool low = false;
+  const uint32_t w[3] = {w0, w1, w2};
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const float gr = tab.gamma(ch[3 * p]), gg = tab.gamma(ch[3 * p + 1]), gb = tab.gamma(ch[3 * p + 2]);
+  for (int p = 0; p < 4; ++p) {   // channel j = 3p + q is byte j % 4 of word j / 4
+    const float gr = tab.gamma_w(w[(3 * p) >> 2], (3 * p) & 3);
+    const float gg = tab.gamma_w(w[(3 * p + 1) >> 2], (3 * p + 1) & 3);
+    const float gb = tab.gamma_w(w[(3 * p + 2) >> 2], (3 * p + 2) & 3);
     t[3 * p] = lab_t(c, 0, gr, gg, gb);
     t[3 * p + 1] = lab_t(c, 1, gr, gg, gb);
     t[3 * p + 2] = lab_t(c, 2, gr, gg, gb);

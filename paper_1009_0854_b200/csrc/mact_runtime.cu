@@ -210,7 +210,11 @@ int make_kcoeffs(const MactCoeffs* c, KCoeffs* k) {
   }
   const double white[3] = {kWhiteX, kWhiteY, kWhiteZ};
   for (int r = 0; r < 3; ++r)
-    for (int col = 0; col < 3; ++col) k->mxyz[r * 3 + col] = (float)(rgb2xyz(r, col) / white[r]);
+    for (int col = 0; col < 3; ++col) {
+      k->mxyz[r * 3 + col] = (float)(rgb2xyz(r, col) / white[r]);
+      if (k->mxyz[r * 3 + col] != kMxyz(r, col))   // the kernels use the immediates
+        return set_error(MACT_ECUDA, "RGB->XYZ immediates differ from the host rounding");
+    }
   k->monic44 = (c->cbrt_num_deg == 4 && c->cbrt_den_deg == 4 && c->cbrt_num[4] != 0.0 &&
                 c->cbrt_den[4] != 0.0) ? 1 : 0;
   if (k->monic44) {

@@ -28,6 +28,8 @@
 // per-pixel generic kernel.
 #pragma once
 
+#include <type_traits>
+
 #include "mact_common.cuh"
 
 namespace mact {
@@ -60,20 +62,51 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Alignment an Op's Shared block needs in the shared-memory window
+// (Shared::kAlign; default 128).  Blocks aligned beyond 128 B are placed at
+// a fixed offset computed for the dynamic-smem window starting at
+// kDynSmemBase (sm_90 / sm_100 reserve the first 1 KB of every CTA's window);
+// the kernels check the resulting address and trap if the assumption breaks.
+constexpr uint32_t kDynSmemBase = 0x400;
+template <class T, class = void>
+struct ShAlign { static constexpr uint32_t v = 128; };
+template <class T>
+struct ShAlign<T, std::void_t<decltype(T::kAlign)>> { static constexpr uint32_t v = T::kAlign; };
+
 template <class Op, int NW, int G, int SIN, int NOB>
 struct WsLayout {
+  using Sh = typename Op::Shared;
+  static constexpr uint32_t A = ShAlign<Sh>::v;
   static constexpr int WPX = 128 * G;                 // pixels per warp slice
   static constexpr int TP = NW * WPX;                 // pixels per tile
   static constexpr int IN_BYTES = TP * 3;
   static constexpr int OUT_FLOATS = WPX * 3;          // one output array of one slice
   static constexpr size_t in_off = 0;
-  static constexpr size_t out_off = (size_t)SIN * IN_BYTES;
   static constexpr size_t out_warp = (size_t)NOB * Op::NOUT * OUT_FLOATS * 4;
-  static constexpr size_t bar_off = out_off + NW * out_warp;
-  static constexpr size_t sh_off = (bar_off + 2 * SIN * 8 + 127) / 128 * 128;
-  static constexpr size_t bytes = sh_off + sizeof(typename Op::Shared);
+  // A <= 128: [in stages][out slices][barriers][Shared]
+  // A  > 128: [in stages][barriers] ... [Shared at the aligned offset][out slices]
+  static constexpr size_t in_end = (size_t)SIN * IN_BYTES;
+  static constexpr size_t bar_off = A <= 128 ? in_end + NW * out_warp : in_end;
+  static constexpr size_t sh_off = A <= 128 ? (bar_off + 2 * SIN * 8 + 127) / 128 * 128
+                                            : (A - kDynSmemBase % A) % A;
+  static constexpr size_t out_off = A <= 128 ? in_end : sh_off + sizeof(Sh);
+  static constexpr size_t bytes = A <= 128 ? sh_off + sizeof(Sh) : out_off + NW * out_warp;
+  static_assert(A <= 128 || bar_off + 2 * SIN * 8 <= sh_off, "stages overlap the aligned tables");
   static constexpr int threads = 32 * (NW + 1);
 };
+// Shared block of a per-pixel kernel at the start of dynamic smem, aligned at run time.
+template <class Op>
+__device__ __forceinline__ typename Op::Shared* shared_block(uint8_t* smem) {
+  constexpr uint32_t A = ShAlign<typename Op::Shared>::v;
+  if constexpr (A <= 128) return reinterpret_cast<typename Op::Shared*>(smem);
+  const uint32_t pad = (A - (smem_u32(smem) & (A - 1))) & (A - 1);
+  return reinterpret_cast<typename Op::Shared*>(smem + pad);
+}
+template <class Op>
+constexpr size_t shared_block_bytes() {
+  constexpr uint32_t A = ShAlign<typename Op::Shared>::v;
+  return sizeof(typename Op::Shared) + (A <= 128 ? 0 : A);
+}
 
 template <class Op, int NW, int G, int SIN, int NOB>
 __global__ void __launch_bounds__(32 * (NW + 1)) k_ws(const uint8_t* __restrict__ in, Outs outs,
@@ -88,6 +121,9 @@ __global__ void __launch_bounds__(32 * (NW + 1)) k_ws(const uint8_t* __restrict_
   uint64_t* empty = full + SIN;
   auto* sh = reinterpret_cast<typename Op::Shared*>(smem + L::sh_off);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if constexpr (L::A > 128) {
+    if (smem_u32(sh) & (L::A - 1)) __trap();            // window base differs from kDynSmemBase
+  }
 
   const int64_t first = blockIdx.x, stride = gridDim.x;
   const int64_t my_tiles = ntiles > first ? (ntiles - first + stride - 1) / stride : 0;
@@ -186,7 +222,7 @@ __global__ void __launch_bounds__(NT) k_generic(const uint8_t* __restrict__ in, 
                                                  int64_t start, int64_t n, int planar,
                                                  const __grid_constant__ typename Op::Params p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  auto* sh = reinterpret_cast<typename Op::Shared*>(smem);
+  auto* sh = shared_block<Op>(smem);
   Op::init(sh, p);
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
@@ -216,7 +252,7 @@ template <class Op, int NT>
 __global__ void __launch_bounds__(NT) k_direct(const uint8_t* __restrict__ in, Outs outs, int64_t ngroups,
                                                const __grid_constant__ typename Op::Params p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  auto* sh = reinterpret_cast<typename Op::Shared*>(smem);
+  auto* sh = shared_block<Op>(smem);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t* w = reinterpret_cast<const uint32_t*>(in);
   const int64_t stride = (int64_t)gridDim.x * NT;
@@ -249,7 +285,7 @@ inline int launch_direct(const uint8_t* in, Outs outs, int64_t n, const typename
                          cudaStream_t st, const char* name) {
   NvtxRange range(name);
   auto kfn = k_direct<Op, NT>;
-  const size_t sb = sizeof(typename Op::Shared);
+  const size_t sb = shared_block_bytes<Op>();
   const int64_t cap = persistent_grid((const void*)kfn, NT, sb);
   if (cap <= 0) return MACT_ECUDA;
   const int64_t ngroups = n / 4;
@@ -286,7 +322,7 @@ inline int launch_stream_t(const uint8_t* in, Outs outs, int64_t n, int planar,
   const int64_t done = ntiles * L::TP;
   if (done < n) {
     auto kfn = k_generic<Op, 256>;
-    const size_t sb = sizeof(typename Op::Shared);
+    const size_t sb = shared_block_bytes<Op>();
     const int64_t cap = persistent_grid((const void*)kfn, 256, sb);
     if (cap <= 0) return MACT_ECUDA;
     int64_t grid = (n - done + 255) / 256;
