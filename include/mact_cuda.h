@@ -259,7 +259,8 @@ int mact_probe_expand(const uint8_t* rgb, float* out, int64_t n, void* stream);
  * (fast.py:110-115): MACT_LAB_PATH_SEG = segmented fp32 cubic (the default
  * when the host-side fit check passes), MACT_LAB_PATH_MONIC = fp64 monic
  * (4,4) quotient, MACT_LAB_PATH_PQ = fp64 P/Q; negative = error status.
- * Host-only (no device work). */
+ * The environment variable MACT_LAB_EVAL=fp64 (read per call) forces the fp64
+ * evaluation.  Host-only (no device work). */
 #define MACT_LAB_PATH_SEG 1
 #define MACT_LAB_PATH_MONIC 2
 #define MACT_LAB_PATH_PQ 3

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -238,10 +239,14 @@ int make_kcoeffs(const MactCoeffs* c, KCoeffs* k) {
       k->b_s = (float)(200.0 * sc);
     }
   }
+  // MACT_LAB_EVAL=fp64 in the environment (read per call) keeps the fp64
+  // evaluation: an A/B switch, and how the tests exercise the fallback.
+  const char* ev = std::getenv("MACT_LAB_EVAL");
+  const bool force_fp64 = ev != nullptr && std::strcmp(ev, "fp64") == 0;
 #ifdef MACT_LAB_NO_SEG   // A/B builds: keep the fp64 evaluation
   k->lab_seg = 0;
 #else
-  k->lab_seg = build_lab_segments(k) ? 1 : 0;
+  k->lab_seg = !force_fp64 && build_lab_segments(k) ? 1 : 0;
 #endif
   return MACT_OK;
 }

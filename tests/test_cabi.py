@@ -152,3 +152,12 @@ def test_lab_eval_path_segmented_for_every_registry_rational(lib):
     for degs in O.CBRT_RATIONALS:
         cfg = fast.MactConfig(cielab_degrees=degs)
         assert lib.mact_lab_eval_path(C.byref(cfg._pack())) == _lib.LAB_PATH_SEG, degs
+
+
+def test_lab_eval_path_env_switch(lib, monkeypatch):
+    """MACT_LAB_EVAL=fp64 selects the fp64 evaluation (host-only query)."""
+    from paper_1009_0854_b200 import _lib, fast
+    monkeypatch.setenv("MACT_LAB_EVAL", "fp64")
+    assert lib.mact_lab_eval_path(C.byref(fast.DEFAULT_CONFIG._pack())) == _lib.LAB_PATH_MONIC
+    monkeypatch.delenv("MACT_LAB_EVAL")
+    assert lib.mact_lab_eval_path(C.byref(fast.DEFAULT_CONFIG._pack())) == _lib.LAB_PATH_SEG

@@ -58,6 +58,25 @@ def test_lab_full_cube_every_degree(P, degs):
         check_lab(got[s:s + (1 << 22)], O.rgb_to_lab_fast(host[s:s + (1 << 22)], ocfg))
 
 
+@pytest.mark.parametrize("degs", [(4, 4), (3, 3)])
+def test_lab_fp64_fallback_full_cube(P, degs, monkeypatch):
+    """MACT_LAB_EVAL=fp64 keeps the fp64 evaluation (monic (4,4) quotient, P/Q
+    otherwise) -- the path a configuration whose segment fit fails takes."""
+    import ctypes
+    from paper_1009_0854_b200 import _lib
+    monkeypatch.setenv("MACT_LAB_EVAL", "fp64")
+    fast = P["fast"]
+    cfg = fast.MactConfig(cielab_degrees=degs)
+    want = _lib.LAB_PATH_MONIC if degs == (4, 4) else _lib.LAB_PATH_PQ
+    assert _lib.load().mact_lab_eval_path(ctypes.byref(cfg._pack())) == want
+    cube = P["harness"].cube_chunk(0, 1 << 24, device="cuda")
+    got = fast.rgb_to_lab_fast(cube, cfg).cpu().numpy()
+    host = cube.cpu().numpy()
+    ocfg = O.OracleConfig(cielab_degrees=degs)
+    for s in range(0, 1 << 24, 1 << 22):
+        check_lab(got[s:s + (1 << 22)], O.rgb_to_lab_fast(host[s:s + (1 << 22)], ocfg))
+
+
 def test_other_degrees(P, golden):
     fast = P["fast"]
     s = dev(golden["small"])
