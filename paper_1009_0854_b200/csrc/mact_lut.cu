@@ -39,6 +39,84 @@ struct LutParams {
   const float4* lat;   // (n^3, 4) fp32, r-major, padded
 };
 
+// ---------------------------------------------- 64-bit fixed-point lattice
+// Node = (q0 | q1 << 21 | q2 << 42), q_c in 21 / 21 / 22 bits, value
+// v_c = lo_c + S_c q_c.  Decoding ORs q_c into the mantissa of 2^23 (exact
+// float F = 2^23 + q_c) and takes ONE fma: fmaf(F, S_c, K_c) with
+// K_c = lo_c - S_c 2^23 chosen exactly representable (rounded down from
+// min_c - S_c 2^23, so lo_c <= min_c), i.e. S_c q_c + lo_c rounded once.
+// Enabled only when every half-step S_c / 2 <= kLutQuantTol (CIELAB 17^3:
+// 2.4e-5 / 4.4e-5 / 2.4e-5 on L*, a*, b*), so an interpolated value moves by
+// at most sum|w| * 4.4e-5 (sum|w| = 1 for trilinear / prism / tetrahedral,
+// <= 1.5 for the pyramid) -- inside the 1e-4 north-star tolerance.  Other
+// lattices (wider ranges, non-finite values) keep the fp32 planes.
+constexpr double kLutQuantTol = 5e-5;
+struct LutQuant {
+  float s[3], k[3];
+  int on;
+};
+__device__ __forceinline__ uint2 lut_quant_pack(const LutQuant& q, float4 v) {
+  const double lo0 = (double)q.k[0] + (double)q.s[0] * 8388608.0;
+  const double lo1 = (double)q.k[1] + (double)q.s[1] * 8388608.0;
+  const double lo2 = (double)q.k[2] + (double)q.s[2] * 8388608.0;
+  const uint32_t q0 = (uint32_t)__double2uint_rn(((double)v.x - lo0) / (double)q.s[0]);
+  const uint32_t q1 = (uint32_t)__double2uint_rn(((double)v.y - lo1) / (double)q.s[1]);
+  const uint32_t q2 = (uint32_t)__double2uint_rn(((double)v.z - lo2) / (double)q.s[2]);
+  return make_uint2(q0 | (q1 << 21), (q1 >> 11) | (q2 << 10));
+}
+__device__ __forceinline__ float3 lut_quant_unpack(const LutQuant& q, uint2 w) {
+  const float f0 = __uint_as_float((w.x & 0x1FFFFFu) | 0x4B000000u);
+  const float f1 = __uint_as_float((__funnelshift_r(w.x, w.y, 21) & 0x1FFFFFu) | 0x4B000000u);
+  const float f2 = __uint_as_float((w.y >> 10) | 0x4B000000u);
+  return make_float3(fmaf(f0, q.s[0], q.k[0]), fmaf(f1, q.s[1], q.k[1]), fmaf(f2, q.s[2], q.k[2]));
+}
+// Per-component min / max of the lattice (block reduction, exact) and the
+// quantisation parameters; all threads of the CTA, ends with __syncthreads.
+__device__ __forceinline__ void lut_quant_setup(const float4* lat, int nn, LutQuant* out, float (*red)[6]) {
+  float m[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  bool finite = true;
+  for (int i = threadIdx.x; i < nn; i += blockDim.x) {
+    const float4 v = __ldg(lat + i);
+    finite &= isfinite(v.x) && isfinite(v.y) && isfinite(v.z);
+    m[0] = fminf(m[0], v.x); m[1] = fminf(m[1], v.y); m[2] = fminf(m[2], v.z);
+    m[3] = fmaxf(m[3], v.x); m[4] = fmaxf(m[4], v.y); m[5] = fmaxf(m[5], v.z);
+  }
+  if (!finite) m[0] = NAN;
+  const int any_nan = __syncthreads_or(!finite);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      const float x = __shfl_xor_sync(0xffffffffu, m[c], o);
+      m[c] = c < 3 ? fminf(m[c], x) : fmaxf(m[c], x);
+    }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < 6; ++c) red[warp][c] = m[c];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < nw; ++w)
+      for (int c = 0; c < 6; ++c) m[c] = c < 3 ? fminf(m[c], red[w][c]) : fmaxf(m[c], red[w][c]);
+    LutQuant q;
+    q.on = !any_nan;
+    const int bits[3] = {21, 21, 22};
+    for (int c = 0; c < 3; ++c) {
+      const double lo = m[c], range = (double)m[c + 3] - lo;
+      // two spare codes: lo_c sits below min_c by less than one step
+      const float sc = __double2float_ru(fmax(range, 1e-30) / (double)((1u << bits[c]) - 3u));
+      const float kc = __double2float_rd(lo - (double)sc * 8388608.0);
+      q.s[c] = sc;
+      q.k[c] = kc;
+      const double top = ((double)m[c + 3] - ((double)kc + (double)sc * 8388608.0)) / (double)sc;
+      if (!((double)sc * 0.5 <= kLutQuantTol) || !isfinite(kc) || !(top <= (double)(1u << bits[c]) - 1.5))
+        q.on = 0;
+    }
+    *out = q;
+  }
+  __syncthreads();
+}
+
 template <int N, int METHOD>
 struct OpLut {
   static constexpr int NOUT = 1;
@@ -49,33 +127,59 @@ struct OpLut {
   // slot k = lane & 7 lives at float4 index 8 i + k, so the 8 lanes of a
   // phase always hit 8 different groups (8 x 729 x 16 B = 93 KB).
   static constexpr bool PRIV = N <= 9;
+  // 17^3: 64-bit fixed-point nodes when the lattice's value ranges allow it
+  // (LutQuant; one LDS.64 per node instead of LDS.64 + LDS.32), else the
+  // fp32 planes.  The choice is made per CTA from the lattice itself, by the
+  // same deterministic arithmetic in every CTA.
+  static constexpr bool PACK = SMEM && !PRIV;
   struct Shared {
     float4 lat[PRIV ? 8 * N * N * N : 1];
-    float2 c01[SMEM && !PRIV ? N * N * N : 1];
-    float c2[SMEM && !PRIV ? N * N * N : 1];
+    union {
+      struct {
+        float2 c01[PACK ? N * N * N : 1];
+        float c2[PACK ? N * N * N : 1];
+      } f;
+      uint2 pk[PACK ? N * N * N : 1];
+    } u;
+    LutQuant q;
+    float red[32][6];
   };
   static __device__ __forceinline__ void init(Shared* s, const Params& p) {
     if constexpr (PRIV) {
       for (int i = threadIdx.x; i < 8 * N * N * N; i += blockDim.x) s->lat[i] = __ldg(p.lat + (i >> 3));
-    } else if constexpr (SMEM) {
+    } else if constexpr (PACK) {
+      lut_quant_setup(p.lat, N * N * N, &s->q, s->red);   // ends with __syncthreads
+      const LutQuant q = s->q;
       for (int i = threadIdx.x; i < N * N * N; i += blockDim.x) {
         const float4 v = __ldg(p.lat + i);
-        s->c01[i] = make_float2(v.x, v.y);
-        s->c2[i] = v.z;
+        if (q.on) {
+          s->u.pk[i] = lut_quant_pack(q, v);
+        } else {
+          s->u.f.c01[i] = make_float2(v.x, v.y);
+          s->u.f.c2[i] = v.z;
+        }
       }
     }
   }
-  static __device__ __forceinline__ float3 node(const Shared* s, const Params& p, int i, uint32_t lane) {
+  // PK: the CTA's lattice is in the fixed-point format (decided once per call site, not per node)
+  template <bool PK = false>
+  static __device__ __forceinline__ float3 node(const Shared* s, const Params& p, int i, uint32_t lane,
+                                                const LutQuant& q) {
     if constexpr (PRIV) {
       const float4 v = s->lat[(i << 3) | (lane & 7)];
       return make_float3(v.x, v.y, v.z);
-    } else if constexpr (SMEM) {
-      const float2 v = s->c01[i];
-      return make_float3(v.x, v.y, s->c2[i]);
+    } else if constexpr (PACK) {
+      if constexpr (PK) return lut_quant_unpack(q, s->u.pk[i]);
+      const float2 v = s->u.f.c01[i];
+      return make_float3(v.x, v.y, s->u.f.c2[i]);
     } else {
       const float4 v = __ldg(p.lat + i);
       return make_float3(v.x, v.y, v.z);
     }
+  }
+  static __device__ __forceinline__ LutQuant quant(const Shared* s) {
+    if constexpr (PACK) return s->q;
+    else return LutQuant{};
   }
   static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
                                             uint32_t lane, const Params& p, float (*o)[3]) {
@@ -83,11 +187,13 @@ struct OpLut {
     int idx[K];
     float w[K];
     lut_nodes<N, METHOD>(r, g, b, idx, w);
-    float3 v = node(s, p, idx[0], lane);
+    const LutQuant q = quant(s);
+    auto nd = [&](int i) { return q.on ? node<true>(s, p, i, lane, q) : node<false>(s, p, i, lane, q); };
+    float3 v = nd(idx[0]);
     float a0 = w[0] * v.x, a1 = w[0] * v.y, a2 = w[0] * v.z;
 #pragma unroll
     for (int j = 1; j < K; ++j) {
-      v = node(s, p, idx[j], lane);
+      v = nd(idx[j]);
       a0 = fmaf(w[j], v.x, a0);
       a1 = fmaf(w[j], v.y, a1);
       a2 = fmaf(w[j], v.z, a2);
@@ -98,9 +204,23 @@ struct OpLut {
   // 4*K independent gathers are in flight per thread (L2 latency for 33^3,
   // LDS latency for the smem lattice).  Trilinear (K = 8) goes 2 pixels at a
   // time to bound register pressure.
+  using Ctx = LutQuant;   // kept in registers by the streaming kernel
+  static __device__ __forceinline__ Ctx ctx(const Shared* s, const Params&) { return quant(s); }
+  static __device__ __forceinline__ void px4w_ctx(uint32_t w0, uint32_t w1, uint32_t w2,
+                                                  const Shared* s, uint32_t lane, const Params& p,
+                                                  const Ctx& qt, float (*o)[1][3]) {
+    if (PACK && qt.on) px4w_t<PACK>(w0, w1, w2, s, lane, p, qt, o);
+    else px4w_t<false>(w0, w1, w2, s, lane, p, qt, o);
+  }
   static __device__ __forceinline__ void px4w(uint32_t w0, uint32_t w1, uint32_t w2,
                                               const Shared* s, uint32_t lane, const Params& p,
                                               float (*o)[1][3]) {
+    px4w_ctx(w0, w1, w2, s, lane, p, quant(s), o);
+  }
+  template <bool PK>
+  static __device__ __forceinline__ void px4w_t(uint32_t w0, uint32_t w1, uint32_t w2,
+                                                const Shared* s, uint32_t lane, const Params& p,
+                                                const LutQuant& qt, float (*o)[1][3]) {
     constexpr int K = LutK<METHOD>::K;
     constexpr int PB = K > 6 ? 2 : 4;                 // pixels per batch
     const uint32_t ch[12] = {byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), byte_of(w0, 3),
@@ -117,7 +237,7 @@ struct OpLut {
 #pragma unroll
       for (int q = 0; q < PB; ++q)
 #pragma unroll
-        for (int j = 0; j < K; ++j) v[q][j] = node(s, p, idx[q][j], lane);
+        for (int j = 0; j < K; ++j) v[q][j] = node<PK>(s, p, idx[q][j], lane, qt);
 #pragma unroll
       for (int q = 0; q < PB; ++q) {
         float a0 = w[q][0] * v[q][0].x, a1 = w[q][0] * v[q][0].y, a2 = w[q][0] * v[q][0].z;

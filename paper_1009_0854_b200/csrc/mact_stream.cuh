@@ -73,6 +73,14 @@ struct ShAlign { static constexpr uint32_t v = 128; };
 template <class T>
 struct ShAlign<T, std::void_t<decltype(T::kAlign)>> { static constexpr uint32_t v = T::kAlign; };
 
+// Optional per-thread context an Op derives once from its staged tables
+// (Op::Ctx, Op::ctx(sh, p)) and the streaming kernel keeps in registers for
+// the whole tile loop (Op::px4w_ctx); Ops without one use px4w.
+template <class Op, class = void>
+struct HasCtx : std::false_type {};
+template <class Op>
+struct HasCtx<Op, std::void_t<typename Op::Ctx>> : std::true_type {};
+
 template <class Op, int NW, int G, int SIN, int NOB>
 struct WsLayout {
   using Sh = typename Op::Shared;
@@ -162,6 +170,10 @@ __global__ void __launch_bounds__(32 * (NW + 1)) k_ws(const uint8_t* __restrict_
 
   // ---- compute warps
   float* out_w = reinterpret_cast<float*>(smem + L::out_off + warp * L::out_warp);
+  const auto ctx = [&] {
+    if constexpr (HasCtx<Op>::value) return Op::ctx(sh, p);
+    else return 0;
+  }();
   for (int64_t i = 0; i < my_tiles; ++i) {
     const int64_t t = first + i * stride;
     const int s = (int)(i % SIN);
@@ -176,7 +188,10 @@ __global__ void __launch_bounds__(32 * (NW + 1)) k_ws(const uint8_t* __restrict_
     for (int g = 0; g < G; ++g) {
       const int grp = g * 32 + (int)lane;                 // 4-pixel group inside the warp slice
       float o[4][NOUT][3];
-      Op::px4w(wsrc[3 * grp], wsrc[3 * grp + 1], wsrc[3 * grp + 2], sh, lane, p, o);
+      if constexpr (HasCtx<Op>::value)
+        Op::px4w_ctx(wsrc[3 * grp], wsrc[3 * grp + 1], wsrc[3 * grp + 2], sh, lane, p, ctx, o);
+      else
+        Op::px4w(wsrc[3 * grp], wsrc[3 * grp + 1], wsrc[3 * grp + 2], sh, lane, p, o);
 #pragma unroll
       for (int k = 0; k < NOUT; ++k) {
         float* base = ob_s + k * L::OUT_FLOATS;

@@ -223,3 +223,33 @@ def test_lut_beyond_int32_pixel_count(grid):
     np.testing.assert_array_equal(out[idx].cpu().numpy(), ref[idx % (1 << 24)].cpu().numpy())
     del out, x
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("method", O.METHODS)
+def test_lut17_interp_full_cube(P, method):
+    """17^3 CIELAB LUT on all 2^24 colours vs the oracle on the same fp32
+    lattice values: covers the 64-bit fixed-point node format (quantisation
+    half-step <= 4.4e-5) inside the 1e-4 tolerance."""
+    lt = P["lut"].build_lut("lab", 17)
+    cube = P["harness"].cube_chunk(0, 1 << 24, device="cuda")
+    got = P["lut"].interpolate(lt, cube, method).cpu().numpy()
+    host = cube.cpu().numpy()
+    vals = lt.values.astype(np.float32).astype(np.float64)
+    worst = 0.0
+    for s in range(0, 1 << 24, 1 << 22):
+        worst = max(worst, check_lab(got[s:s + (1 << 22)], O.interpolate(vals, host[s:s + (1 << 22)], method)))
+    print(f"17^3 {method}: max |dLab| {worst:.3e}")
+
+
+def test_lut17_wide_range_lattice_keeps_fp32(P):
+    """A lattice whose value range is too wide for the fixed-point format
+    (x1000) takes the fp32 planes: the result still matches the oracle to fp32
+    accuracy."""
+    import dataclasses
+    lt = P["lut"].build_lut("lab", 17)
+    wide = dataclasses.replace(lt, values=lt.values * 1000.0, _device={})
+    img = np.random.default_rng(5).integers(0, 256, (1 << 16, 3), dtype=np.uint8)
+    got = P["lut"].interpolate(wide, dev(img), "tetrahedral").cpu().numpy()
+    vals = wide.values.astype(np.float32).astype(np.float64)
+    ref = O.interpolate(vals, img, "tetrahedral")
+    np.testing.assert_allclose(got, ref, rtol=2e-6, atol=1e-2)
