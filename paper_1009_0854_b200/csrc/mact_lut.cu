@@ -125,7 +125,10 @@ struct OpLut {
   // 9^3: bank-private copies.  An LDS.128 warp access is served 8 lanes per
   // phase, one 16-byte bank group per lane when conflict-free; node i of lane
   // slot k = lane & 7 lives at float4 index 8 i + k, so the 8 lanes of a
-  // phase always hit 8 different groups (8 x 729 x 16 B = 93 KB).
+  // phase always hit 8 different groups (8 x 729 x 16 B = 93 KB).  (The
+  // fixed-point node below with 16 copies -- conflict-free LDS.64 -- was
+  // measured slower here: 172-229 against 210-308 Gpix/s; without conflicts
+  // to save, the decode's 8 integer/FMA ops per node cost more issue.)
   static constexpr bool PRIV = N <= 9;
   // 17^3: 64-bit fixed-point nodes when the lattice's value ranges allow it
   // (LutQuant; one LDS.64 per node instead of LDS.64 + LDS.32), else the
