@@ -55,19 +55,22 @@ struct LutQuant {
   float s[3], k[3];
   int on;
 };
+// q_c = rint((v_c - lo_c) / S_c), the quotient taken as a product with the
+// fp64 reciprocal (|error| ~1e-9 codes: any rounding of it keeps |v - v'| <=
+// S_c / 2 + 1e-9 S_c); identical in every CTA.
 __device__ __forceinline__ uint2 lut_quant_pack(const LutQuant& q, float4 v) {
   const double lo0 = (double)q.k[0] + (double)q.s[0] * 8388608.0;
   const double lo1 = (double)q.k[1] + (double)q.s[1] * 8388608.0;
   const double lo2 = (double)q.k[2] + (double)q.s[2] * 8388608.0;
-  const uint32_t q0 = (uint32_t)__double2uint_rn(((double)v.x - lo0) / (double)q.s[0]);
-  const uint32_t q1 = (uint32_t)__double2uint_rn(((double)v.y - lo1) / (double)q.s[1]);
-  const uint32_t q2 = (uint32_t)__double2uint_rn(((double)v.z - lo2) / (double)q.s[2]);
+  const uint32_t q0 = (uint32_t)__double2uint_rn(((double)v.x - lo0) * (1.0 / (double)q.s[0]));
+  const uint32_t q1 = (uint32_t)__double2uint_rn(((double)v.y - lo1) * (1.0 / (double)q.s[1]));
+  const uint32_t q2 = (uint32_t)__double2uint_rn(((double)v.z - lo2) * (1.0 / (double)q.s[2]));
   return make_uint2(q0 | (q1 << 21), (q1 >> 11) | (q2 << 10));
 }
 __device__ __forceinline__ float3 lut_quant_unpack(const LutQuant& q, uint2 w) {
   const float f0 = __uint_as_float((w.x & 0x1FFFFFu) | 0x4B000000u);
   const float f1 = __uint_as_float((__funnelshift_r(w.x, w.y, 21) & 0x1FFFFFu) | 0x4B000000u);
-  const float f2 = __uint_as_float((w.y >> 10) | 0x4B000000u);
+  const float f2 = __uint_as_float((w.y >> 10) + 0x4B000000u);   // 22-bit field: add == or
   return make_float3(fmaf(f0, q.s[0], q.k[0]), fmaf(f1, q.s[1], q.k[1]), fmaf(f2, q.s[2], q.k[2]));
 }
 // Per-component min / max of the lattice (block reduction, exact) and the
@@ -171,10 +174,17 @@ struct OpLut {
     if constexpr (PRIV) {
       const float4 v = s->lat[(i << 3) | (lane & 7)];
       return make_float3(v.x, v.y, v.z);
-    } else if constexpr (PACK) {
-      if constexpr (PK) return lut_quant_unpack(q, s->u.pk[i]);
-      const float2 v = s->u.f.c01[i];
-      return make_float3(v.x, v.y, s->u.f.c2[i]);
+    } else if constexpr (PACK) {   // 32-bit shared addresses: one LEA per node
+      if constexpr (PK) {
+        uint2 w;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w.x), "=r"(w.y)
+                     : "r"(smem_u32(s->u.pk) + ((uint32_t)i << 3)));
+        return lut_quant_unpack(q, w);
+      }
+      float2 v;
+      asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y)
+                   : "r"(smem_u32(s->u.f.c01) + ((uint32_t)i << 3)));
+      return make_float3(v.x, v.y, lds_f32(smem_u32(s->u.f.c2) + ((uint32_t)i << 2)));
     } else {
       const float4 v = __ldg(p.lat + i);
       return make_float3(v.x, v.y, v.z);
@@ -189,7 +199,7 @@ struct OpLut {
     constexpr int K = LutK<METHOD>::K;
     int idx[K];
     float w[K];
-    lut_nodes<N, METHOD>(r, g, b, idx, w);
+    lut_nodes<N, METHOD, float, false>(r, g, b, idx, w);
     const LutQuant q = quant(s);
     auto nd = [&](int i) { return q.on ? node<true>(s, p, i, lane, q) : node<false>(s, p, i, lane, q); };
     float3 v = nd(idx[0]);
@@ -236,7 +246,7 @@ struct OpLut {
       float3 v[PB][K];
 #pragma unroll
       for (int q = 0; q < PB; ++q)
-        lut_nodes<N, METHOD>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], idx[q], w[q]);
+        lut_nodes<N, METHOD, float, false>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], idx[q], w[q]);
 #pragma unroll
       for (int q = 0; q < PB; ++q)
 #pragma unroll
@@ -503,7 +513,7 @@ __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
         float w[PB][K], v[PB][K];
 #pragma unroll
         for (int q = 0; q < PB; ++q)
-          lut_nodes<N, METHOD>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], idx[q], w[q]);
+          lut_nodes<N, METHOD, float, false>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], idx[q], w[q]);
 #pragma unroll
         for (int q = 0; q < PB; ++q)
 #pragma unroll
@@ -590,7 +600,7 @@ __global__ void __launch_bounds__(kLut33Threads, 1)
         float w[PB][K], v[PB][K];
 #pragma unroll
         for (int q = 0; q < PB; ++q)
-          lut_nodes<N, METHOD>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], idx[q], w[q]);
+          lut_nodes<N, METHOD, float, false>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], idx[q], w[q]);
 #pragma unroll
         for (int q = 0; q < PB; ++q)
 #pragma unroll

@@ -36,7 +36,12 @@ __device__ __forceinline__ void lut_locate(uint32_t p, int& base, int& rem) {
 }
 
 // Node flat indices and weights of one pixel.  rem values in [0,255].
-template <int N, int METHOD, typename W = float>
+// TIES = false (interpolation only): the tetrahedral order comes from
+// max / min / sum instead of the stable sort.  The weights are the same
+// integers; under ties the zero-weight middle node may be a different corner
+// of the cell, which leaves every sum bit-identical (fmaf(0, v, a) == a).
+// mact_lut_nodes reports the reference's indices and keeps TIES = true.
+template <int N, int METHOD, typename W = float, bool TIES = true>
 __device__ __forceinline__ void lut_nodes(uint32_t pr, uint32_t pg, uint32_t pb,
                                           int (&idx)[LutK<METHOD>::K],
                                           W (&w)[LutK<METHOD>::K]) {
@@ -85,6 +90,15 @@ __device__ __forceinline__ void lut_nodes(uint32_t pr, uint32_t pg, uint32_t pb,
     w[2] = fv * ((W)255 - fu) * inv2;
     w[3] = (W)(u * v - 255 * m) * inv2;
     w[4] = (W)m * inv1;
+  } else if constexpr (!TIES) {
+    const int d1 = max(rr, max(rg, rb)), d3 = min(rr, min(rg, rb)), d2 = rr + rg + rb - d1 - d3;
+    const int s1 = rr == d1 ? SR : rg == d1 ? SG : SB;     // stride of the largest offset
+    const int s3 = rb == d3 ? SB : rg == d3 ? SG : SR;     // ... of the smallest (!= s1 unless all equal)
+    idx[0] = bf; idx[1] = bf + s1; idx[2] = bf + SR + SG + SB - s3; idx[3] = bf + SR + SG + SB;
+    w[0] = (W)(255 - d1) * inv1;
+    w[1] = (W)(d1 - d2) * inv1;
+    w[2] = (W)(d2 - d3) * inv1;
+    w[3] = (W)d3 * inv1;
   } else {
     // stable argsort of -d (lut.py:185): ties keep r before g before b
     const int pos_r = (rg > rr) + (rb > rr);
