@@ -219,6 +219,8 @@ struct NvtxRange {
 int set_error(int code, const char* fmt, ...);
 int check_launch(const char* what);
 int num_sms();
+// cudaDevAttrReservedSharedMemoryPerBlock of the current device (cached).
+int reserved_smem();
 int make_kcoeffs(const MactCoeffs* c, KCoeffs* out);
 // Sets the dynamic-smem attribute once per (kernel, device) and returns the
 // persistent grid size occupancy x SM count (cached), or <= 0 on error.

@@ -58,6 +58,20 @@ int num_sms() {
   return sms;
 }
 
+int reserved_smem() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int v = -1;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess) v = -1;
+  cache[dev] = v;
+  return v;
+}
+
 int persistent_grid(const void* fn, int threads, size_t smem_bytes) {
   static std::mutex mu;
   static std::map<std::tuple<const void*, int, size_t, int>, int> cache;

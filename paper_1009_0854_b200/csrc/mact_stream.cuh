@@ -325,6 +325,11 @@ inline int launch_stream_t(const uint8_t* in, Outs outs, int64_t n, int planar,
     if (outs.o[k] && ((uintptr_t)outs.o[k] % 16) != 0) aligned = false;
   if (planar && (n % 4) != 0) aligned = false;
   const int64_t ntiles = aligned ? n / L::TP : 0;
+  if constexpr (L::A > 128) {   // the aligned-table layout assumes kDynSmemBase (the kernel traps otherwise)
+    if (reserved_smem() != (int)kDynSmemBase)
+      return set_error(MACT_ECUDA, "%s: %d B reserved shared memory per block, layout assumes %u", name,
+                       reserved_smem(), kDynSmemBase);
+  }
   if (ntiles > 0) {
     auto kfn = k_ws<Op, NW, G, SIN, NOB>;
     int64_t grid = persistent_grid((const void*)kfn, L::threads, L::bytes);
