@@ -40,8 +40,9 @@ struct OpLab {
   static __device__ __forceinline__ void init(Shared* s, const Params& c) {
     for (int k = threadIdx.x; k < 256; k += blockDim.x) {   // L2-resident table, one row per thread
       const float v = __ldg(kGammaF32 + k);
-#pragma unroll 8
-      for (int r = 0; r < 32; ++r) s->rows[(k << 6) | ((r + k) & 31)] = v;
+      float4* row = reinterpret_cast<float4*>(s->rows + (k << 6));
+#pragma unroll
+      for (int j = 0; j < 8; ++j) row[(j + k) & 7] = make_float4(v, v, v, v);   // rotated: 8 rows, 8 bank groups
     }
     if (c.lab_seg) {   // warp-uniform parameter reads (one constant-cache broadcast per entry)
       const int lane = (int)(threadIdx.x & 31), nw = (int)(blockDim.x >> 5);
