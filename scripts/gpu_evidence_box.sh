@@ -7,6 +7,7 @@ python scripts/c4_oracle_eps.py > gpurun_out/c4eps.txt 2>&1
 python scripts/precision.py lab > gpurun_out/precision.txt 2>&1
 bash scripts/sweep_gain.sh > gpurun_out/gain.txt 2>&1
 bash scripts/save_evidence.sh
+python -c "import __graft_entry__ as g; g.smoke(); print(\"smoke ok\")" > gpurun_out/smoke.txt 2>&1
 for m in trilinear prism pyramidal tetrahedral; do
   timeout 600 ncu --set full --clock-control none -k regex:"k_ws" -s 2 -c 1 -o gpurun_out/prof_lut17_$m -f \
     python scripts/prof_kernel.py --op lut17 --method $m --iters 1 > /dev/null 2>&1
