@@ -8,13 +8,16 @@
 // Device lattice format: (n^3, 4) fp32, r-major, node = (c0, c1, c2, 0) so a
 // node is one 16-byte load.  Interpolation runs inside the streaming skeleton
 // (mact_stream.cuh).  For grids 9^3 and 17^3 the lattice is staged once per
-// persistent CTA into shared memory as two planes, (c0, c1) float2 and c2
-// float (17^3 x 12 B = 59 KB): one LDS.64 + one LDS.32 per node.  Random
-// gathers are bank-conflict bound, and on B200 a random warp LDS.64 + LDS.32
-// costs 7.9 smem cycles against 9.4 for one LDS.128 of a padded float4 node
-// (tools/ldsbench.cu), with 25 % less smem per CTA.  33^3 (575 KB) exceeds a
-// CTA's 227 KB and is gathered with LDG.128 through L1/L2 (the lattice stays
-// L2-resident).
+// persistent CTA into shared memory: 9^3 as 8 bank-private float4 copies
+// (conflict-free LDS.128), 17^3 as 64-bit fixed-point nodes (LutQuant below:
+// one LDS.64 per node, 38 KB) or, for lattices whose value range is too wide
+// for that format, as two planes, (c0, c1) float2 and c2 float (59 KB): one
+// LDS.64 + one LDS.32 per node.  Random gathers are bank-conflict bound: on
+// B200 a random warp LDS.64 costs 5.2 smem cycles, LDS.64 + LDS.32 7.9, one
+// LDS.128 of a padded float4 node 9.4 (tools/ldsbench.cu).  33^3 (575 KB)
+// exceeds a CTA's 227 KB: a 3-CTA cluster holds one component per CTA
+// (k_lut33_comp), with the L1/L2 gather kernel only for tails and unaligned
+// buffers.
 #include <atomic>
 
 #include <cooperative_groups.h>
