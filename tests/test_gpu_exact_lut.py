@@ -253,3 +253,21 @@ def test_lut17_wide_range_lattice_keeps_fp32(P):
     vals = wide.values.astype(np.float32).astype(np.float64)
     ref = O.interpolate(vals, img, "tetrahedral")
     np.testing.assert_allclose(got, ref, rtol=2e-6, atol=1e-2)
+
+
+@pytest.mark.parametrize("scale", [0.25, 1.0, 1.1, 1.2, 3.0])
+@pytest.mark.parametrize("method", ["pyramidal", "tetrahedral"])
+def test_lut17_error_bound_either_format(P, scale, method):
+    """Lattices scaled around the fixed-point threshold (half-step 5e-5: the
+    CIELAB lattice x1.14): below it the 64-bit nodes are used, above it the
+    fp32 planes.  Either way |interp - oracle| <= 1.5 * 5e-5 (pyramid sum|w|)
+    plus fp32 rounding of the values."""
+    import dataclasses
+    lt = P["lut"].build_lut("lab", 17)
+    sc = dataclasses.replace(lt, values=lt.values * scale, _device={})
+    img = np.random.default_rng(11).integers(0, 256, (1 << 18, 3), dtype=np.uint8)
+    got = P["lut"].interpolate(sc, dev(img), method).cpu().numpy().astype(np.float64)
+    vals = sc.values.astype(np.float32).astype(np.float64)
+    ref = O.interpolate(vals, img, method)
+    bound = 1.5 * 5e-5 + 4e-7 * np.abs(ref).max()
+    assert np.abs(got - ref).max() <= bound
