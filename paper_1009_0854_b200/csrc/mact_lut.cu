@@ -70,11 +70,29 @@ __device__ __forceinline__ uint2 lut_quant_pack(const LutQuant& q, float4 v) {
   const uint32_t q2 = (uint32_t)__double2uint_rn(((double)v.z - lo2) * (1.0 / (double)q.s[2]));
   return make_uint2(q0 | (q1 << 21), (q1 >> 11) | (q2 << 10));
 }
-__device__ __forceinline__ float3 lut_quant_unpack(const LutQuant& q, uint2 w) {
+// A node as (c0, c1) + c2, so the (c0, c1) pair can use Blackwell's packed
+// fp32x2 FMA (FFMA2: one issue, each lane rounded exactly like FFMA).
+struct Node2 {
+  float2 xy;
+  float z;
+};
+__device__ __forceinline__ uint32_t mad_hi_u32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t r;   // hi(a * b) + c on the FMA pipe (IMAD.HI), where a shift + add would take the ALU pipe
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+__device__ __forceinline__ Node2 lut_quant_unpack2(const LutQuant& q, uint2 w) {
   const float f0 = __uint_as_float((w.x & 0x1FFFFFu) | 0x4B000000u);
   const float f1 = __uint_as_float((__funnelshift_r(w.x, w.y, 21) & 0x1FFFFFu) | 0x4B000000u);
-  const float f2 = __uint_as_float((w.y >> 10) + 0x4B000000u);   // 22-bit field: add == or
-  return make_float3(fmaf(f0, q.s[0], q.k[0]), fmaf(f1, q.s[1], q.k[1]), fmaf(f2, q.s[2], q.k[2]));
+  const float f2 = __uint_as_float(mad_hi_u32(w.y, 1u << 22, 0x4B000000u));   // (w.y >> 10) + 2^23 bits
+  Node2 n;
+  n.xy = __ffma2_rn(make_float2(f0, f1), make_float2(q.s[0], q.s[1]), make_float2(q.k[0], q.k[1]));
+  n.z = fmaf(f2, q.s[2], q.k[2]);
+  return n;
+}
+__device__ __forceinline__ float3 lut_quant_unpack(const LutQuant& q, uint2 w) {
+  const Node2 n = lut_quant_unpack2(q, w);
+  return make_float3(n.xy.x, n.xy.y, n.z);
 }
 // Per-component min / max of the lattice (block reduction, exact) and the
 // quantisation parameters; all threads of the CTA, ends with __syncthreads.
@@ -172,25 +190,25 @@ struct OpLut {
   }
   // PK: the CTA's lattice is in the fixed-point format (decided once per call site, not per node)
   template <bool PK = false>
-  static __device__ __forceinline__ float3 node(const Shared* s, const Params& p, int i, uint32_t lane,
-                                                const LutQuant& q) {
+  static __device__ __forceinline__ Node2 node(const Shared* s, const Params& p, int i, uint32_t lane,
+                                               const LutQuant& q) {
     if constexpr (PRIV) {
       const float4 v = s->lat[(i << 3) | (lane & 7)];
-      return make_float3(v.x, v.y, v.z);
+      return Node2{make_float2(v.x, v.y), v.z};
     } else if constexpr (PACK) {   // 32-bit shared addresses: one LEA per node
       if constexpr (PK) {
         uint2 w;
         asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w.x), "=r"(w.y)
                      : "r"(smem_u32(s->u.pk) + ((uint32_t)i << 3)));
-        return lut_quant_unpack(q, w);
+        return lut_quant_unpack2(q, w);
       }
       float2 v;
       asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y)
                    : "r"(smem_u32(s->u.f.c01) + ((uint32_t)i << 3)));
-      return make_float3(v.x, v.y, lds_f32(smem_u32(s->u.f.c2) + ((uint32_t)i << 2)));
+      return Node2{v, lds_f32(smem_u32(s->u.f.c2) + ((uint32_t)i << 2))};
     } else {
       const float4 v = __ldg(p.lat + i);
-      return make_float3(v.x, v.y, v.z);
+      return Node2{make_float2(v.x, v.y), v.z};
     }
   }
   static __device__ __forceinline__ LutQuant quant(const Shared* s) {
@@ -205,16 +223,16 @@ struct OpLut {
     lut_nodes<N, METHOD, float, false>(r, g, b, idx, w);
     const LutQuant q = quant(s);
     auto nd = [&](int i) { return q.on ? node<true>(s, p, i, lane, q) : node<false>(s, p, i, lane, q); };
-    float3 v = nd(idx[0]);
-    float a0 = w[0] * v.x, a1 = w[0] * v.y, a2 = w[0] * v.z;
+    Node2 v = nd(idx[0]);
+    float2 a01 = __fmul2_rn(make_float2(w[0], w[0]), v.xy);
+    float a2 = w[0] * v.z;
 #pragma unroll
-    for (int j = 1; j < K; ++j) {
+    for (int j = 1; j < K; ++j) {   // out += w_j V[node_j], node order (lut.py:233-236); FFMA2 = two FFMAs
       v = nd(idx[j]);
-      a0 = fmaf(w[j], v.x, a0);
-      a1 = fmaf(w[j], v.y, a1);
+      a01 = __ffma2_rn(make_float2(w[j], w[j]), v.xy, a01);
       a2 = fmaf(w[j], v.z, a2);
     }
-    o[0][0] = a0; o[0][1] = a1; o[0][2] = a2;
+    o[0][0] = a01.x; o[0][1] = a01.y; o[0][2] = a2;
   }
   // 4 pixels: all node indices first, then every node load, then the FMAs, so
   // 4*K independent gathers are in flight per thread (L2 latency for 33^3,
@@ -246,7 +264,7 @@ struct OpLut {
     for (int q0 = 0; q0 < 4; q0 += PB) {
       int idx[PB][K];
       float w[PB][K];
-      float3 v[PB][K];
+      Node2 v[PB][K];
 #pragma unroll
       for (int q = 0; q < PB; ++q)
         lut_nodes<N, METHOD, float, false>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], idx[q], w[q]);
@@ -256,14 +274,14 @@ struct OpLut {
         for (int j = 0; j < K; ++j) v[q][j] = node<PK>(s, p, idx[q][j], lane, qt);
 #pragma unroll
       for (int q = 0; q < PB; ++q) {
-        float a0 = w[q][0] * v[q][0].x, a1 = w[q][0] * v[q][0].y, a2 = w[q][0] * v[q][0].z;
+        float2 a01 = __fmul2_rn(make_float2(w[q][0], w[q][0]), v[q][0].xy);
+        float a2 = w[q][0] * v[q][0].z;
 #pragma unroll
         for (int j = 1; j < K; ++j) {
-          a0 = fmaf(w[q][j], v[q][j].x, a0);
-          a1 = fmaf(w[q][j], v[q][j].y, a1);
+          a01 = __ffma2_rn(make_float2(w[q][j], w[q][j]), v[q][j].xy, a01);
           a2 = fmaf(w[q][j], v[q][j].z, a2);
         }
-        o[q0 + q][0][0] = a0; o[q0 + q][0][1] = a1; o[q0 + q][0][2] = a2;
+        o[q0 + q][0][0] = a01.x; o[q0 + q][0][1] = a01.y; o[q0 + q][0][2] = a2;
       }
     }
   }
