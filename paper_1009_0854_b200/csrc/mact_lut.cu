@@ -90,10 +90,6 @@ __device__ __forceinline__ Node2 lut_quant_unpack2(const LutQuant& q, uint2 w) {
   n.z = fmaf(f2, q.s[2], q.k[2]);
   return n;
 }
-__device__ __forceinline__ float3 lut_quant_unpack(const LutQuant& q, uint2 w) {
-  const Node2 n = lut_quant_unpack2(q, w);
-  return make_float3(n.xy.x, n.xy.y, n.z);
-}
 // Per-component min / max of the lattice (block reduction, exact) and the
 // quantisation parameters; all threads of the CTA, ends with __syncthreads.
 __device__ __forceinline__ void lut_quant_setup(const float4* lat, int nn, LutQuant* out, float (*red)[6]) {
