@@ -82,7 +82,12 @@ __device__ __forceinline__ uint32_t mad_hi_u32(uint32_t a, uint32_t b, uint32_t 
   return r;
 }
 __device__ __forceinline__ Node2 lut_quant_unpack2(const LutQuant& q, uint2 w) {
-  const float f0 = __uint_as_float((w.x & 0x1FFFFFu) | 0x4B000000u);
+  // The kernel is ALU-pipe bound, so q0 and q2 are extracted on the FMA pipe
+  // (IMAD / IMAD.HI) rather than with LOP3 / SHF: 17^3 tetrahedral +5 %.
+  uint32_t t0;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(t0) : "r"(w.x), "r"(1u << 11));       // q0 to the top bits
+  const float f0 = __uint_as_float(mad_hi_u32(t0, 1u << 21, 0x4B000000u));
+  // (q1 on the FMA pipe as well -- three IMADs -- measured within +-1 %: kept on the ALU)
   const float f1 = __uint_as_float((__funnelshift_r(w.x, w.y, 21) & 0x1FFFFFu) | 0x4B000000u);
   const float f2 = __uint_as_float(mad_hi_u32(w.y, 1u << 22, 0x4B000000u));   // (w.y >> 10) + 2^23 bits
   Node2 n;
