@@ -160,14 +160,37 @@ struct OpLut {
   // fp32 planes.  The choice is made per CTA from the lattice itself, by the
   // same deterministic arithmetic in every CTA.
   static constexpr bool PACK = SMEM && !PRIV;
+  // 17^3 is staged with one ghost plane per axis (18^3 nodes, copies of the
+  // edge nodes), so cell location needs no clamp: p = 255 lands in cell 16 at
+  // offset 0, where the ghost nodes carry weight exactly 0 -- the same point
+  // of the interpolant as cell 15 at offset 255 for the schemes that are
+  // continuous across cells (trilinear, prism, tetrahedral).  base = x / 255 for
+  // x = 16 p <= 4080 is one IMAD.HI with the shift-free magic 0x01010102
+  // (exact on that range), so locating is FMA-pipe work in an ALU-bound kernel.
+  static constexpr int NG = PACK ? N + 1 : N;
+  static constexpr int NNG = NG * NG * NG;
+  static_assert(!PACK || N == 17, "shift-free /255 is exact for 16 p <= 4080 only");
+  static __device__ __forceinline__ void locate_g(uint32_t r, uint32_t g, uint32_t b, int& bf, int& rr,
+                                                  int& rg, int& rb) {
+    const uint32_t xr = r * (N - 1), xg = g * (N - 1), xb = b * (N - 1);
+    uint32_t br = __umulhi(xr, 0x01010102u), bg = __umulhi(xg, 0x01010102u), bb = __umulhi(xb, 0x01010102u);
+    if constexpr (METHOD == MACT_LUT_PYRAMIDAL) {
+      // the pyramid scheme is not continuous across cells (its far faces are
+      // triangulated, its near faces bilinear), so p = 255 keeps the
+      // reference's cell N-2 at offset 255 (lut.py:98-105)
+      br = min(br, (uint32_t)(N - 2)); bg = min(bg, (uint32_t)(N - 2)); bb = min(bb, (uint32_t)(N - 2));
+    }
+    rr = (int)(xr - 255u * br); rg = (int)(xg - 255u * bg); rb = (int)(xb - 255u * bb);
+    bf = (int)(br * (NG * NG) + bg * NG + bb);
+  }
   struct Shared {
     float4 lat[PRIV ? 8 * N * N * N : 1];
     union {
       struct {
-        float2 c01[PACK ? N * N * N : 1];
-        float c2[PACK ? N * N * N : 1];
+        float2 c01[PACK ? NNG : 1];
+        float c2[PACK ? NNG : 1];
       } f;
-      uint2 pk[PACK ? N * N * N : 1];
+      uint2 pk[PACK ? NNG : 1];
     } u;
     LutQuant q;
     float red[32][6];
@@ -178,8 +201,9 @@ struct OpLut {
     } else if constexpr (PACK) {
       lut_quant_setup(p.lat, N * N * N, &s->q, s->red);   // ends with __syncthreads
       const LutQuant q = s->q;
-      for (int i = threadIdx.x; i < N * N * N; i += blockDim.x) {
-        const float4 v = __ldg(p.lat + i);
+      for (int i = threadIdx.x; i < NNG; i += blockDim.x) {   // ghost nodes copy the edge
+        const int ir = min(i / (NG * NG), N - 1), ig = min((i / NG) % NG, N - 1), ib = min(i % NG, N - 1);
+        const float4 v = __ldg(p.lat + (ir * N + ig) * N + ib);
         if (q.on) {
           s->u.pk[i] = lut_quant_pack(q, v);
         } else {
@@ -221,7 +245,13 @@ struct OpLut {
     constexpr int K = LutK<METHOD>::K;
     int idx[K];
     float w[K];
-    lut_nodes<N, METHOD, float, false>(r, g, b, idx, w);
+    if constexpr (PACK) {
+      int bf, rr, rg, rb;
+      locate_g(r, g, b, bf, rr, rg, rb);
+      lut_nodes_at<NG, METHOD, float, false>(bf, rr, rg, rb, idx, w);
+    } else {
+      lut_nodes<N, METHOD, float, false>(r, g, b, idx, w);
+    }
     const LutQuant q = quant(s);
     auto nd = [&](int i) { return q.on ? node<true>(s, p, i, lane, q) : node<false>(s, p, i, lane, q); };
     Node2 v = nd(idx[0]);
@@ -267,8 +297,16 @@ struct OpLut {
       float w[PB][K];
       Node2 v[PB][K];
 #pragma unroll
-      for (int q = 0; q < PB; ++q)
-        lut_nodes<N, METHOD, float, false>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], idx[q], w[q]);
+      for (int q = 0; q < PB; ++q) {
+        if constexpr (PACK) {
+          int bf, rr, rg, rb;
+          locate_g(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], bf, rr, rg, rb);
+          lut_nodes_at<NG, METHOD, float, false>(bf, rr, rg, rb, idx[q], w[q]);
+        } else {
+          lut_nodes<N, METHOD, float, false>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2],
+                                             idx[q], w[q]);
+        }
+      }
 #pragma unroll
       for (int q = 0; q < PB; ++q)
 #pragma unroll

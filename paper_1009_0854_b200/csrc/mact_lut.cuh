@@ -41,16 +41,14 @@ __device__ __forceinline__ void lut_locate(uint32_t p, int& base, int& rem) {
 // integers; under ties the zero-weight middle node may be a different corner
 // of the cell, which leaves every sum bit-identical (fmaf(0, v, a) == a).
 // mact_lut_nodes reports the reference's indices and keeps TIES = true.
+// lut_nodes_at: the same from the located cell (bf = flat index of its base
+// corner in a lattice of N nodes per axis, rr/rg/rb = the integer offsets);
+// lut_nodes locates first.
 template <int N, int METHOD, typename W = float, bool TIES = true>
-__device__ __forceinline__ void lut_nodes(uint32_t pr, uint32_t pg, uint32_t pb,
-                                          int (&idx)[LutK<METHOD>::K],
-                                          W (&w)[LutK<METHOD>::K]) {
+__device__ __forceinline__ void lut_nodes_at(int bf, int rr, int rg, int rb,
+                                             int (&idx)[LutK<METHOD>::K],
+                                             W (&w)[LutK<METHOD>::K]) {
   constexpr int SR = N * N, SG = N, SB = 1;
-  int br, bg, bb, rr, rg, rb;
-  lut_locate<N>(pr, br, rr);
-  lut_locate<N>(pg, bg, rg);
-  lut_locate<N>(pb, bb, rb);
-  const int bf = (br * N + bg) * N + bb;
   const W fr = (W)rr, fg = (W)rg, fb = (W)rb;
   constexpr W inv1 = (W)(1.0 / 255.0);
   constexpr W inv2 = (W)(1.0 / (255.0 * 255.0));
@@ -114,6 +112,17 @@ __device__ __forceinline__ void lut_nodes(uint32_t pr, uint32_t pg, uint32_t pb,
     w[2] = (W)(d2 - d3) * inv1;
     w[3] = (W)d3 * inv1;
   }
+}
+
+template <int N, int METHOD, typename W = float, bool TIES = true>
+__device__ __forceinline__ void lut_nodes(uint32_t pr, uint32_t pg, uint32_t pb,
+                                          int (&idx)[LutK<METHOD>::K],
+                                          W (&w)[LutK<METHOD>::K]) {
+  int br, bg, bb, rr, rg, rb;
+  lut_locate<N>(pr, br, rr);
+  lut_locate<N>(pg, bg, rg);
+  lut_locate<N>(pb, bb, rb);
+  lut_nodes_at<N, METHOD, W, TIES>((br * N + bg) * N + bb, rr, rg, rb, idx, w);
 }
 
 // Real-valued pixels (lut.py:98-105 and :115-199 in fp64, the reference's
