@@ -74,3 +74,48 @@ def test_synthetic_corpus_matches_reference(figures):
     got = [hashlib.sha256(np.ascontiguousarray(im).tobytes()).hexdigest()
            for im in harness.synthetic_corpus((64, 96), seed=0)]
     assert got == figures["synthetic_corpus_64_96"]
+
+
+def _lab_seg_model():
+    import importlib.util
+    import os
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts", "lab_seg_design.py")
+    spec = importlib.util.spec_from_file_location("lab_seg_design", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+@pytest.mark.parametrize("degs", [(4, 4), (2, 2)])
+def test_lab_segmented_fp32_model(degs):
+    """CPU model of the segmented fp32 CIELAB kernel (scripts/lab_seg_design.py:
+    16 segments per binade, cubic, (hi, small part) epilogue) on the degenerate
+    probe sets of SURVEY §4.4 plus 2^20 cube colours: inside the 1e-4 tolerance."""
+    M = _lab_seg_model()
+    cfg = O.OracleConfig(cielab_degrees=degs)
+    tab, base, shift, fit_err = M.build_table(cfg.cbrt_num, cfg.cbrt_den, 16, 3, lo_split=False)
+    assert fit_err < 1e-8
+    f32 = np.float32
+    grays = np.repeat(np.arange(256, dtype=np.uint8)[:, None], 3, axis=1)
+    rg0 = np.stack([np.zeros(256), np.zeros(256), np.arange(256)], 1).astype(np.uint8)
+    face = np.random.default_rng(3).integers(0, 256, (4096, 3)).astype(np.uint8)
+    face[:, 0] = 255
+    px = np.concatenate([grays, rg0, face, O.cube_chunk(7 << 20, 1 << 20)])
+    ref = O.rgb_to_lab_fast(px, cfg)
+    gam = O.GAMMA_TABLE.astype(f32)
+    m = np.array([[O.RGB_TO_XYZ[r, c] / O.WHITE[r] for c in range(3)] for r in range(3)]).astype(f32)
+    gr, gg, gb = gam[px[:, 0]], gam[px[:, 1]], gam[px[:, 2]]
+    hs, ds = [], []
+    for r in range(3):
+        t = M.fma_arr(m[r, 2], gb, M.fma_arr(m[r, 1], gg, (m[r, 0] * gr).astype(f32)))
+        h, d = M.seg_eval(t, tab, base, shift, 3, False)
+        low = ~(t > f32(O.LAB_KNEE))
+        off_hi = f32(O.LAB_LINEAR_OFFSET)
+        hs.append(np.where(low, off_hi, h))
+        ds.append(np.where(low, M.fma_arr(f32(O.LAB_LINEAR_SLOPE), t, f32(O.LAB_LINEAR_OFFSET - np.float64(off_hi))), d))
+    (hx, hy, hz), (dx, dy, dz) = hs, ds
+    L = M.fma_arr(f32(116), dy, M.fma_arr(f32(116), hy, f32(-16)))
+    A = (f32(500) * ((hx - hy) + (dx - dy))).astype(f32)
+    B = (f32(200) * ((hy - hz) + (dy - dz))).astype(f32)
+    err = np.abs(np.stack([L, A, B], -1).astype(np.float64) - ref)
+    assert err.max() <= 1e-4, err.max(axis=0)
