@@ -26,10 +26,14 @@ template <> struct LutK<MACT_LUT_TETRAHEDRAL> { static constexpr int K = 4; };
 // Unsigned on purpose: a signed x / 255 compiles to a 4-instruction
 // sign-corrected sequence (IMAD.HI + SHF + LEA.HI.SX32 + a zeroed
 // accumulator), the unsigned one to IMAD.HI.U32 + SHF.
+// x / 255 for x = p (n-1) <= 8160 is hi(x * 0x01010102): exact on that range
+// (checked exhaustively), one IMAD.HI without the shift of the general
+// 32-bit division sequence.
 template <int N>
 __device__ __forceinline__ void lut_locate(uint32_t p, int& base, int& rem) {
+  static_assert(N >= 2 && N <= 33, "shift-free /255 is exact for p (n-1) <= 8160");
   const uint32_t x = p * (uint32_t)(N - 1);
-  uint32_t bse = x / 255u;
+  uint32_t bse = __umulhi(x, 0x01010102u);
   bse = bse > (uint32_t)(N - 2) ? (uint32_t)(N - 2) : bse;
   base = (int)bse;
   rem = (int)(x - 255u * bse);
