@@ -119,3 +119,10 @@ def test_lab_segmented_fp32_model(degs):
     B = (f32(200) * ((hy - hz) + (dy - dz))).astype(f32)
     err = np.abs(np.stack([L, A, B], -1).astype(np.float64) - ref)
     assert err.max() <= 1e-4, err.max(axis=0)
+
+
+def test_shift_free_div255_magic():
+    """lut_locate / the 17^3 ghost-plane locate divide x = p (n-1) by 255 as
+    hi(x * 0x01010102) (csrc/mact_lut.cuh): exact for every x <= 8160 (33^3)."""
+    x = np.arange(0, 8161, dtype=np.uint64)
+    assert np.array_equal((x * np.uint64(0x01010102)) >> np.uint64(32), x // np.uint64(255))
