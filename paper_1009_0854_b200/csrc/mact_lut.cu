@@ -622,10 +622,11 @@ __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
 }
 
 // Planar output (3, N) needs no exchange at all: component c of a step is a
-// contiguous 16 KB run of plane c.  Independent CTAs (no cluster), CTA b holds
+// contiguous 16 KB run of plane c.  STRIDED: the same CTAs write interleaved
+// (N, 3) output directly, component c of pixel i at 3 i + c.  Independent CTAs (no cluster), CTA b holds
 // component b % 3 and streams steps b / 3, b / 3 + G/3, ...; the two warp
 // groups alternate steps and each drains its staging plane with one bulk store.
-template <int METHOD>
+template <int METHOD, bool STRIDED = false>
 __global__ void __launch_bounds__(kLut33Threads, 1)
     k_lut33_planar(const float4* __restrict__ lat4, const uint8_t* __restrict__ rgb,
                    float* __restrict__ out, int64_t n, int64_t nsteps) {
@@ -672,10 +673,16 @@ __global__ void __launch_bounds__(kLut33Threads, 1)
           for (int j = 1; j < K; ++j) a[q0 + q] = fmaf(w[q][j], v[q][j], a[q0 + q]);
         }
       }
+      if constexpr (STRIDED) {   // interleaved (N, 3) output: this CTA's component of 4 pixels
+        float* d = out + 3 * (4 * g) + comp;
+        d[0] = a[0]; d[3] = a[1]; d[6] = a[2]; d[9] = a[3];
+        continue;
+      }
       if (h == 0 && tg == 0) bulk_wait_read<0>();       // this group's previous plane run drained
       if (h == 0) asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(512) : "memory");
       *reinterpret_cast<float4*>(sg + 4 * (h * 512 + tg)) = make_float4(a[0], a[1], a[2], a[3]);
     }
+    if constexpr (STRIDED) continue;
     fence_proxy_async_smem();
     asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(512) : "memory");
     if (tg == 0) {
@@ -694,9 +701,14 @@ static int launch_lut33_comp(const float* lat, const uint8_t* rgb, float* out, i
   const bool aligned = (uintptr_t)rgb % 16 == 0 && (uintptr_t)out % 16 == 0;
   const bool ok = !planar && aligned;
   const int64_t nsteps = aligned && (!planar || n % 4 == 0) ? n / kLut33Step : 0;
-  if (planar && nsteps > 0) {   // planar: independent component CTAs, no exchange
+  // Interleaved trilinear: independent component CTAs writing their component
+  // of every pixel with stride-12 B stores (L2 merges the three components)
+  // beat the cluster exchange (82 vs 74 Gpix/s); the simplex methods, whose
+  // cluster kernel is faster, keep it (strided: 62-71 vs 86-101).
+  constexpr bool kStrided = METHOD == MACT_LUT_TRILINEAR;
+  if ((planar || kStrided) && nsteps > 0) {   // planar: independent component CTAs, no exchange
     constexpr size_t psmem = (((33 * 33 * 33) + 31) / 32 * 32 + 2 * kLut33Step) * sizeof(float);
-    auto pfn = k_lut33_planar<METHOD>;
+    auto pfn = planar ? k_lut33_planar<METHOD, false> : k_lut33_planar<METHOD, true>;
     const int64_t cap = persistent_grid((const void*)pfn, kLut33Threads, psmem);
     if (cap <= 0) return MACT_ECUDA;
     int64_t groups = cap / 3;
