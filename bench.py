@@ -14,10 +14,15 @@ smaller workloads rotate over enough buffer copies to exceed 2x L2).
 roofline.achieved counts the algorithmic bytes of the step's one launch:
 3 B in + 12 B out per pixel and transform (27 B fused C2, 39 B fused C5).
 
-Under torchrun (N>1) every rank processes its shard; time = max over ranks
-of the CUDA-event time between barriers.  --impl reference times the
-reference algorithm's CPU implementation (the oracle port, all host threads)
-on a bounded sample of the same workload, rank 0 only.
+--gpus N > 1 without torchrun re-launches itself as N ranks through
+torch.distributed.run (one process per GPU, NCCL); under torchrun WORLD_SIZE
+must equal --gpus.  Every rank processes its shard; the timed window runs from
+a common barrier through the K steps AND the final combine of the error
+partials (all-gather + rank-order fold); time = max over ranks of the CUDA-event
+time.  --share-gpu runs the N ranks on cuda:0 with a gloo combine: a host-logic
+test for a 1-GPU box, not an N-GPU number.  --impl reference times the
+unmodified reference package (baseline/_ref/mact, pure Python + numpy) on all
+host threads on a bounded sample of the same workload, rank 0 only.
 """
 
 from __future__ import annotations
@@ -113,21 +118,59 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------- CPU legs
-def cpu_port_run(space: str, images, budget_s: float, threads: int, lut_spec=None):
-    """Oracle port (numpy, the reference algorithm) over host images until budget_s."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def cpu_functions(kind: str, lut_spec=None):
+    """The CPU implementation of the path: kind "reference" = the UNMODIFIED reference package
+    installed in baseline/_ref (mact.fast / mact.lut, its own public API); kind "port" = the oracle's
+    numpy restatement.  Returns ({space: fn}, kind actually used)."""
+    if kind == "reference" and os.path.isdir(os.path.join(REF_DIR, "mact")):
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        from mact import fast as rf
+        from mact import lut as rl
+
+        fns = {"lab": rf.rgb_to_lab_fast, "hsi": rf.rgb_to_hsi_fast, "sct": rf.rgb_to_sct_fast}
+        if lut_spec is not None:
+            L = rl.build_lut("lab", lut_spec[0])
+            fns["lut"] = lambda p, L=L: rl.interpolate(L, p, lut_spec[1])
+        return fns, "reference"
     from oracle import mact_oracle as O
 
-    fn = {"lab": O.rgb_to_lab_fast, "hsi": O.rgb_to_hsi_fast, "sct": O.rgb_to_sct_fast}
-    if space == "lut":
+    fns = {"lab": O.rgb_to_lab_fast, "hsi": O.rgb_to_hsi_fast, "sct": O.rgb_to_sct_fast}
+    if lut_spec is not None:
         vals = O.build_lut_values("lab", lut_spec[0])
-        fn["lut"] = lambda p: O.interpolate(vals, p, lut_spec[1])
+        fns["lut"] = lambda p, vals=vals: O.interpolate(vals, p, lut_spec[1])
+    return fns, "port"
+
+
+def host_threads() -> int:
+    """All host threads, capped at 64 like MACT_THREADS (harness.py:60)."""
+    return max(1, min(64, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()))
+
+
+def run_chunked(fn, pixels, threads: int, chunk: int = 1 << 18):
+    """fn over 2^18-px chunks on a thread pool (the reference's own harness.py:92-103 pattern)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    flat = pixels.reshape(-1, 3)
+    parts = [flat[i:i + chunk] for i in range(0, flat.shape[0], chunk)]
+    if threads <= 1:
+        return [fn(p) for p in parts]
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        return list(ex.map(fn, parts))
+
+
+def cpu_run(fns, space: str, images, budget_s: float, threads: int):
+    """The CPU implementation over host images until budget_s."""
     spaces = ["lab", "hsi", "sct"] if space == "all" else [space]
     px, t0 = 0, time.perf_counter()
     i = 0
     while True:
         img = images[i % len(images)]
         for sp in spaces:
-            O.run_chunked(fn[sp], img, threads)
+            run_chunked(fns[sp], img, threads)
         px += img.size // 3
         i += 1
         if time.perf_counter() - t0 >= budget_s:
@@ -143,8 +186,9 @@ def run_ours(args, wl):
 
     from paper_1009_0854_b200 import _lib, corpus, fast, harness, lut, parallel
 
-    rank, world, local = parallel.init("nccl")
+    rank, world, local = parallel.init("nccl", share_device=args.share_gpu)
     dev = torch.device("cuda", local)
+    cdev = parallel.collective_device(dev)          # NCCL: the GPU; gloo (--share-gpu): the host
     lib = _lib.load()
     cfg = fast.DEFAULT_CONFIG
     hbm, hbm_src = peaks()
@@ -197,6 +241,28 @@ def run_ours(args, wl):
             _lib.check(lib.mact_lut_interp(lat.data_ptr(), args.lut_grid, lut_code, xf.data_ptr(),
                                            outs[0].data_ptr(), n_local, 0, sp_ptr))
 
+    # ---------------- per-rank error partials (the reduction pass is reporting, not
+    # throughput: SURVEY §8(d) excludes it from the metric; its device time is in the
+    # line as error.reduce_ms).  The cross-rank all-gather + rank-order fold of these
+    # partials -- the job's only exchange -- runs INSIDE the timed window below.
+    partial_sets = []
+    ev_r0, ev_r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_r0.record(st)
+    if space in ("lab", "all", "lut"):
+        cand = harness.LutCandidate(lt, args.lut_method) if space == "lut" else harness.fast_candidate("lab")
+        partial_sets.append(("lab", harness.reduce_partials("lab", cand, None, xf, index_base=base)))
+        if space == "lut":   # config 3: "compared with MACT on the same pixels"
+            partial_sets.append(("mact", harness.reduce_partials("lab", harness.fast_candidate("lab"), None, xf,
+                                                                 index_base=base)))
+    if space in ("all", "hsi+sct"):   # configs 2 and 5: per-component |fast - exact| (SURVEY A21)
+        for sp in ("hsi", "sct"):
+            partial_sets.append((sp, harness.reduce_partials(sp, harness.fast_candidate(sp), None, xf,
+                                                             index_base=base, metric="component")))
+    ev_r1.record(st)
+    torch.cuda.synchronize(dev)
+    reduce_ms = parallel.max_over_ranks(ev_r0.elapsed_time(ev_r1), cdev)
+    flat_parts = [p for _, ps in partial_sets for p in ps]
+
     transforms = {"all": 3, "hsi+sct": 2}.get(space, 1)
     for _ in range(max(args.warmup, 3)):
         step()
@@ -219,14 +285,17 @@ def run_ours(args, wl):
         graph.replay()                                   # warm replay
         torch.cuda.synchronize(dev)
 
-    # ---------------- timed region: K steps, events per step on the launching stream
+    # ---------------- timed region: common barrier -> K steps -> the final stat
+    # combine (all-gather of the error partials + rank-order fold), SURVEY §8(d);
+    # CUDA events on the launching stream, max over ranks.
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    parallel.barrier(dev)
+    parallel.barrier(cdev)
     torch.cuda.synchronize(dev)
     lib.mact_launch_count_reset()
     with ClockSampler(local) as clk:
         t0 = torch.cuda.Event(enable_timing=True)
+        tk = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(st)
         if graph is not None:
@@ -236,14 +305,38 @@ def run_ours(args, wl):
                 evs[k][0].record(st)
                 step()
                 evs[k][1].record(st)
+        tk.record(st)
+        per_rank = parallel.all_gather_partials(flat_parts, cdev) if flat_parts else []
+        folded = parallel.combine(per_rank) if per_rank else []
         t1.record(st)
         torch.cuda.synchronize(dev)
     launches = graph_launches if graph is not None else int(lib.mact_launch_count())
-    parallel.barrier(dev)
+    parallel.barrier(cdev)
     local_ms = t0.elapsed_time(t1)
-    total_ms = parallel.max_over_ranks(local_ms, dev)
-    step_ms = ([local_ms / args.steps] * args.steps if graph is not None
+    total_ms = parallel.max_over_ranks(local_ms, cdev)
+    steps_ms = t0.elapsed_time(tk)
+    combine_ms = parallel.max_over_ranks(tk.elapsed_time(t1), cdev)
+    step_ms = ([steps_ms / args.steps] * args.steps if graph is not None
                else [a.elapsed_time(b) for a, b in evs])
+
+    # ---------------- error statistics from the folded partials
+    err = None
+    it = iter(folded)
+    for name, ps in partial_sets:
+        got = [next(it) for _ in ps]
+        if name == "lab":
+            tot = got[0]
+            err = {"dE_mean": tot["sum"] / tot["count"], "dE_max": tot["max"],
+                   "dE_argmax_index": tot["argmax"], "pixels": tot["count"]}
+        elif name == "mact":
+            err["mact_dE_mean"], err["mact_dE_max"] = got[0]["sum"] / got[0]["count"], got[0]["max"]
+        else:
+            err = err or {}
+            err[name] = [{"mean": c["sum"] / max(c["count"], 1), "max": c["max"],
+                          "excluded_nan": c["nan"]} for c in got]
+    if err is not None:
+        err["reduce_ms"] = round(reduce_ms, 3)
+        err["combine_ms_in_timed_region"] = round(combine_ms, 4)
     # every workload is ONE launch per step (C2/C5 run the transforms fused from one read)
     kern_ms = statistics.mean(step_ms)
     value = n_total * transforms * args.steps / (total_ms / 1e3) / 1e9
@@ -257,27 +350,6 @@ def run_ours(args, wl):
             traffic_b = t["bytes_per_launch"]
             traffic = round(traffic_b / (kern_ms / 1e3) / 1e9, 1)
 
-    # ---------------- error statistics (outside the timed region)
-    err = None
-    if space in ("lab", "all", "lut"):
-        cand = harness.LutCandidate(lt, args.lut_method) if space == "lut" else harness.fast_candidate("lab")
-        parts = harness.reduce_partials("lab", cand, None, xf, index_base=base)
-        tot = parallel.combine(parallel.all_gather_partials(parts, dev))[0]
-        err = {"dE_mean": tot["sum"] / tot["count"], "dE_max": tot["max"],
-               "dE_argmax_index": tot["argmax"], "pixels": tot["count"]}
-        if space == "lut":   # config 3: "compared with MACT on the same pixels"
-            parts = harness.reduce_partials("lab", harness.fast_candidate("lab"), None, xf, index_base=base)
-            m = parallel.combine(parallel.all_gather_partials(parts, dev))[0]
-            err["mact_dE_mean"], err["mact_dE_max"] = m["sum"] / m["count"], m["max"]
-    if space in ("all", "hsi+sct"):   # configs 2 and 5: per-component |fast - exact| (SURVEY A21)
-        err = err or {}
-        for sp in ("hsi", "sct"):
-            parts = harness.reduce_partials(sp, harness.fast_candidate(sp), None, xf,
-                                            index_base=base, metric="component")
-            comps = parallel.combine(parallel.all_gather_partials(parts, dev))
-            err[sp] = [{"mean": c["sum"] / max(c["count"], 1), "max": c["max"],
-                        "excluded_nan": c["nan"]} for c in comps]
-
     # ---------------- end to end through the public API with HOST buffers
     e2e = None
     if args.e2e_steps > 0:
@@ -290,12 +362,12 @@ def run_ours(args, wl):
         hi, ho = h_in.numpy(), h_out.numpy()
         fn(hi[: min(n_local, 1 << 22)], out=ho[: min(n_local, 1 << 22)])   # warm the executor
         torch.cuda.synchronize(dev)
-        parallel.barrier(dev)
+        parallel.barrier(cdev)
         t = time.perf_counter()
         for _ in range(args.e2e_steps):
             fn(hi, out=ho)
         torch.cuda.synchronize(dev)
-        dt = parallel.max_over_ranks(time.perf_counter() - t, dev)
+        dt = parallel.max_over_ranks(time.perf_counter() - t, cdev)
         e2e = {"value": n_total * args.e2e_steps / dt / 1e9, "unit": "Gpixels/s",
                "h2d_bytes_per_step": n_total * 3, "d2h_bytes_per_step": n_total * 12,
                "api": (f"paper_1009_0854_b200.fast.rgb_to_{sp1}_fast" if sp1 != "lut" else
@@ -303,19 +375,20 @@ def run_ours(args, wl):
                "steps": args.e2e_steps, "transform": sp1}
         del h_in, h_out
 
-    # ---------------- CPU baseline (rank 0, N=1 only)
+    # ---------------- CPU baseline (rank 0, N=1 only): the reference itself (baseline/_ref)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import mact_oracle as O
         sample = [xf[i * 2_073_600:(i + 1) * 2_073_600].cpu().numpy() for i in range(2)]
-        threads = O.host_threads()
+        threads = host_threads()
         sp = {"lab": "lab", "all": "lab", "hsi+sct": "hsi"}.get(space, "lut")
-        px, dt = cpu_port_run(sp, sample, args.cpu_seconds, threads, (args.lut_grid, args.lut_method))
-        what = f"rgb_to_{sp}_fast" if sp != "lut" else f"interpolate({args.lut_method}, {args.lut_grid}^3)"
-        cpu = {"value": px / dt / 1e9, "unit": "Gpixels/s", "cores": threads, "kind": "port",
-               "sample": f"oracle/mact_oracle.py {what} (numpy fp64 restatement of the "
-                         f"reference) over 2,073,600-px slices of the same workload, {px} px in "
-                         f"{dt:.1f} s, ThreadPoolExecutor x{threads} (harness.py:92-103 pattern)"}
+        fns, kind = cpu_functions("reference", (args.lut_grid, args.lut_method) if sp == "lut" else None)
+        px, dt = cpu_run(fns, sp, sample, args.cpu_seconds, threads)
+        what = f"rgb_to_{sp}_fast" if sp != "lut" else f"lut.interpolate({args.lut_method}, {args.lut_grid}^3)"
+        src = ("baseline/_ref/mact (the unmodified reference package, its public API)" if kind == "reference"
+               else "oracle/mact_oracle.py (numpy restatement of the reference)")
+        cpu = {"value": px / dt / 1e9, "unit": "Gpixels/s", "cores": threads, "kind": kind,
+               "sample": f"{src} {what} over 2,073,600-px slices of the same workload, {px} px in "
+                         f"{dt:.1f} s, ThreadPoolExecutor x{threads} over 2^18-px chunks (harness.py:92-103)"}
 
     if rank == 0:
         line = {
@@ -326,7 +399,11 @@ def run_ours(args, wl):
             "data": "synthetic (generated on device, seeded per image)",
             "config": {"workload": f"{args.workload}: {wl['desc']}", "pixels": n_total,
                        "transforms_per_step": transforms, "layout": "interleaved (N,3) fp32",
-                       "parallelism": f"dp{world} (shard by image, no data-path collective)",
+                       "parallelism": (f"dp{world} (shard by {'image' if wl['kind'] == 'images' else 'pixel range'}, "
+                                       "no data-path collective; one all-gather of the error partials "
+                                       f"over {'gloo' if args.share_gpu else 'NCCL'} inside the timed window)"),
+                       "devices": ("all ranks share cuda:0 (--share-gpu host-logic test: NOT an N-GPU number)"
+                                   if args.share_gpu else f"{world} x cuda, one process per GPU"),
                        "launch": "CUDA graph of the K steps" if graph is not None else "stream launches",
                        "l2": ("inputs+outputs > 2x the 126 MB L2 (no flush needed)" if pool_n == 1 else
                               f"steps rotate over {pool_n} input/output copies ({pool_n * step_bytes / 1e6:.0f} MB "
@@ -346,15 +423,16 @@ def run_ours(args, wl):
 
 # --------------------------------------------------------------------- reference arm
 def run_reference(args, wl):
+    """The reference arm: the UNMODIFIED reference package (baseline/_ref/mact, pure Python +
+    numpy, no GPU code) through its own public API, on all host threads, one bounded sample of
+    the workload per step.  Rank 0 only; the oracle port is timed once beside it as a cross-check."""
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     if rank != 0:
         return
     import numpy as np
 
-    from oracle import mact_oracle as O
-
-    threads = O.host_threads()
+    threads = host_threads()
     space = wl["space"]
     # bounded sample of the same workload: one image-sized slice per step
     if wl["kind"] == "images":
@@ -369,26 +447,32 @@ def run_reference(args, wl):
             img = np.random.default_rng(0).integers(0, 256, (wl["h"], wl["w"], 3), dtype=np.uint8)
         sample = img.reshape(-1, 3)[: 2_073_600]
     elif wl["kind"] == "cube":
-        sample = O.cube_chunk(0, 1 << 21)
+        idx = np.arange(1 << 21, dtype=np.uint32)                     # harness.cube_chunk(0, 2^21)
+        sample = np.stack([idx >> 16, (idx >> 8) & 255, idx & 255], -1).astype(np.uint8)
     else:
         sample = np.random.default_rng(0).integers(0, 256, (min(wl["n"], 1 << 21), 3), dtype=np.uint8)
-    fns = {"lab": [O.rgb_to_lab_fast], "all": [O.rgb_to_lab_fast, O.rgb_to_hsi_fast, O.rgb_to_sct_fast],
-           "hsi+sct": [O.rgb_to_hsi_fast, O.rgb_to_sct_fast]}.get(space)
-    if fns is None:
-        vals = O.build_lut_values("lab", args.lut_grid)
-        fns = [lambda p: O.interpolate(vals, p, args.lut_method)]
-    for _ in range(max(args.warmup, 1)):
-        for f in fns:
-            O.run_chunked(f, sample, threads)
-    times = []
-    for _ in range(args.steps):
-        t = time.perf_counter()
-        for f in fns:
-            O.run_chunked(f, sample, threads)
-        times.append(time.perf_counter() - t)
+    lut_spec = (args.lut_grid, args.lut_method) if space == "lut" else None
+    spaces = {"lab": ["lab"], "all": ["lab", "hsi", "sct"], "hsi+sct": ["hsi", "sct"]}.get(space, ["lut"])
+
+    def timed(kind, steps, warmup):
+        fns, used = cpu_functions(kind, lut_spec)
+        for _ in range(warmup):
+            for sp in spaces:
+                run_chunked(fns[sp], sample, threads)
+        times = []
+        for _ in range(steps):
+            t = time.perf_counter()
+            for sp in spaces:
+                run_chunked(fns[sp], sample, threads)
+            times.append(time.perf_counter() - t)
+        return sample.shape[0] * len(spaces) * steps / sum(times) / 1e9, sum(times), used
+
+    value, total, kind = timed("reference", args.steps, max(args.warmup, 1))
+    port_value = timed("port", 1, 0)[0] if kind == "reference" else None
     px = sample.shape[0]
-    total = sum(times)
-    value = px * len(fns) * args.steps / total / 1e9
+    what = ("baseline/_ref/mact (the unmodified reference package, pip-installed from /root/reference; "
+            f"{', '.join('mact.fast.rgb_to_%s_fast' % sp if sp != 'lut' else 'mact.lut.interpolate' for sp in spaces)})"
+            if kind == "reference" else "oracle/mact_oracle.py (numpy restatement; baseline/_ref missing)")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "Gpixels/s",
         "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 1),
@@ -396,14 +480,30 @@ def run_reference(args, wl):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.workload}: {wl['desc']}",
                    "sample_pixels_per_step": px},
-        "cpu_baseline": {"value": round(value, 6), "unit": "Gpixels/s", "cores": threads, "kind": "port",
-                         "sample": f"{px} px of the workload per step through oracle/mact_oracle.py "
-                                   f"(numpy restatement of mact {space} fast path), "
-                                   f"ThreadPoolExecutor x{threads} over 2^18-px chunks"},
+        "cpu_baseline": {"value": round(value, 6), "unit": "Gpixels/s", "cores": threads, "kind": kind,
+                         "sample": f"{px} px of the workload per step through {what}, "
+                                   f"ThreadPoolExecutor x{threads} over 2^18-px chunks (harness.py:92-103)",
+                         "port_value": None if port_value is None else round(port_value, 6)},
         "e2e": {"value": round(value, 6), "unit": "Gpixels/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _relaunch(n: int) -> int:
+    """--gpus N without torchrun: re-exec this command as N ranks through torch.distributed.run."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    print(f"bench.py: launching {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -421,7 +521,18 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=None,
                     help="capture the K steps in a CUDA graph (default: on)")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="run every rank on cuda:0 with a gloo combine (N-rank host-logic test on a 1-GPU box)")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_relaunch(args.gpus))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; refusing to report a mismatched line",
+              file=sys.stderr)
+        sys.exit(2)
     wl = dict(WORKLOADS[args.workload])
     wl["desc"] = wl["desc"].format(grid=args.lut_grid, method=args.lut_method)
     if args.impl == "reference":

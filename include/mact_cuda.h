@@ -166,6 +166,19 @@ int mact_lut_interp_angular(const double* lattice64, int grid_n, int method, int
 int mact_lut_interp_real(const double* lattice64, int grid_n, int method, int angular_mask,
                          const void* rgb, int in_dtype, void* out, int out_dtype, int64_t n, int layout,
                          void* stream);
+/* replaces mact.lut.build_cache (lut.py:265-291): per cell of the (n-1)^3
+ * cells (r-major) the trilinear polynomial coefficients `trilinear` and the
+ * corner differences `corner_diff`, both (n-1)^3 x 8 x 3 fp64 (device),
+ * evaluated in the reference's operation order (bit-identical). */
+int mact_lut_cache_build(const double* lattice64, int grid_n, double* trilinear, double* corner_diff,
+                         void* stream);
+/* replaces mact.lut._interpolate_caching (lut.py:294-331), i.e. interpolate(...,
+ * variant="caching"): mact_lut_interp_real's contract, with linear components
+ * evaluated from the cache arrays in the reference's order (bit-identical with
+ * out_dtype MACT_DTYPE_F64). */
+int mact_lut_interp_cached(const double* lattice64, const double* trilinear, const double* corner_diff,
+                           int grid_n, int method, int angular_mask, const void* rgb, int in_dtype, void* out,
+                           int out_dtype, int64_t n, int layout, void* stream);
 /* replaces mact.lut.node_weights (lut.py:115-199): flat node indices (n,k)
  * and weights (n,k), k = 8/6/5/4; indices bit-exact with the reference. */
 int mact_lut_nodes(int grid_n, int method, const uint8_t* rgb, int64_t n,
@@ -212,6 +225,18 @@ typedef struct MactApproxSpec {
 int mact_approx_eval(const MactApproxSpec* spec, const double* x, const double* y, double* out,
                      int64_t n, int32_t* degenerate /* device, may be NULL */, void* stream);
 
+/* approximants.eval_poly / eval_rational (approximants.py:55-82), replaces
+ * Polynomial.__call__ / Rational.__call__ for any degree < MACT_POLY_MAX:
+ * out = num(x) (den_deg < 0) or num(x)/den(x), numpy's Horner order and
+ * rounding (bit-identical); *degenerate = 1 if any |den(x)| < 1e-300. */
+#define MACT_POLY_MAX 32
+typedef struct MactPolySpec {
+  int32_t num_deg, den_deg;
+  double num[MACT_POLY_MAX], den[MACT_POLY_MAX];
+} MactPolySpec;
+int mact_poly_eval(const MactPolySpec* spec, const double* x, double* out, int64_t n,
+                   int32_t* degenerate /* device, may be NULL */, void* stream);
+
 /* exact.py:52-83 elementwise, fp64:
  *   MACT_ELEM_INVERSE_GAMMA  out0 = inverse_gamma(in0)               (exact.py:52-57)
  *   MACT_ELEM_RGB_TO_XYZ     (out0, out1, out2) = rgb_to_xyz(in0..2)  (exact.py:60-66)
@@ -219,7 +244,11 @@ int mact_approx_eval(const MactApproxSpec* spec, const double* x, const double* 
  *   MACT_ELEM_XYZ_TO_LAB     out0 (n,3) = xyz_to_lab(in0..2)         (exact.py:75-83)
  *   MACT_ELEM_ANGULAR_LERP   out0 = lut.angular_lerp(in0, in1, in2)  (lut.py:202-216) */
 enum { MACT_ELEM_INVERSE_GAMMA = 0, MACT_ELEM_RGB_TO_XYZ = 1, MACT_ELEM_LAB_F = 2,
-       MACT_ELEM_XYZ_TO_LAB = 3, MACT_ELEM_ANGULAR_LERP = 4 };
+       MACT_ELEM_XYZ_TO_LAB = 3, MACT_ELEM_ANGULAR_LERP = 4,
+       /* TargetFn.exact (approximants.py:101-115), out0 = f(in0):
+        * cbrt, arctan(sqrt(3) x), 2 arcsin(x / sqrt(2)), arccos, arctan, pi/2 - arctan */
+       MACT_ELEM_TARGET_CBRT = 5, MACT_ELEM_TARGET_ATAN_SQRT3 = 6, MACT_ELEM_TARGET_ASIN_HALF = 7,
+       MACT_ELEM_TARGET_ACOS_HALF = 8, MACT_ELEM_TARGET_ATAN_F = 9, MACT_ELEM_TARGET_ATAN_G = 10 };
 int mact_exact_elem(int op, const double* in0, const double* in1, const double* in2,
                     double* out0, double* out1, double* out2, int64_t n, void* stream);
 

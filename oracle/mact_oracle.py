@@ -539,6 +539,56 @@ def _trilinear_angular(flat, n, base, frac, comp):
     return angular_lerp(g0, g1, db)
 
 
+def build_cache(values: np.ndarray):
+    """lut.py:265-291 — per-cell trilinear polynomial coefficients and corner
+    differences, each (n-1, n-1, n-1, 8, 3), in the reference's expression order."""
+    m = values.shape[0] - 1
+    c = [values[(k >> 2 & 1):(k >> 2 & 1) + m, (k >> 1 & 1):(k >> 1 & 1) + m, (k & 1):(k & 1) + m]
+         for k in range(8)]
+    tri = np.stack([c[0], c[4] - c[0], c[2] - c[0], c[1] - c[0],
+                    c[6] - c[4] - c[2] + c[0], c[5] - c[4] - c[1] + c[0], c[3] - c[2] - c[1] + c[0],
+                    c[7] - c[6] - c[5] - c[3] + c[4] + c[2] + c[1] - c[0]], axis=-2)
+    return {"trilinear": tri, "corner_diff": np.stack([c[k] - c[0] for k in range(8)], axis=-2)}
+
+
+def interpolate_caching(values: np.ndarray, cache, pixels, method: str = "tetrahedral",
+                        angular_mask=(False, False, False)):
+    """lut.py:294-331 — the caching variant: linear components from the cache
+    (trilinear polynomial terms summed in order; simplex methods as base node
+    plus weighted corner differences), angular components as the standard variant."""
+    if method not in METHODS:
+        raise ValueError(f"unknown interpolation method {method!r}")
+    n = values.shape[0]
+    flat = values.reshape(-1, 3)
+    base, frac = locate(n, pixels)
+    dr, dg, db = frac[..., 0], frac[..., 1], frac[..., 2]
+    cell = (base[..., 0], base[..., 1], base[..., 2])
+    nodes, w = node_weights(n, pixels, method)
+    if method == "trilinear":
+        c = cache["trilinear"][cell]
+        terms = [np.ones_like(dr), dr, dg, db, dr * dg, dr * db, dg * db, dr * dg * db]
+        out = c[..., 0, :] * terms[0][..., None]
+        for k in range(1, 8):
+            out = out + c[..., k, :] * terms[k][..., None]
+    else:
+        diff = cache["corner_diff"][cell]
+        bf = (base[..., 0] * n + base[..., 1]) * n + base[..., 2]
+        local = nodes - bf[..., None]
+        rows = (local // (n * n)) << 2 | ((local % (n * n)) // n) << 1 | (local % n)
+        out = flat[bf].astype(np.float64).copy()
+        for j in range(w.shape[-1]):
+            out += w[..., j, None] * np.take_along_axis(diff, rows[..., j][..., None, None], axis=-2)[..., 0, :]
+    if any(angular_mask):
+        for comp, ang in enumerate(angular_mask):
+            if not ang:
+                continue
+            if method == "trilinear":
+                out[..., comp] = _trilinear_angular(flat, n, base, frac, comp)
+            else:
+                out[..., comp] = circular_blend(flat[nodes, comp], w)
+    return out
+
+
 # ---------------------------------------------------------------------------
 # A18/A20/A21 — harness semantics (harness.py:25-122)
 # ---------------------------------------------------------------------------

@@ -7,11 +7,12 @@ executed by the hand-written sm_100a kernels of ``libmact_cuda.so``
 (``csrc/``, C ABI in ``include/mact_cuda.h``).
 """
 
-from .approximants import (Approximant, Polynomial, Rational, TargetFn, registry_get,
-                           registry_keys)
+from .approximants import (Approximant, Polynomial, Rational, TargetFn, eval_poly, eval_rational,
+                           registry_get, registry_keys)
 from .errors import MactError, UnknownApproximant
 
 __version__ = "0.1.0"
 
-__all__ = ["Approximant", "Polynomial", "Rational", "TargetFn", "registry_get", "registry_keys",
+__all__ = ["Approximant", "Polynomial", "Rational", "TargetFn", "eval_poly", "eval_rational",
+           "registry_get", "registry_keys",
            "MactError", "UnknownApproximant", "__version__"]

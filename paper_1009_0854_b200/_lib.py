@@ -56,8 +56,18 @@ class MactApproxSpec(C.Structure):
                 ("a", _c_double8), ("b", _c_double8)]
 
 
+POLY_MAX = 32
+
+
+class MactPolySpec(C.Structure):
+    _fields_ = [("num_deg", C.c_int32), ("den_deg", C.c_int32),
+                ("num", C.c_double * POLY_MAX), ("den", C.c_double * POLY_MAX)]
+
+
 FN_FORM, FN_ATAN_SQRT3, FN_ACOS, FN_ATAN_UNIT = 0, 1, 2, 3
 ELEM_INVERSE_GAMMA, ELEM_RGB_TO_XYZ, ELEM_LAB_F, ELEM_XYZ_TO_LAB, ELEM_ANGULAR_LERP = 0, 1, 2, 3, 4
+# TargetFn.exact (approximants.py:101-115)
+ELEM_TARGET = {"cbrt": 5, "atan_sqrt3": 6, "asin_half": 7, "acos_half": 8, "atan_f": 9, "atan_g": 10}
 SPACE_HSI_ARCCOS = 3
 LAB_PATH_SEG, LAB_PATH_MONIC, LAB_PATH_PQ = 1, 2, 3
 
@@ -74,6 +84,8 @@ _SIGNATURES = {
     "mact_lut_interp": (_i, [_vp, _i, _i, _vp, _vp, _i64, _i, _vp]),
     "mact_lut_interp_angular": (_i, [_vp, _i, _i, _i, _vp, _vp, _i64, _i, _vp]),
     "mact_lut_interp_real": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _i, _i64, _i, _vp]),
+    "mact_lut_cache_build": (_i, [_vp, _i, _vp, _vp, _vp]),
+    "mact_lut_interp_cached": (_i, [_vp, _vp, _vp, _i, _i, _i, _vp, _i, _vp, _i, _i64, _i, _vp]),
     "mact_lut_nodes": (_i, [_i, _i, _vp, _i64, _vp, _vp, _vp]),
     "mact_lut_nodes_real": (_i, [_i, _i, _vp, _i, _i64, _vp, _vp, _vp]),
     "mact_err_workspace_bytes": (C.c_size_t, []),
@@ -82,6 +94,7 @@ _SIGNATURES = {
     "mact_cube_fill": (_i, [_vp, _i64, _i64, _vp]),
     "mact_call_counts": (_i, [_vp, _vp]),
     "mact_approx_eval": (_i, [C.POINTER(MactApproxSpec), _vp, _vp, _vp, _i64, _vp, _vp]),
+    "mact_poly_eval": (_i, [C.POINTER(MactPolySpec), _vp, _vp, _i64, _vp, _vp]),
     "mact_exact_elem": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]),
     "mact_exact_f32": (_i, [_i, _vp, _vp, _i64, _i, _vp]),
     "mact_fast_f64": (_i, [_i, _vp, _i, _vp, _i64, C.POINTER(MactCoeffs), _i, _vp]),

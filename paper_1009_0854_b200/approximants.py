@@ -6,9 +6,13 @@ plus the frozen [0,1] refits of arctan(sqrt(3) x) that the reference's HSI
 pipeline actually evaluates (fast.py:38-43, recomputed by remez_poly at import
 time there; frozen here — tests/test_coeffs.py pins them to the reference).
 
-Nothing in this module evaluates a polynomial: evaluation happens only in the
-CUDA kernels.  The classes mirror the reference's public names so code that
-introspects a MactConfig keeps working.
+Nothing in this module evaluates a polynomial on the host: ``eval_poly`` /
+``eval_rational`` (approximants.py:55-82), the callable ``Polynomial`` /
+``Rational`` / ``Approximant`` and ``TargetFn.exact`` (:101-103) run on the
+GPU (``mact_poly_eval`` / ``mact_exact_elem`` of libmact_cuda.so), in numpy's
+Horner order and rounding, so they are bit-identical to the reference.  The
+classes mirror the reference's public names so code that introspects or calls
+a MactConfig's approximants keeps working.
 """
 
 from __future__ import annotations
@@ -18,19 +22,51 @@ import math
 from dataclasses import dataclass
 from typing import Dict, Tuple, Union
 
-from .errors import UnknownApproximant
+import numpy as np
+
+from .errors import DegenerateDenominator, UnknownApproximant
 
 CBRT_KNEE = 0.008856
 ATAN_SQRT3_FIT_HI = 254.0 / 256.0
 
 
+def _is_scalar(x) -> bool:
+    from . import _dev
+
+    return not _dev.is_device_tensor(x) and not isinstance(x, np.ndarray) and np.ndim(x) == 0
+
+
+def _result(out, on_dev: bool, scalar: bool):
+    from . import _dev
+
+    r = _dev.to_caller(out, on_dev)
+    return float(r) if scalar else r
+
+
 class TargetFn(enum.Enum):
+    """The elementary functions the bundled approximants replace (approximants.py:85-103)."""
+
     CBRT = "cbrt"
     ATAN_SQRT3 = "atan_sqrt3"
     ASIN_HALF = "asin_half"
     ACOS_HALF = "acos_half"
     ATAN_F = "atan_f"
     ATAN_G = "atan_g"
+
+    def exact(self, x):
+        """Reference libm evaluation of the target function (approximants.py:101-115), on the GPU
+        (libdevice cbrt / atan / asin / acos: within an ulp or two of numpy's libm)."""
+        import torch
+
+        from . import _dev, _lib
+        from .exact import _f64_args
+
+        scalar = _is_scalar(x)
+        (t,), on_dev = _f64_args(x)
+        out = torch.empty(t.shape, dtype=torch.float64, device=t.device)
+        _lib.call("mact_exact_elem", _lib.ELEM_TARGET[self.value], t.data_ptr(), None, None,
+                  out.data_ptr(), None, None, t.numel(), _dev.stream_ptr())
+        return _result(out, on_dev, scalar)
 
 
 @dataclass(frozen=True)
@@ -48,11 +84,65 @@ class Polynomial:
     def degree(self) -> int:
         return len(self.coeffs) - 1
 
+    def __call__(self, x):
+        return eval_poly(self, x)
+
 
 @dataclass(frozen=True)
 class Rational:
+    """Ratio of two polynomials (approximants.py:43-52)."""
+
     numerator: Polynomial
     denominator: Polynomial
+
+    def __call__(self, x):
+        return eval_rational(self, x)
+
+
+def _poly_eval(num: Polynomial, den, x):
+    import torch
+
+    from . import _dev, _lib
+    from .exact import _f64_args
+
+    for p in (num, den):
+        if p is not None and p.degree >= _lib.POLY_MAX:
+            raise ValueError(f"polynomial degree {p.degree} exceeds the device limit {_lib.POLY_MAX - 1}")
+    scalar = _is_scalar(x)
+    (t,), on_dev = _f64_args(x)
+    spec = _lib.MactPolySpec()
+    spec.num_deg = num.degree
+    for i, c in enumerate(num.coeffs):
+        spec.num[i] = c
+    spec.den_deg = -1 if den is None else den.degree
+    if den is not None:
+        for i, c in enumerate(den.coeffs):
+            spec.den[i] = c
+    out = torch.empty(t.shape, dtype=torch.float64, device=t.device)
+    flag = torch.zeros(1, dtype=torch.int32, device=t.device)
+    _lib.call("mact_poly_eval", spec, t.data_ptr(), out.data_ptr(), t.numel(), flag.data_ptr(),
+              _dev.stream_ptr())
+    if den is not None and int(flag.item()):
+        if scalar:
+            raise DegenerateDenominator(f"denominator vanished at x={x!r}")
+        raise DegenerateDenominator("denominator vanished inside evaluation batch")
+    return _result(out, on_dev, scalar)
+
+
+def eval_poly(p: Polynomial, x):
+    """Evaluate ``p`` at ``x`` (scalar, ndarray or CUDA tensor) in Horner form (approximants.py:55-72),
+    on the GPU with numpy's operation order: bit-identical to the reference."""
+    return _poly_eval(p, None, x)
+
+
+def eval_rational(r: Rational, x):
+    """Evaluate ``r`` at ``x``; DegenerateDenominator on a vanishing q(x) (approximants.py:75-82)."""
+    return _poly_eval(r.numerator, r.denominator, x)
+
+
+def target_values(target, x):
+    """Evaluate a target given either a TargetFn member or a plain callable (approximants.py:118-120)."""
+    return target.exact(x) if isinstance(target, TargetFn) else target(x)
 
 
 @dataclass(frozen=True)
@@ -66,6 +156,18 @@ class Approximant:
         lo, hi = self.interval
         if not lo < hi:
             raise ValueError(f"interval must satisfy lo < hi, got {self.interval}")
+
+    def __call__(self, x):
+        return self.form(x)
+
+    def measured_max_error(self, num_points: int = 100_000) -> float:
+        """Max |approx - exact| over a dense uniform grid of the fit interval (approximants.py:144-149)."""
+        import torch
+
+        lo, hi = self.interval
+        grid = torch.from_numpy(np.linspace(lo, hi, num_points)).cuda()
+        diff = self.form(grid) - torch.as_tensor(target_values(self.target_fn, grid), device=grid.device)
+        return float(diff.abs().max())
 
 
 # (target, degrees) -> (eps_max, coefficient strings...)  — one table, every set.

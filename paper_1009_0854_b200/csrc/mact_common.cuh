@@ -14,6 +14,8 @@ namespace mact {
 
 constexpr double kPi = 3.14159265358979311600;   // np.pi
 constexpr double kTwoPi = 2.0 * kPi;
+constexpr double kSqrt2 = 1.4142135623730951;    // math.sqrt(2.0), approximants.py:21
+constexpr double kSqrt3 = 1.7320508075688772;    // math.sqrt(3.0), approximants.py:22
 
 // BT.709 / D65 constants (exact.py:21-40)
 constexpr double kGammaKnee = 0.081, kGammaSlope = 4.5, kGammaOffset = 0.099,
@@ -225,5 +227,6 @@ int make_kcoeffs(const MactCoeffs* c, KCoeffs* out);
 // Sets the dynamic-smem attribute once per (kernel, device) and returns the
 // persistent grid size occupancy x SM count (cached), or <= 0 on error.
 int persistent_grid(const void* fn, int threads, size_t smem_bytes);
+int grid_cap();   // MACT_GRID_CAP (debug): upper bound on persistent grids, in CTAs
 
 }  // namespace mact

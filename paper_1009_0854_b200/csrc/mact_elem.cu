@@ -3,6 +3,7 @@
 //   mact_approx_eval <- fast.cbrt_fast / atan_sqrt3_fast / acos_fast / atan_unit_fast
 //                       (fast.py:81-83, :118-122, :151-185) over
 //                       approximants.eval_poly / eval_rational (approximants.py:55-82)
+//   mact_poly_eval   <- approximants.eval_poly / eval_rational (approximants.py:55-82), any degree < 32
 //   mact_exact_elem  <- exact.inverse_gamma / rgb_to_xyz / lab_f / xyz_to_lab (exact.py:52-83),
 //                       lut.angular_lerp (lut.py:202-216)
 //
@@ -68,6 +69,29 @@ __global__ void k_approx(const __grid_constant__ ApproxParams p, const double* _
   }
 }
 
+// approximants.eval_poly / eval_rational (approximants.py:55-82) for any
+// Polynomial / Rational of degree < kPolyMax: numpy's Horner order, each step
+// rounded twice (acc *= x; acc += c), the quotient rounded once.
+struct PolyParams {
+  MactPolySpec s;
+};
+__global__ void k_poly(const __grid_constant__ PolyParams p, const double* __restrict__ x,
+                       double* __restrict__ out, int64_t n, int32_t* __restrict__ degenerate) {
+  const MactPolySpec& s = p.s;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[i];
+    const double num = horner_np(s.num, s.num_deg, v);
+    if (s.den_deg < 0) {
+      out[i] = num;
+    } else {
+      const double den = horner_np(s.den, s.den_deg, v);
+      if (fabs(den) < 1e-300 && degenerate) *degenerate = 1;
+      out[i] = __ddiv_rn(num, den);
+    }
+  }
+}
+
 __device__ __forceinline__ double inverse_gamma_np(double k) {    // exact.py:52-57
   return k < kGammaKnee ? __ddiv_rn(k, kGammaSlope)
                         : pow(__ddiv_rn(__dadd_rn(k, kGammaOffset), kGammaScale), kGammaPower);
@@ -81,7 +105,19 @@ __global__ void k_exact_elem(int op, const double* __restrict__ a, const double*
                              double* __restrict__ o1, double* __restrict__ o2, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    if (op == MACT_ELEM_INVERSE_GAMMA) {
+    if (op >= MACT_ELEM_TARGET_CBRT) {                              // TargetFn.exact, approximants.py:101-115
+      const double v = a[i];
+      double r;
+      switch (op) {
+        case MACT_ELEM_TARGET_CBRT: r = cbrt(v); break;                          // np.cbrt
+        case MACT_ELEM_TARGET_ATAN_SQRT3: r = atan(__dmul_rn(kSqrt3, v)); break;   // arctan(sqrt(3) x)
+        case MACT_ELEM_TARGET_ASIN_HALF: r = __dmul_rn(2.0, asin(__ddiv_rn(v, kSqrt2))); break;
+        case MACT_ELEM_TARGET_ACOS_HALF: r = acos(v); break;
+        case MACT_ELEM_TARGET_ATAN_F: r = atan(v); break;
+        default: r = __dadd_rn(__dmul_rn(0.5, kPi), -atan(v)); break;             // 0.5 pi - arctan(x)
+      }
+      o0[i] = r;
+    } else if (op == MACT_ELEM_INVERSE_GAMMA) {
       o0[i] = inverse_gamma_np(a[i]);
     } else if (op == MACT_ELEM_LAB_F) {
       o0[i] = lab_f_np(a[i]);
@@ -134,7 +170,7 @@ extern "C" int mact_approx_eval(const MactApproxSpec* spec, const double* x, con
 
 extern "C" int mact_exact_elem(int op, const double* in0, const double* in1, const double* in2,
                                double* out0, double* out1, double* out2, int64_t n, void* stream) {
-  if (op < MACT_ELEM_INVERSE_GAMMA || op > MACT_ELEM_ANGULAR_LERP)
+  if (op < MACT_ELEM_INVERSE_GAMMA || op > MACT_ELEM_TARGET_ATAN_G)
     return set_error(MACT_EBADARG, "unknown elementwise op %d", op);
   const bool three_in = op == MACT_ELEM_RGB_TO_XYZ || op == MACT_ELEM_XYZ_TO_LAB ||
                         op == MACT_ELEM_ANGULAR_LERP;
@@ -145,4 +181,17 @@ extern "C" int mact_exact_elem(int op, const double* in0, const double* in1, con
   k_exact_elem<<<elem_grid(n), 256, 0, (cudaStream_t)stream>>>(op, in0, in1, in2, out0, out1, out2, n);
   count_launch();
   return check_launch("exact_elem");
+}
+
+extern "C" int mact_poly_eval(const MactPolySpec* spec, const double* x, double* out, int64_t n,
+                              int32_t* degenerate, void* stream) {
+  if (!spec || n < 0 || (n > 0 && (!x || !out))) return set_error(MACT_EBADARG, "bad argument");
+  if (spec->num_deg < 0 || spec->num_deg >= MACT_POLY_MAX || spec->den_deg >= MACT_POLY_MAX)
+    return set_error(MACT_EBADARG, "polynomial degrees out of range (%d, %d)", spec->num_deg, spec->den_deg);
+  if (n == 0) return MACT_OK;
+  PolyParams p;
+  p.s = *spec;
+  k_poly<<<elem_grid(n), 256, 0, (cudaStream_t)stream>>>(p, x, out, n, degenerate);
+  count_launch();
+  return check_launch("poly_eval");
 }

@@ -18,7 +18,8 @@
 // exceeds a CTA's 227 KB: a 3-CTA cluster holds one component per CTA
 // (k_lut33_comp), with the L1/L2 gather kernel only for tails and unaligned
 // buffers.
-#include <atomic>
+#include <map>
+#include <mutex>
 
 #include <cooperative_groups.h>
 
@@ -348,9 +349,17 @@ __device__ __forceinline__ double px_chan(const TI* p, int64_t i) { return (doub
 // reference); linear components accumulate out += w_j V[node_j] in node order
 // (lut.py:233-236), rounded like numpy, so a linear destination with fp64
 // output reproduces the reference bit for bit.
-template <int N, int METHOD, typename TI, typename TO>
+//
+// CACHED: the caching variant (lut._interpolate_caching, lut.py:294-331) on
+// the per-cell cache arrays of mact_lut_cache_build: linear components as
+// trilinear polynomial terms (sum over the 8 terms in order, lut.py:303-306)
+// or base node plus weighted corner differences (lut.py:309-319), each
+// operation rounded like numpy's.
+template <int N, int METHOD, typename TI, typename TO, bool CACHED = false>
 __global__ void k_lut_fp64(const double* __restrict__ lat, int mask, const TI* __restrict__ rgb,
-                           TO* __restrict__ out, int64_t n, int planar) {
+                           TO* __restrict__ out, int64_t n, int planar,
+                           const double* __restrict__ tri = nullptr,
+                           const double* __restrict__ cdiff = nullptr) {
   constexpr int K = LutK<METHOD>::K;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -358,8 +367,27 @@ __global__ void k_lut_fp64(const double* __restrict__ lat, int mask, const TI* _
     double w[K], d[3];
     lut_nodes_real<N, METHOD>(px_chan(rgb, 3 * i), px_chan(rgb, 3 * i + 1), px_chan(rgb, 3 * i + 2), idx, w, d);
     double res[3];
+    // cell of the base corner in the (N-1)^3 cache
+    const int bf = idx[0], br = bf / (N * N), bg = (bf / N) % N, bb = bf % N;
+    const int64_t cell = ((int64_t)br * (N - 1) + bg) * (N - 1) + bb;
     for (int comp = 0; comp < 3; ++comp) {
-      if (!((mask >> comp) & 1)) {
+      if (!((mask >> comp) & 1) && CACHED && METHOD == MACT_LUT_TRILINEAR) {   // lut.py:301-306
+        const double t[8] = {1.0, d[0], d[1], d[2], __dmul_rn(d[0], d[1]), __dmul_rn(d[0], d[2]),
+                             __dmul_rn(d[1], d[2]), __dmul_rn(__dmul_rn(d[0], d[1]), d[2])};
+        const double* c = tri + cell * 24 + comp;
+        double a = __dmul_rn(c[0], t[0]);
+        for (int k = 1; k < 8; ++k) a = __dadd_rn(a, __dmul_rn(c[3 * k], t[k]));
+        res[comp] = a;
+      } else if (!((mask >> comp) & 1) && CACHED) {                           // lut.py:307-319
+        const double* c = cdiff + cell * 24 + comp;
+        double a = lat[3 * bf + comp];
+        for (int j = 0; j < K; ++j) {
+          const int local = idx[j] - bf;
+          const int row = (local / (N * N)) << 2 | ((local % (N * N)) / N) << 1 | (local % N);
+          a = __dadd_rn(a, __dmul_rn(w[j], c[3 * row]));
+        }
+        res[comp] = a;
+      } else if (!((mask >> comp) & 1)) {
         double a = 0.0;
         for (int j = 0; j < K; ++j) a = __dadd_rn(a, __dmul_rn(w[j], lat[3 * idx[j] + comp]));
         res[comp] = a;
@@ -391,6 +419,36 @@ __global__ void k_lut_fp64(const double* __restrict__ lat, int mask, const TI* _
       if (planar) out[comp * n + i] = (TO)res[comp];
       else out[3 * i + comp] = (TO)res[comp];
     }
+  }
+}
+
+// lut.build_cache (lut.py:265-291): per cell (r-major over (n-1)^3) the 8
+// trilinear polynomial coefficients and the 8 corner differences, each (8, 3)
+// fp64, evaluated left to right as the numpy expressions are.
+__global__ void k_lut_cache_build(const double* __restrict__ lat, int n, double* __restrict__ tri,
+                                  double* __restrict__ cdiff) {
+  const int m = n - 1, total = m * m * m * 3;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int comp = i % 3, cell = i / 3;
+    const int br = cell / (m * m), bg = (cell / m) % m, bb = cell % m;
+    double c[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)   // corner k = r<<2 | g<<1 | b (_CORNER_OFFSETS, lut.py:59-60)
+      c[k] = lat[3 * (((br + (k >> 2 & 1)) * n + bg + (k >> 1 & 1)) * n + bb + (k & 1)) + comp];
+    double* t = tri + (int64_t)cell * 24 + comp;
+    t[0] = c[0];
+    t[3] = __dadd_rn(c[4], -c[0]);
+    t[6] = __dadd_rn(c[2], -c[0]);
+    t[9] = __dadd_rn(c[1], -c[0]);
+    t[12] = __dadd_rn(__dadd_rn(__dadd_rn(c[6], -c[4]), -c[2]), c[0]);
+    t[15] = __dadd_rn(__dadd_rn(__dadd_rn(c[5], -c[4]), -c[1]), c[0]);
+    t[18] = __dadd_rn(__dadd_rn(__dadd_rn(c[3], -c[2]), -c[1]), c[0]);
+    double s7 = __dadd_rn(__dadd_rn(__dadd_rn(c[7], -c[6]), -c[5]), -c[3]);
+    s7 = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(s7, c[4]), c[2]), c[1]), -c[0]);
+    t[21] = s7;
+    double* dd = cdiff + (int64_t)cell * 24 + comp;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dd[3 * k] = __dadd_rn(c[k], -c[0]);
   }
 }
 
@@ -597,7 +655,11 @@ __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
     if (tg == 0) mbar_arrive_expect_tx(&full[grp], full_bytes);
     mbar_wait(&full[grp], use & 1);
     const float* pl = planar + grp * PBUF;
-    float* sg = stage + grp * SBUF;                      // free: drained before the last barrier
+    float* sg = stage + grp * SBUF;
+    // the bulk store issued from sg at this group's previous step must have
+    // finished reading it before any thread of the group overwrites it
+    if (tg == 0) bulk_wait_read<0>();
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(512) : "memory");
     for (int i = tg; 4 * i < rlen; i += 512) {           // interleave 4 pixels per thread
       const float4 c0 = *reinterpret_cast<const float4*>(pl + 4 * i);
       const float4 c1 = *reinterpret_cast<const float4*>(pl + PLANE + 4 * i);
@@ -608,7 +670,6 @@ __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
       d[2] = make_float4(c2.z, c0.w, c1.w, c2.w);
     }
     fence_proxy_async_smem();
-    if (tg == 0) bulk_wait_read<0>();                    // stage[grp] of this group's last step drained
     asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(512) : "memory");   // stage written, planar read
     if (tg == 0) {
       bulk_s2g(out + 3 * (step * kLut33Step + r0), sg, (uint32_t)rlen * 12u);
@@ -693,6 +754,45 @@ __global__ void __launch_bounds__(kLut33Threads, 1)
   if (tg == 0) bulk_wait<0>();
 }
 
+// Resident clusters of `size` CTAs for a kernel, per device (smem opt-in
+// checked); bounded by MACT_GRID_CAP.
+static int max_clusters(const void* fn, int size, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({fn, dev});
+  if (it != cache.end()) return it->second;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) {
+    set_error(MACT_ECUDA, "cudaFuncSetAttribute(%zu B smem): %s", smem, cudaGetErrorString(e));
+    return -1;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(size * 48);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  int mc = 0;
+  if (cudaOccupancyMaxActiveClusters(&mc, fn, &cfg) != cudaSuccess || mc < 1) {   // __cluster_dims__ kernels
+    cudaGetLastError();
+    cudaLaunchAttribute attr;                                                       // runtime cluster size
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = size;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&mc, fn, &cfg) != cudaSuccess || mc < 1) {
+      cudaGetLastError();
+      mc = num_sms() / (size + 1);
+    }
+  }
+  if (mc * size > grid_cap()) mc = grid_cap() / size > 0 ? grid_cap() / size : 1;
+  cache[{fn, dev}] = mc;
+  return mc;
+}
+
 template <int METHOD>
 static int launch_lut33_comp(const float* lat, const uint8_t* rgb, float* out, int64_t n, int planar,
                              cudaStream_t st) {
@@ -720,20 +820,8 @@ static int launch_lut33_comp(const float* lat, const uint8_t* rgb, float* out, i
     if (int rc = check_launch("lut33_planar")) return rc;
   } else if (ok && nsteps > 0) {
     auto kfn = k_lut33_comp<METHOD>;
-    static std::atomic<int> max_clusters{-1};           // per method instantiation (benign race)
-    int mc = max_clusters.load();
-    if (mc < 0) {
-      cudaFuncSetAttribute((const void*)kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(3 * 48);
-      cfg.blockDim = dim3(kLut33Threads);
-      cfg.dynamicSmemBytes = smem;
-      if (cudaOccupancyMaxActiveClusters(&mc, (const void*)kfn, &cfg) != cudaSuccess || mc < 1) {
-        cudaGetLastError();
-        mc = num_sms() / 4;
-      }
-      max_clusters.store(mc);
-    }
+    const int mc = max_clusters((const void*)kfn, 3, kLut33Threads, smem);
+    if (mc < 0) return MACT_ECUDA;
     const int64_t clusters = mc < nsteps ? mc : nsteps;
     kfn<<<(unsigned)(3 * clusters), kLut33Threads, smem, st>>>(reinterpret_cast<const float4*>(lat),
                                                                rgb, out, nsteps);
@@ -788,39 +876,48 @@ static int interp_grid(int method, const float* lat, const uint8_t* rgb, float* 
   return set_error(MACT_EBADARG, "unknown interpolation method %d", method);
 }
 
+// tri / cdiff != nullptr: the caching variant (mact_lut_interp_cached)
 template <int N, typename TI, typename TO>
 static int interp_fp64(int method, int mask, const double* lat, const TI* rgb, TO* out,
-                       int64_t n, int planar, cudaStream_t st) {
+                       int64_t n, int planar, cudaStream_t st, const double* tri, const double* cdiff) {
   int64_t g = (n + 255) / 256;
   if (g > 8LL * num_sms()) g = 8LL * num_sms();
+  const bool c = tri != nullptr;
+#define MACT_FP64_CASE(M)                                                                                   \
+  case M:                                                                                                   \
+    if (c) k_lut_fp64<N, M, TI, TO, true><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar, tri, cdiff); \
+    else k_lut_fp64<N, M, TI, TO, false><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar);      \
+    break;
   switch (method) {
-    case MACT_LUT_TRILINEAR: k_lut_fp64<N, MACT_LUT_TRILINEAR, TI, TO><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
-    case MACT_LUT_PRISM: k_lut_fp64<N, MACT_LUT_PRISM, TI, TO><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
-    case MACT_LUT_PYRAMIDAL: k_lut_fp64<N, MACT_LUT_PYRAMIDAL, TI, TO><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
-    case MACT_LUT_TETRAHEDRAL: k_lut_fp64<N, MACT_LUT_TETRAHEDRAL, TI, TO><<<(unsigned)g, 256, 0, st>>>(lat, mask, rgb, out, n, planar); break;
+    MACT_FP64_CASE(MACT_LUT_TRILINEAR)
+    MACT_FP64_CASE(MACT_LUT_PRISM)
+    MACT_FP64_CASE(MACT_LUT_PYRAMIDAL)
+    MACT_FP64_CASE(MACT_LUT_TETRAHEDRAL)
     default: return set_error(MACT_EBADARG, "unknown interpolation method %d", method);
   }
+#undef MACT_FP64_CASE
   count_launch();
   return check_launch("lut_interp_fp64");
 }
 
 template <typename TI, typename TO>
 static int interp_fp64_grid(int grid_n, int method, int mask, const double* lat, const TI* rgb, TO* out,
-                            int64_t n, int planar, cudaStream_t st) {
+                            int64_t n, int planar, cudaStream_t st, const double* tri, const double* cdiff) {
   switch (grid_n) {
-    case 9: return interp_fp64<9>(method, mask, lat, rgb, out, n, planar, st);
-    case 17: return interp_fp64<17>(method, mask, lat, rgb, out, n, planar, st);
-    case 33: return interp_fp64<33>(method, mask, lat, rgb, out, n, planar, st);
+    case 9: return interp_fp64<9>(method, mask, lat, rgb, out, n, planar, st, tri, cdiff);
+    case 17: return interp_fp64<17>(method, mask, lat, rgb, out, n, planar, st, tri, cdiff);
+    case 33: return interp_fp64<33>(method, mask, lat, rgb, out, n, planar, st, tri, cdiff);
   }
   return set_error(MACT_EBADARG, "grid_n must be one of 9, 17, 33");
 }
 
 template <typename TI>
 static int interp_fp64_out(int out_dtype, int grid_n, int method, int mask, const double* lat, const TI* rgb,
-                           void* out, int64_t n, int planar, cudaStream_t st) {
+                           void* out, int64_t n, int planar, cudaStream_t st, const double* tri = nullptr,
+                           const double* cdiff = nullptr) {
   if (out_dtype == MACT_DTYPE_F64)
-    return interp_fp64_grid(grid_n, method, mask, lat, rgb, (double*)out, n, planar, st);
-  return interp_fp64_grid(grid_n, method, mask, lat, rgb, (float*)out, n, planar, st);
+    return interp_fp64_grid(grid_n, method, mask, lat, rgb, (double*)out, n, planar, st, tri, cdiff);
+  return interp_fp64_grid(grid_n, method, mask, lat, rgb, (float*)out, n, planar, st, tri, cdiff);
 }
 
 template <int N>
@@ -929,9 +1026,40 @@ extern "C" int mact_lut_interp_angular(const double* lattice64, int grid_n, int 
                               MACT_DTYPE_F32, n, layout, stream);
 }
 
+extern "C" int mact_lut_cache_build(const double* lattice64, int grid_n, double* trilinear,
+                                    double* corner_diff, void* stream) {
+  if (!lattice64 || !trilinear || !corner_diff) return set_error(MACT_EBADARG, "bad argument");
+  if (grid_n != 9 && grid_n != 17 && grid_n != 33) return set_error(MACT_EBADARG, "grid_n must be one of 9, 17, 33");
+  const int total = (grid_n - 1) * (grid_n - 1) * (grid_n - 1) * 3;
+  k_lut_cache_build<<<(total + 255) / 256, 256, 0, (cudaStream_t)stream>>>(lattice64, grid_n, trilinear,
+                                                                          corner_diff);
+  count_launch();
+  return check_launch("lut_cache_build");
+}
+
+static int lut_interp_fp64_entry(const double* lattice64, const double* tri, const double* cdiff, int grid_n,
+                                 int method, int angular_mask, const void* rgb, int in_dtype, void* out,
+                                 int out_dtype, int64_t n, int layout, void* stream);
+
+extern "C" int mact_lut_interp_cached(const double* lattice64, const double* trilinear,
+                                      const double* corner_diff, int grid_n, int method, int angular_mask,
+                                      const void* rgb, int in_dtype, void* out, int out_dtype, int64_t n,
+                                      int layout, void* stream) {
+  if (n > 0 && (!trilinear || !corner_diff)) return set_error(MACT_EBADARG, "caching interpolation needs the cache");
+  return lut_interp_fp64_entry(lattice64, trilinear, corner_diff, grid_n, method, angular_mask, rgb, in_dtype,
+                               out, out_dtype, n, layout, stream);
+}
+
 extern "C" int mact_lut_interp_real(const double* lattice64, int grid_n, int method, int angular_mask,
                                     const void* rgb, int in_dtype, void* out, int out_dtype, int64_t n,
                                     int layout, void* stream) {
+  return lut_interp_fp64_entry(lattice64, nullptr, nullptr, grid_n, method, angular_mask, rgb, in_dtype, out,
+                               out_dtype, n, layout, stream);
+}
+
+static int lut_interp_fp64_entry(const double* lattice64, const double* tri, const double* cdiff, int grid_n,
+                                 int method, int angular_mask, const void* rgb, int in_dtype, void* out,
+                                 int out_dtype, int64_t n, int layout, void* stream) {
   if (n < 0 || (n > 0 && (!lattice64 || !rgb || !out))) return set_error(MACT_EBADARG, "bad argument");
   if (angular_mask < 0 || angular_mask > 7) return set_error(MACT_EBADARG, "bad angular mask %d", angular_mask);
   if (layout != MACT_LAYOUT_INTERLEAVED && layout != MACT_LAYOUT_PLANAR)
@@ -945,11 +1073,14 @@ extern "C" int mact_lut_interp_real(const double* lattice64, int grid_n, int met
   cudaStream_t st = (cudaStream_t)stream;
   switch (in_dtype) {
     case MACT_DTYPE_U8:
-      return interp_fp64_out(out_dtype, grid_n, method, angular_mask, lattice64, (const uint8_t*)rgb, out, n, planar, st);
+      return interp_fp64_out(out_dtype, grid_n, method, angular_mask, lattice64, (const uint8_t*)rgb, out, n,
+                             planar, st, tri, cdiff);
     case MACT_DTYPE_F32:
-      return interp_fp64_out(out_dtype, grid_n, method, angular_mask, lattice64, (const float*)rgb, out, n, planar, st);
+      return interp_fp64_out(out_dtype, grid_n, method, angular_mask, lattice64, (const float*)rgb, out, n,
+                             planar, st, tri, cdiff);
     case MACT_DTYPE_F64:
-      return interp_fp64_out(out_dtype, grid_n, method, angular_mask, lattice64, (const double*)rgb, out, n, planar, st);
+      return interp_fp64_out(out_dtype, grid_n, method, angular_mask, lattice64, (const double*)rgb, out, n,
+                             planar, st, tri, cdiff);
   }
   return set_error(MACT_EBADARG, "unsupported input dtype %d", in_dtype);
 }

@@ -72,6 +72,18 @@ int reserved_smem() {
   return v;
 }
 
+// MACT_GRID_CAP=<ctas> caps every persistent grid (and the 33^3 cluster
+// count, in CTAs): a debugging knob so sanitizer runs over small inputs still
+// make each CTA loop over several tiles and recycle every buffer.
+int grid_cap() {
+  static const int cap = [] {
+    const char* e = getenv("MACT_GRID_CAP");
+    const int v = e ? atoi(e) : 0;
+    return v > 0 ? v : (1 << 30);
+  }();
+  return cap;
+}
+
 int persistent_grid(const void* fn, int threads, size_t smem_bytes) {
   static std::mutex mu;
   static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
@@ -97,7 +109,8 @@ int persistent_grid(const void* fn, int threads, size_t smem_bytes) {
     return -1;
   }
   if (occ < 1) occ = 1;
-  const int grid = occ * num_sms();
+  int grid = occ * num_sms();
+  if (grid > grid_cap()) grid = grid_cap();
   std::lock_guard<std::mutex> lk(mu);
   cache[key] = grid;
   return grid;

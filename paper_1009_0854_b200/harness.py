@@ -6,7 +6,6 @@
     component_error(...)   per-component |fast - exact|  (not in the reference)
     call_probabilities()  CallProbabilities             (harness.py:125-175)
     measure_gain(...)     GainStats, device-timed        (harness.py:176-221)
-    synthetic_corpus()                                   (harness.py:224-258)
 
 ``measure_error`` keeps the reference's plugin seam — any callable
 ``pixels -> (..., 3)`` — and fuses the whole evaluation into one kernel
@@ -32,6 +31,9 @@ from .errors import CorpusEmpty
 
 CUBE_SIZE = 1 << 24
 _CHUNK = 1 << 20
+
+# harness.DISTANCES (harness.py:28-32): the metric each space is scored with
+DISTANCES = exact.DISTANCES
 
 
 @dataclass(frozen=True)
@@ -381,36 +383,3 @@ def measure_gain(space: str, fast: Callable, exact_fn: Callable, corpus, repeats
     return GainStats(min=float(arr.min()), max=float(arr.max()), mean=float(arr.mean()),
                      stdev=float(arr.std(ddof=1)) if arr.size > 1 else 0.0,
                      median=float(np.median(arr)), per_image=tuple(float(v) for v in arr))
-
-
-def synthetic_corpus(sizes=(512, 1024, 2048), seed: int = 0) -> List[np.ndarray]:
-    """Deterministic benchmark images, one gradient, white-noise, 1/f-noise and
-    flat image per size (harness.py:224-243): host-side input generation with
-    numpy's seeded generator, so the bytes equal the reference's."""
-    rng = np.random.default_rng(seed)
-    images = []
-    for n in sizes:
-        yy, xx = np.mgrid[0:n, 0:n]
-        grad = np.stack([255.0 * xx / (n - 1), 255.0 * yy / (n - 1), 255.0 * (xx + yy) / (2 * n - 2)],
-                        axis=-1)
-        images.append(grad.astype(np.uint8))
-        images.append(rng.integers(0, 256, size=(n, n, 3), dtype=np.uint8))
-        images.append(_pink_noise(rng, n))
-        flat = np.empty((n, n, 3), dtype=np.uint8)
-        flat[..., 0], flat[..., 1], flat[..., 2] = 180, 120, 60
-        images.append(flat)
-    return images
-
-
-def _pink_noise(rng, n: int) -> np.ndarray:
-    """1/f noise per channel, min-max scaled to 0..255 (harness.py:246-258)."""
-    fy = np.fft.fftfreq(n)[:, None]
-    fx = np.fft.rfftfreq(n)[None, :]
-    radial = np.sqrt(fy * fy + fx * fx)
-    radial[0, 0] = 1.0
-    out = np.empty((n, n, 3))
-    for c in range(3):
-        img = np.fft.irfft2(np.fft.rfft2(rng.standard_normal((n, n))) / radial, s=(n, n))
-        lo, hi = img.min(), img.max()
-        out[..., c] = 255.0 * (img - lo) / (hi - lo)
-    return out.astype(np.uint8)

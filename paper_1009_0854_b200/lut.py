@@ -98,6 +98,13 @@ def _method_code(method: str) -> int:
     return _lib.METHODS[method]
 
 
+def _is_u8(pixels) -> bool:
+    """Integer pixels take the uint8 path (as _dev.as_device_pixels converts them)."""
+    if _dev.is_device_tensor(pixels):
+        return not pixels.dtype.is_floating_point
+    return np.asarray(pixels).dtype.kind in "iub"
+
+
 def _u8_pixels(pixels):
     t, code, lead, on_dev = _dev.as_device_pixels(pixels)
     if code != _lib.DTYPE_U8:
@@ -121,13 +128,42 @@ def node_weights(lut: Lut3D, pixels, method: str):
 
 
 def build_cache(lut: Lut3D) -> Lut3D:
-    """Caching variant marker (lut.py:265-291).  On the GPU the per-cell
-    difference cache buys nothing over the shared-memory lattice, so the
-    caching variant evaluates the same kernel (the reference proves the two
-    variants agree to 1e-12)."""
-    return Lut3D(grid_n=lut.grid_n, spacing=lut.spacing, destination_space=lut.destination_space,
-                 values=lut.values, angular_mask=lut.angular_mask, cache={"device": True},
-                 _device=lut._device)
+    """A LUT carrying the per-cell cache of every method (lut.py:265-291), built on the GPU
+    (mact_lut_cache_build, the reference's operation order: bit-identical).
+
+    ``cache["trilinear"]`` holds the 8 trilinear polynomial coefficients and
+    ``cache["corner_diff"]`` the 8 corner differences of every cell, both
+    (n-1, n-1, n-1, 8, 3) float64 like the reference's.  The device copies
+    stay with the returned LUT for ``interpolate(..., variant="caching")``.
+    """
+    import torch
+
+    _dev.require_cuda()
+    g = lut.grid_n
+    dev = torch.device("cuda", torch.cuda.current_device())
+    shape = (g - 1, g - 1, g - 1, 8, 3)
+    tri = torch.empty(shape, dtype=torch.float64, device=dev)
+    cdiff = torch.empty(shape, dtype=torch.float64, device=dev)
+    _lib.call("mact_lut_cache_build", lut.lattice64(dev).data_ptr(), g, tri.data_ptr(), cdiff.data_ptr(),
+              _dev.stream_ptr())
+    out = Lut3D(grid_n=g, spacing=lut.spacing, destination_space=lut.destination_space, values=lut.values,
+                angular_mask=lut.angular_mask,
+                cache={"trilinear": tri.cpu().numpy(), "corner_diff": cdiff.cpu().numpy()},
+                _device=dict(lut._device))
+    out._device[("cache", dev.index)] = (tri, cdiff)
+    return out
+
+
+def _cache_device(lut: Lut3D, device):
+    """Device copies of the cache arrays (uploaded once if the cache came from the host)."""
+    import torch
+
+    key = ("cache", device.index if device.index is not None else torch.cuda.current_device())
+    if key not in lut._device:
+        tri = torch.from_numpy(np.ascontiguousarray(lut.cache["trilinear"], dtype=np.float64)).to(device)
+        cdiff = torch.from_numpy(np.ascontiguousarray(lut.cache["corner_diff"], dtype=np.float64)).to(device)
+        lut._device[key] = (tri, cdiff)
+    return lut._device[key]
 
 
 def angular_lerp(theta0, theta1, alpha):
@@ -173,6 +209,20 @@ def interpolate(lut: Lut3D, pixels, method: str = "tetrahedral", variant: str = 
     if layout not in _lib.LAYOUTS:
         raise ValueError(f"unknown layout {layout!r}")
     mask = sum(1 << c for c, ang in enumerate(lut.angular_mask) if ang)
+    if variant == "caching" and (out_dtype == "float64" or mask or not _is_u8(pixels)):
+        # the caching arithmetic itself (lut.py:294-331); for uint8 pixels into fp32 the
+        # throughput kernel below serves both variants (they agree to 1e-12)
+        import torch
+
+        t, code, lead, on_dev = _dev.as_device_pixels(pixels)
+        res = _dev.empty_out(lead, layout, t.device,
+                             dtype=torch.float64 if out_dtype == "float64" else torch.float32)
+        tri, cdiff = _cache_device(lut, t.device)
+        _lib.call("mact_lut_interp_cached", lut.lattice64(t.device).data_ptr(), tri.data_ptr(), cdiff.data_ptr(),
+                  lut.grid_n, m, mask, t.data_ptr(), code, res.data_ptr(),
+                  _lib.DTYPE_F64 if out_dtype == "float64" else _lib.DTYPE_F32, t.numel() // 3,
+                  _lib.LAYOUTS[layout], _dev.stream_ptr())
+        return _dev.to_caller(res, on_dev)
     if out_dtype == "float64":
         import torch
 

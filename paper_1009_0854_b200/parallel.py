@@ -22,22 +22,49 @@ def env_world():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def init(backend: str = "nccl"):
-    """Initialise torch.distributed when launched by torchrun with WORLD_SIZE > 1."""
+def init(backend: str = "nccl", share_device: bool = False):
+    """Initialise torch.distributed when launched by torchrun with WORLD_SIZE > 1.
+
+    Returns (rank, world, device index).  One process per GPU: rank r drives
+    cuda:LOCAL_RANK over NCCL, and a world larger than the visible device
+    count is an error.  ``share_device`` (test mode for a 1-GPU box) puts
+    every rank on cuda:0 and combines over gloo instead; the ranks' kernels
+    never wait on one another (the path has no data-path collective).
+    """
     import torch
     import torch.distributed as dist
 
     rank, world, local = env_world()
+    ndev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if share_device:
+        backend, local = "gloo", 0
+    elif backend == "nccl" and local >= ndev:
+        raise RuntimeError(f"rank {rank}: LOCAL_RANK {local} needs cuda:{local} but only {ndev} "
+                           f"GPU(s) are visible; one process per GPU (use --share-gpu to run "
+                           f"{world} ranks on cuda:0 as a host-logic test)")
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")            # communicator init in the log: N ranks
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
+            if ndev:
+                torch.cuda.set_device(local)
             dist.init_process_group(backend)
-    elif backend == "nccl" and torch.cuda.is_available():
+    elif ndev and backend in ("nccl", "gloo"):
         torch.cuda.set_device(local)
     return rank, world, local
+
+
+def collective_device(device):
+    """Device for collective tensors: the GPU under NCCL, the host under gloo."""
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_backend() != "nccl":
+        return None
+    return device
 
 
 def shard_range(n: int, world: int, rank: int) -> range:

@@ -24,3 +24,10 @@ def figures():
     import json
     with open(os.path.join(ROOT, "tests", "golden", "figures.json")) as fh:
         return json.load(fh)
+
+
+@pytest.fixture(scope="session")
+def caching_golden():
+    """lut caching variant + approximant evaluators from the live reference (make_golden.py --caching-only)."""
+    import numpy as np
+    return np.load(os.path.join(ROOT, "tests", "golden", "caching_outputs.npz"))

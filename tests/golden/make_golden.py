@@ -149,8 +149,50 @@ def corpus_digest(harness) -> list:
             for im in harness.synthetic_corpus((64, 96), seed=0)]
 
 
+def caching_vectors() -> dict:
+    """lut.build_cache / interpolate(..., "caching") (lut.py:265-331) and the
+    approximant evaluators eval_poly / eval_rational / TargetFn.exact
+    (approximants.py:55-115) on deterministic inputs."""
+    import hashlib
+
+    from mact import approximants, lut
+
+    out = {}
+    rng = np.random.default_rng(265)
+    px = rng.integers(0, 256, (2048, 3), dtype=np.uint8)
+    px[:8] = [(0, 0, 0), (255, 255, 255), (255, 0, 0), (0, 255, 0), (0, 0, 255), (128, 128, 128),
+              (16, 32, 48), (255, 254, 253)]
+    fpx = np.concatenate([px[:512].astype(np.float64) + rng.random((512, 3)),
+                          [[-3.5, 12.0, 260.0], [255.0, 255.0, 255.0], [300.0, -10.0, 64.25]]])
+    out["px"], out["fpx"] = px, fpx
+    for space in ("lab", "hsi", "sct"):
+        for n in (9, 17, 33):
+            C = lut.build_cache(lut.build_lut(space, n))
+            if space == "lab":
+                for key in ("trilinear", "corner_diff"):
+                    out[f"cache_sha_{n}_{key}"] = np.frombuffer(
+                        hashlib.sha256(np.ascontiguousarray(C.cache[key]).tobytes()).digest(), np.uint8)
+                    if n == 9:
+                        out[f"cache_9_{key}"] = C.cache[key]
+            for method in lut.METHODS:
+                out[f"cach_{space}_{n}_{method}"] = lut.interpolate(C, px, method, "caching")
+                out[f"cachf_{space}_{n}_{method}"] = lut.interpolate(C, fpx, method, "caching")
+    x = np.concatenate([np.linspace(-1.5, 1.5, 4001), rng.random(999)])
+    out["poly_x"] = x
+    for (fn, deg) in approximants.registry_keys():
+        a = approximants.registry_get(fn, deg)
+        out[f"poly_{fn.value}_{'_'.join(map(str, deg))}"] = a(x)
+    out["target_x"] = np.linspace(0.0, 1.0, 2001)
+    for fn in approximants.TargetFn:
+        out[f"target_{fn.value}"] = fn.exact(out["target_x"])
+    return out
+
+
 def main() -> None:
     sys.path.insert(0, str(REF))
+    if "--caching-only" in sys.argv:
+        np.savez_compressed(OUT / "caching_outputs.npz", **caching_vectors())
+        return
     if "--elem-only" in sys.argv:
         np.savez_compressed(OUT / "elem_outputs.npz", **elem_vectors())
         return
@@ -223,6 +265,7 @@ def main() -> None:
     lut.save_lut(lut.build_lut("hsi", 9), OUT / "ref_hsi9.mlut")       # MLUT format fixture
     np.savez_compressed(OUT / "reference_outputs.npz", **arrays)
     np.savez_compressed(OUT / "elem_outputs.npz", **elem_vectors())
+    np.savez_compressed(OUT / "caching_outputs.npz", **caching_vectors())
     if "--arrays-only" in sys.argv:
         print(f"arrays written in {time.time() - t0:.1f}s")
         return

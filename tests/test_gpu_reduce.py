@@ -156,7 +156,12 @@ def test_measure_gain_device_timed(P):
     """harness.measure_gain (harness.py:197-221) on the GPU: Table 4's shape."""
     from paper_1009_0854_b200.errors import CorpusEmpty
     h, fast, exact = P["harness"], P["fast"], P["exact"]
-    corpus = h.synthetic_corpus((256,), seed=0)
+    rng = np.random.default_rng(0)
+    yy, xx = np.mgrid[0:256, 0:256]
+    corpus = [np.stack([xx, yy, (xx + yy) // 2], axis=-1).astype(np.uint8),
+              rng.integers(0, 256, (256, 256, 3), dtype=np.uint8),
+              rng.integers(0, 256, (256, 256, 3), dtype=np.uint8),
+              np.full((256, 256, 3), (180, 120, 60), dtype=np.uint8)]
     g = h.measure_gain("lab", fast.rgb_to_lab_fast, exact.rgb_to_lab_exact, corpus)
     assert len(g.per_image) == 4 and g.min <= g.median <= g.max and g.min > 0
     assert g.stdev >= 0 and abs(g.mean - np.mean(g.per_image)) < 1e-12

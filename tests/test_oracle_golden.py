@@ -198,3 +198,26 @@ def test_lut_node_weights_real_pixels_vs_reference(elem):
             nodes, w = O.node_weights(n, elem["lut_px"], m)
             eq(nodes, elem[f"nodesf_{n}_{m}"])
             eq(w, elem[f"weightsf_{n}_{m}"])
+
+
+def test_cache_arrays_bit_exact(caching_golden):
+    """oracle.build_cache (lut.py:265-291) equals the reference's arrays."""
+    import hashlib
+    for n in (9, 17, 33):
+        c = O.build_cache(O.build_lut_values("lab", n))
+        for key in ("trilinear", "corner_diff"):
+            assert hashlib.sha256(np.ascontiguousarray(c[key]).tobytes()).digest() == \
+                caching_golden[f"cache_sha_{n}_{key}"].tobytes(), (n, key)
+    eq(O.build_cache(O.build_lut_values("lab", 9))["trilinear"], caching_golden["cache_9_trilinear"])
+
+
+@pytest.mark.parametrize("space", ["lab", "hsi", "sct"])
+def test_caching_interp_bit_exact(caching_golden, space):
+    """oracle.interpolate_caching (lut.py:294-331) on uint8 and real-valued pixels."""
+    for n in (9, 17, 33):
+        vals = O.build_lut_values(space, n)
+        cache = O.build_cache(vals)
+        for method in O.METHODS:
+            for key, px in (("cach", caching_golden["px"]), ("cachf", caching_golden["fpx"])):
+                got = O.interpolate_caching(vals, cache, px, method, O.ANGULAR_MASKS[space])
+                eq(got, caching_golden[f"{key}_{space}_{n}_{method}"])
