@@ -86,6 +86,7 @@ _SIGNATURES = {
     "mact_lut_interp_real": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _i, _i64, _i, _vp]),
     "mact_lut_cache_build": (_i, [_vp, _i, _vp, _vp, _vp]),
     "mact_lut_interp_cached": (_i, [_vp, _vp, _vp, _i, _i, _i, _vp, _i, _vp, _i, _i64, _i, _vp]),
+    "mact_lut_nodes_timed": (_i, [_i, _i, _vp, _i64, _vp, _vp, _vp]),
     "mact_lut_nodes": (_i, [_i, _i, _vp, _i64, _vp, _vp, _vp]),
     "mact_lut_nodes_real": (_i, [_i, _i, _vp, _i, _i64, _vp, _vp, _vp]),
     "mact_err_workspace_bytes": (C.c_size_t, []),

@@ -18,6 +18,8 @@
 // exceeds a CTA's 227 KB: a 3-CTA cluster holds one component per CTA
 // (k_lut33_comp), with the L1/L2 gather kernel only for tails and unaligned
 // buffers.
+#include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 
@@ -241,19 +243,38 @@ struct OpLut {
     if constexpr (PACK) return s->q;
     else return LutQuant{};
   }
+  // Cell location and node selection of one pixel exactly as the interpolation
+  // kernels run it (indices into the staged NG^3 lattice; mact_lut_nodes_timed
+  // emits them for the parity tests).
+  // GHOST = false (the fp32-plane fallback, i.e. lattices that may hold
+  // non-finite nodes) keeps the reference's clamped cell in the staged NG^3
+  // lattice, so p = 255 never puts a zero weight on an inf / NaN node the
+  // reference does not touch.
+  template <bool GHOST = true>
+  static __device__ __forceinline__ void select(uint32_t r, uint32_t g, uint32_t b,
+                                                int (&idx)[LutK<METHOD>::K], float (&w)[LutK<METHOD>::K]) {
+    if constexpr (PACK && GHOST) {
+      int bf, rr, rg, rb;
+      locate_g(r, g, b, bf, rr, rg, rb);
+      lut_nodes_at<NG, METHOD, float, false>(bf, rr, rg, rb, idx, w);
+    } else if constexpr (PACK) {
+      int br, bg, bb, rr, rg, rb;
+      lut_locate<N>(r, br, rr);
+      lut_locate<N>(g, bg, rg);
+      lut_locate<N>(b, bb, rb);
+      lut_nodes_at<NG, METHOD, float, false>((br * NG + bg) * NG + bb, rr, rg, rb, idx, w);
+    } else {
+      lut_nodes<N, METHOD, float, false>(r, g, b, idx, w);
+    }
+  }
   static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
                                             uint32_t lane, const Params& p, float (*o)[3]) {
     constexpr int K = LutK<METHOD>::K;
     int idx[K];
     float w[K];
-    if constexpr (PACK) {
-      int bf, rr, rg, rb;
-      locate_g(r, g, b, bf, rr, rg, rb);
-      lut_nodes_at<NG, METHOD, float, false>(bf, rr, rg, rb, idx, w);
-    } else {
-      lut_nodes<N, METHOD, float, false>(r, g, b, idx, w);
-    }
     const LutQuant q = quant(s);
+    if (q.on) select<true>(r, g, b, idx, w);
+    else select<false>(r, g, b, idx, w);
     auto nd = [&](int i) { return q.on ? node<true>(s, p, i, lane, q) : node<false>(s, p, i, lane, q); };
     Node2 v = nd(idx[0]);
     float2 a01 = __fmul2_rn(make_float2(w[0], w[0]), v.xy);
@@ -298,20 +319,136 @@ struct OpLut {
       float w[PB][K];
       Node2 v[PB][K];
 #pragma unroll
-      for (int q = 0; q < PB; ++q) {
-        if constexpr (PACK) {
-          int bf, rr, rg, rb;
-          locate_g(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], bf, rr, rg, rb);
-          lut_nodes_at<NG, METHOD, float, false>(bf, rr, rg, rb, idx[q], w[q]);
-        } else {
-          lut_nodes<N, METHOD, float, false>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2],
-                                             idx[q], w[q]);
-        }
-      }
+      for (int q = 0; q < PB; ++q) select<PK>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], idx[q], w[q]);
 #pragma unroll
       for (int q = 0; q < PB; ++q)
 #pragma unroll
         for (int j = 0; j < K; ++j) v[q][j] = node<PK>(s, p, idx[q][j], lane, qt);
+#pragma unroll
+      for (int q = 0; q < PB; ++q) {
+        float2 a01 = __fmul2_rn(make_float2(w[q][0], w[q][0]), v[q][0].xy);
+        float a2 = w[q][0] * v[q][0].z;
+#pragma unroll
+        for (int j = 1; j < K; ++j) {
+          a01 = __ffma2_rn(make_float2(w[q][j], w[q][j]), v[q][j].xy, a01);
+          a2 = fmaf(w[q][j], v[q][j].z, a2);
+        }
+        o[q0 + q][0][0] = a01.x; o[q0 + q][0][1] = a01.y; o[q0 + q][0][2] = a2;
+      }
+    }
+  }
+};
+
+// ------------------------------------------------- 33^3: r-split CTA pairs
+// The 33^3 lattice as 64-bit fixed-point nodes (LutQuant) is 287 KB -- more
+// than one CTA's 227 KB -- but HALF of it by r-planes is not: a 2-CTA cluster
+// holds planes 0..16 in rank 0 and planes 16..32 in rank 1 (17 x 33^2 x 8 B =
+// 148 KB each, plane 16 in both).  A cell with base_r <= 15 then has all its
+// nodes in rank 0's planes, one with base_r >= 16 all in rank 1's, so every
+// pixel gathers its K nodes from ONE CTA's shared memory: its own, or its
+// partner's through distributed shared memory (ld.shared::cluster on the
+// mapa address).  Each CTA streams its own tiles through the skeleton; cell
+// and simplex selection run once per pixel (the component-split cluster ran
+// them in all three CTAs).  Lattices the fixed-point format cannot hold
+// (LutQuant off: wide ranges, non-finite nodes) gather the fp32 lattice from
+// L2 instead, decided per launch by the same arithmetic in every CTA.
+constexpr int kL33Planes = 17;
+constexpr int kL33Plane = 33 * 33;
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ uint2 ld_cluster_v2(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared::cluster.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+
+template <int METHOD>
+struct OpLut33Pair {
+  static constexpr int NOUT = 1;
+  static constexpr bool kCluster = true;
+  using Params = LutParams;
+  struct Shared {
+    uint2 pk[kL33Planes * kL33Plane];
+    LutQuant q;
+    float red[32][6];
+  };
+  static __device__ __forceinline__ void init(Shared* s, const Params& p) {
+    lut_quant_setup(p.lat, 33 * 33 * 33, &s->q, s->red);   // ends with __syncthreads
+    const LutQuant q = s->q;
+    if (!q.on) return;
+    const int first = 16 * kL33Plane * (int)cluster_rank();
+    for (int i = threadIdx.x; i < kL33Planes * kL33Plane; i += blockDim.x)
+      s->pk[i] = lut_quant_pack(q, __ldg(p.lat + first + i));
+  }
+  struct Ctx {
+    LutQuant q;
+    uint32_t base[2];   // cluster address of node 0 of the lattice as seen through rank k's planes
+  };
+  static __device__ __forceinline__ Ctx ctx(const Shared* s, const Params&) {
+    Ctx c;
+    c.q = s->q;
+    const uint32_t a = smem_u32(s->pk);
+    c.base[0] = mapa_shared(a, 0);
+    c.base[1] = mapa_shared(a, 1) - 16u * kL33Plane * 8u;
+    return c;
+  }
+  template <bool = true>
+  static __device__ __forceinline__ void select(uint32_t r, uint32_t g, uint32_t b,
+                                                int (&idx)[LutK<METHOD>::K], float (&w)[LutK<METHOD>::K]) {
+    int br, bg, bb, rr, rg, rb;
+    lut_locate<33>(r, br, rr);
+    lut_locate<33>(g, bg, rg);
+    lut_locate<33>(b, bb, rb);
+    lut_nodes_at<33, METHOD, float, false>((br * 33 + bg) * 33 + bb, rr, rg, rb, idx, w);
+  }
+  static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
+                                            uint32_t lane, const Params& p, float (*o)[3]) {
+    OpLut<33, METHOD>::px(r, g, b, nullptr, lane, p, o);   // per-pixel fallback: L2 gathers
+  }
+  static __device__ __forceinline__ void px4w_ctx(uint32_t w0, uint32_t w1, uint32_t w2, const Shared* s,
+                                                  uint32_t lane, const Params& p, const Ctx& c,
+                                                  float (*o)[1][3]) {
+    if (c.q.on) px4w_t<true>(w0, w1, w2, p, c, o);
+    else px4w_t<false>(w0, w1, w2, p, c, o);
+  }
+  template <bool PK>
+  static __device__ __forceinline__ void px4w_t(uint32_t w0, uint32_t w1, uint32_t w2, const Params& p,
+                                                const Ctx& c, float (*o)[1][3]) {
+    constexpr int K = LutK<METHOD>::K;
+    constexpr int PB = K > 6 ? 2 : 4;
+    const uint32_t ch[12] = {byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), byte_of(w0, 3),
+                             byte_of(w1, 0), byte_of(w1, 1), byte_of(w1, 2), byte_of(w1, 3),
+                             byte_of(w2, 0), byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3)};
+#pragma unroll
+    for (int q0 = 0; q0 < 4; q0 += PB) {
+      int idx[PB][K];
+      float w[PB][K];
+      uint32_t base[PB];
+      Node2 v[PB][K];
+#pragma unroll
+      for (int q = 0; q < PB; ++q) {
+        select<>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], idx[q], w[q]);
+        base[q] = idx[q][0] >= 16 * kL33Plane ? c.base[1] : c.base[0];   // base_r >= 16: rank 1's planes
+      }
+#pragma unroll
+      for (int q = 0; q < PB; ++q)
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          if constexpr (PK) {
+            v[q][j] = lut_quant_unpack2(c.q, ld_cluster_v2(base[q] + ((uint32_t)idx[q][j] << 3)));
+          } else {
+            const float4 t = __ldg(p.lat + idx[q][j]);
+            v[q][j] = Node2{make_float2(t.x, t.y), t.z};
+          }
+        }
 #pragma unroll
       for (int q = 0; q < PB; ++q) {
         float2 a01 = __fmul2_rn(make_float2(w[q][0], w[q][0]), v[q][0].xy);
@@ -486,6 +623,29 @@ __global__ void k_lut_nodes(const uint8_t* __restrict__ rgb, int64_t n, int32_t*
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       nodes[i * K + j] = idx[j];
+      weights[i * K + j] = w[j];
+    }
+  }
+}
+
+// The interpolation kernels' own selection (Op::select: TIES = false, the
+// 17^3 ghost planes), node indices mapped back to the n^3 lattice (a ghost
+// node is a copy of the edge node it maps to, and carries weight 0).
+template <int N, int METHOD>
+__global__ void k_lut_nodes_timed(const uint8_t* __restrict__ rgb, int64_t n, int32_t* __restrict__ nodes,
+                                  float* __restrict__ weights) {
+  constexpr int K = LutK<METHOD>::K;
+  using Sel = std::conditional_t<N == 33, OpLut33Pair<METHOD>, OpLut<N, METHOD>>;
+  constexpr int NG = N == 33 ? 33 : OpLut<N, METHOD>::NG;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int idx[K];
+    float w[K];
+    Sel::template select<true>(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2], idx, w);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int ir = min(idx[j] / (NG * NG), N - 1), ig = min((idx[j] / NG) % NG, N - 1), ib = min(idx[j] % NG, N - 1);
+      nodes[i * K + j] = (ir * N + ig) * N + ib;
       weights[i * K + j] = w[j];
     }
   }
@@ -847,6 +1007,72 @@ static int launch_lut33_comp(const float* lat, const uint8_t* rgb, float* out, i
   return MACT_OK;
 }
 
+#ifndef MACT_LUT33_NW
+#define MACT_LUT33_NW 16
+#endif
+#ifndef MACT_LUT33_SIN
+#define MACT_LUT33_SIN 3
+#endif
+// 33^3 on r-split CTA pairs (OpLut33Pair): whole tiles on k_ws launched as
+// 2-CTA clusters, the tail (and unaligned buffers) on the L2-gather kernel.
+template <int METHOD>
+static int launch_lut33_pair(const float* lat, const uint8_t* rgb, float* out, int64_t n, int planar,
+                             cudaStream_t st) {
+  using Op = OpLut33Pair<METHOD>;
+  constexpr int NW = MACT_LUT33_NW, G = 1, SIN = MACT_LUT33_SIN, NOB = 1;
+  using L = WsLayout<Op, NW, G, SIN, NOB>;
+  NvtxRange range("lut33_interp");
+  Outs outs{{out, nullptr, nullptr}};
+  LutParams p{reinterpret_cast<const float4*>(lat)};
+  const bool aligned = (uintptr_t)rgb % 16 == 0 && (uintptr_t)out % 16 == 0 && (!planar || n % 4 == 0);
+  const int64_t ntiles = aligned ? n / L::TP : 0;
+  if (ntiles > 0) {
+    auto kfn = k_ws<Op, NW, G, SIN, NOB>;
+    const int mc = max_clusters((const void*)kfn, 2, L::threads, L::bytes);
+    if (mc < 0) return MACT_ECUDA;
+    int64_t grid = 2LL * mc;
+    if (grid > ntiles) grid = ntiles + (ntiles & 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(L::threads);
+    cfg.dynamicSmemBytes = L::bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, rgb, outs, n, ntiles, planar, p);
+    if (e != cudaSuccess) return set_error(MACT_ECUDA, "lut33_pair launch: %s", cudaGetErrorString(e));
+    count_launch();
+    if (int rc = check_launch("lut33_pair")) return rc;
+  }
+  const int64_t done = ntiles * L::TP;
+  if (done < n) {
+    auto kfn = k_generic<OpLut<33, METHOD>, 256>;
+    const size_t sb = sizeof(typename OpLut<33, METHOD>::Shared);
+    const int64_t cap = persistent_grid((const void*)kfn, 256, sb);
+    if (cap <= 0) return MACT_ECUDA;
+    int64_t grid = (n - done + 255) / 256;
+    if (grid > cap) grid = cap;
+    kfn<<<(unsigned)grid, 256, sb, st>>>(rgb, outs, done, n, planar, p);
+    count_launch();
+    return check_launch("lut_interp");
+  }
+  return MACT_OK;
+}
+
+// MACT_LUT33_KERNEL=comp selects the R01 component-split kernels (A/B only).
+static bool lut33_legacy() {
+  static const bool v = [] {
+    const char* e = getenv("MACT_LUT33_KERNEL");
+    return e && strcmp(e, "comp") == 0;
+  }();
+  return v;
+}
+
 template <int N, int METHOD>
 static int launch_interp(const float* lat, const uint8_t* rgb, float* out, int64_t n, int planar,
                          cudaStream_t st) {
@@ -858,7 +1084,8 @@ static int launch_interp(const float* lat, const uint8_t* rgb, float* out, int64
   // the L2 streaming kernel remains its fallback for planar output, unaligned
   // buffers and the tail.
   if constexpr (N == 33)
-    return launch_lut33_comp<METHOD>(lat, rgb, out, n, planar, st);
+    return lut33_legacy() ? launch_lut33_comp<METHOD>(lat, rgb, out, n, planar, st)
+                          : launch_lut33_pair<METHOD>(lat, rgb, out, n, planar, st);
   else
     return launch_stream_t<OpLut<N, METHOD>, MACT_LUT_NW, (N <= 9 ? 2 : 1), MACT_LUT_SIN, 1>(
         rgb, outs, n, planar, p, st, "lut_interp");
@@ -934,6 +1161,22 @@ static int nodes_grid(int method, const uint8_t* rgb, int64_t n, int32_t* nodes,
   }
   count_launch();
   return check_launch("lut_nodes");
+}
+
+template <int N>
+static int nodes_timed_grid(int method, const uint8_t* rgb, int64_t n, int32_t* nodes, float* w,
+                            cudaStream_t st) {
+  int64_t g = (n + 255) / 256;
+  if (g > 8LL * num_sms()) g = 8LL * num_sms();
+  switch (method) {
+    case MACT_LUT_TRILINEAR: k_lut_nodes_timed<N, MACT_LUT_TRILINEAR><<<(unsigned)g, 256, 0, st>>>(rgb, n, nodes, w); break;
+    case MACT_LUT_PRISM: k_lut_nodes_timed<N, MACT_LUT_PRISM><<<(unsigned)g, 256, 0, st>>>(rgb, n, nodes, w); break;
+    case MACT_LUT_PYRAMIDAL: k_lut_nodes_timed<N, MACT_LUT_PYRAMIDAL><<<(unsigned)g, 256, 0, st>>>(rgb, n, nodes, w); break;
+    case MACT_LUT_TETRAHEDRAL: k_lut_nodes_timed<N, MACT_LUT_TETRAHEDRAL><<<(unsigned)g, 256, 0, st>>>(rgb, n, nodes, w); break;
+    default: return set_error(MACT_EBADARG, "unknown interpolation method %d", method);
+  }
+  count_launch();
+  return check_launch("lut_nodes_timed");
 }
 
 template <int N, typename TI>
@@ -1083,4 +1326,17 @@ static int lut_interp_fp64_entry(const double* lattice64, const double* tri, con
                              planar, st, tri, cdiff);
   }
   return set_error(MACT_EBADARG, "unsupported input dtype %d", in_dtype);
+}
+
+extern "C" int mact_lut_nodes_timed(int grid_n, int method, const uint8_t* rgb, int64_t n, int32_t* nodes,
+                                    float* weights, void* stream) {
+  if (n < 0 || (n > 0 && (!rgb || !nodes || !weights))) return set_error(MACT_EBADARG, "bad argument");
+  if (n == 0) return MACT_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (grid_n) {
+    case 9: return nodes_timed_grid<9>(method, rgb, n, nodes, weights, st);
+    case 17: return nodes_timed_grid<17>(method, rgb, n, nodes, weights, st);
+    case 33: return nodes_timed_grid<33>(method, rgb, n, nodes, weights, st);
+  }
+  return set_error(MACT_EBADARG, "grid_n must be one of 9, 17, 33");
 }

@@ -81,6 +81,19 @@ struct HasCtx : std::false_type {};
 template <class Op>
 struct HasCtx<Op, std::void_t<typename Op::Ctx>> : std::true_type {};
 
+// Ops that run as 2-CTA clusters (Op::kCluster = true: the pair shares its
+// staged tables through distributed shared memory) replace the CTA barrier
+// after Op::init with a cluster barrier, and keep every CTA resident until
+// its partner is done reading its shared memory.
+template <class Op, class = void>
+struct IsCluster : std::false_type {};
+template <class Op>
+struct IsCluster<Op, std::void_t<decltype(Op::kCluster)>> : std::integral_constant<bool, Op::kCluster> {};
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 template <class Op, int NW, int G, int SIN, int NOB>
 struct WsLayout {
   using Sh = typename Op::Shared;
@@ -153,7 +166,9 @@ __global__ void __launch_bounds__(32 * (NW + 1)) k_ws(const uint8_t* __restrict_
     }
   }
   Op::init(sh, p);
-  __syncthreads();
+  constexpr bool CL = IsCluster<Op>::value;
+  if constexpr (CL) cluster_sync_all();
+  else __syncthreads();
 
   if (warp == NW) {                                       // ---- producer warp
     if (lane == 0) {
@@ -165,6 +180,8 @@ __global__ void __launch_bounds__(32 * (NW + 1)) k_ws(const uint8_t* __restrict_
                  L::IN_BYTES, &full[s]);
       }
     }
+    __syncwarp();
+    if constexpr (CL) cluster_sync_all();                 // the partner may still read our tables
     return;
   }
 
@@ -229,6 +246,8 @@ __global__ void __launch_bounds__(32 * (NW + 1)) k_ws(const uint8_t* __restrict_
     }
   }
   if (lane == 0) bulk_wait<0>();
+  __syncwarp();
+  if constexpr (CL) cluster_sync_all();
 }
 
 // Per-pixel fallback for the tail tile and unaligned buffers.

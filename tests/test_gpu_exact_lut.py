@@ -183,7 +183,8 @@ def test_lut_interp_host_executor(grid, method):
 @pytest.mark.parametrize("n", [4096 * 37 + 8, 4096 * 5 + 3, 1000])
 @pytest.mark.parametrize("method", ["trilinear", "tetrahedral"])
 def test_lut33_planar_equals_interleaved(n, method):
-    """33^3 planar output (component CTAs, no exchange) == the interleaved cluster path."""
+    """33^3 planar output == interleaved output (the r-split pair kernel writes
+    either layout through the streaming skeleton; tails take the L2 kernel)."""
     from paper_1009_0854_b200 import lut
     px = torch.from_numpy(np.random.default_rng(n).integers(0, 256, (n, 3), dtype=np.uint8)).cuda()
     L = lut.build_lut("lab", 33)
@@ -225,20 +226,98 @@ def test_lut_beyond_int32_pixel_count(grid):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("n", [9, 17, 33])
 @pytest.mark.parametrize("method", O.METHODS)
-def test_lut17_interp_full_cube(P, method):
-    """17^3 CIELAB LUT on all 2^24 colours vs the oracle on the same fp32
-    lattice values: covers the 64-bit fixed-point node format (quantisation
-    half-step <= 4.4e-5) inside the 1e-4 tolerance."""
-    lt = P["lut"].build_lut("lab", 17)
+def test_lut_interp_full_cube(P, n, method):
+    """The TIMED uint8 kernels (9^3 bank-private copies, 17^3 fixed-point nodes
+    with ghost planes, 33^3 r-split CTA pairs) on all 2^24 colours vs the oracle
+    on the same fp32 lattice values, interleaved; planar output bit-identical
+    to interleaved.  The fixed-point formats stay inside 1e-4 (quantisation
+    half-step <= 4.4e-5)."""
+    lt = P["lut"].build_lut("lab", n)
     cube = P["harness"].cube_chunk(0, 1 << 24, device="cuda")
     got = P["lut"].interpolate(lt, cube, method).cpu().numpy()
+    planar = P["lut"].interpolate(lt, cube, method, layout="planar").cpu().numpy()
+    np.testing.assert_array_equal(planar.T, got)
     host = cube.cpu().numpy()
     vals = lt.values.astype(np.float32).astype(np.float64)
     worst = 0.0
     for s in range(0, 1 << 24, 1 << 22):
         worst = max(worst, check_lab(got[s:s + (1 << 22)], O.interpolate(vals, host[s:s + (1 << 22)], method)))
-    print(f"17^3 {method}: max |dLab| {worst:.3e}")
+    print(f"{n}^3 {method}: max |dLab| {worst:.3e}")
+
+
+def _sorted_nonzero(nodes, w, tiny):
+    """Per pixel: the (node, weight) pairs with |weight| > tiny, sorted by node (zeros -> sentinel)."""
+    nodes = np.where(np.abs(w) > tiny, nodes, np.iinfo(np.int32).max).astype(np.int64)
+    order = np.argsort(nodes, axis=1, kind="stable")
+    return np.take_along_axis(nodes, order, 1), np.take_along_axis(w, order, 1)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n", [9, 17, 33])
+@pytest.mark.parametrize("method", O.METHODS)
+def test_timed_kernel_selection_full_cube(P, n, method):
+    """Cells and simplices of the INTERPOLATION kernels (their own select():
+    tetrahedral order from max/min/sum, 17^3 ghost cells at p = 255) on all 2^24
+    colours: the nodes carrying nonzero weight are exactly the reference's
+    (lut.py:98-199), with the same weights to fp32 rounding.  Only zero-weight
+    nodes may differ (a tie's middle corner, a ghost node = a copy of the edge
+    node); fmaf(0, v, a) == a, so they cannot change a sum of finite nodes."""
+    from paper_1009_0854_b200 import _lib
+    k = P["lut"].NEIGHBOR_COUNT[method]
+    cube = P["harness"].cube_chunk(0, 1 << 24, device="cuda")
+    nodes = torch.empty((1 << 24, k), dtype=torch.int32, device="cuda")
+    w = torch.empty((1 << 24, k), dtype=torch.float32, device="cuda")
+    _lib.call("mact_lut_nodes_timed", n, _lib.METHODS[method], cube.data_ptr(), 1 << 24, nodes.data_ptr(),
+              w.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    nodes, w, host = nodes.cpu().numpy(), w.cpu().numpy(), cube.cpu().numpy()
+    step = 1 << 21
+    for s in range(0, 1 << 24, step):
+        on, ow = O.node_weights(n, host[s:s + step], method)
+        gn, gw = _sorted_nonzero(nodes[s:s + step], w[s:s + step], 0.0)
+        rn, rw = _sorted_nonzero(on, ow, 1e-12)     # the pyramid's u v - m may round to +-1e-19 in fp64
+        np.testing.assert_array_equal(gn, rn)
+        np.testing.assert_allclose(gw, rw, rtol=0, atol=2e-7)
+
+
+@pytest.mark.parametrize("n", [17, 33])
+def test_lut_nonfinite_lattice(P, n):
+    """A lattice with inf / NaN nodes keeps the reference's cells (no ghost-cell
+    0 * inf) and gathers in fp32: the non-finite pattern and every finite value
+    match the oracle on the same fp32 values."""
+    import dataclasses
+    lt = P["lut"].build_lut("lab", n)
+    vals = lt.values.copy()
+    vals[n - 1, n - 1, n - 1, 0] = np.inf          # the white corner
+    vals[n - 1, 0, :, 1] = -np.inf                 # a face edge
+    vals[n // 2, n // 2, n // 2, 2] = np.nan       # an interior node
+    bad = dataclasses.replace(lt, values=vals, _device={})
+    rng = np.random.default_rng(n)
+    img = np.concatenate([rng.integers(0, 256, (1 << 16, 3), dtype=np.uint8),
+                          np.array([[255, 255, 255], [255, 0, 0], [255, 0, 255], [128, 128, 128]], np.uint8)])
+    ref = O.interpolate(vals.astype(np.float32).astype(np.float64), img, "tetrahedral")
+    for method in O.METHODS:
+        ref = O.interpolate(vals.astype(np.float32).astype(np.float64), img, method)
+        got = P["lut"].interpolate(bad, dev(img), method).cpu().numpy().astype(np.float64)
+        np.testing.assert_array_equal(np.isnan(got), np.isnan(ref), err_msg=method)
+        np.testing.assert_array_equal(np.isinf(got), np.isinf(ref), err_msg=method)
+        fin = np.isfinite(ref)
+        np.testing.assert_allclose(got[fin], ref[fin], rtol=2e-6, atol=1e-4, err_msg=method)
+
+
+def test_lut33_wide_range_lattice_falls_back(P):
+    """33^3 lattice too wide for the fixed-point nodes (x1000): the pair kernel
+    gathers the fp32 lattice from L2 and still matches the oracle."""
+    import dataclasses
+    lt = P["lut"].build_lut("lab", 33)
+    wide = dataclasses.replace(lt, values=lt.values * 1000.0, _device={})
+    img = np.random.default_rng(5).integers(0, 256, (1 << 18, 3), dtype=np.uint8)
+    vals = wide.values.astype(np.float32).astype(np.float64)
+    for method in O.METHODS:
+        got = P["lut"].interpolate(wide, dev(img), method).cpu().numpy()
+        np.testing.assert_allclose(got, O.interpolate(vals, img, method), rtol=2e-6, atol=1e-2)
 
 
 def test_lut17_wide_range_lattice_keeps_fp32(P):
@@ -255,15 +334,16 @@ def test_lut17_wide_range_lattice_keeps_fp32(P):
     np.testing.assert_allclose(got, ref, rtol=2e-6, atol=1e-2)
 
 
+@pytest.mark.parametrize("n", [17, 33])
 @pytest.mark.parametrize("scale", [0.25, 1.0, 1.1, 1.2, 3.0])
 @pytest.mark.parametrize("method", ["pyramidal", "tetrahedral"])
-def test_lut17_error_bound_either_format(P, scale, method):
+def test_lut_error_bound_either_format(P, n, scale, method):
     """Lattices scaled around the fixed-point threshold (half-step 5e-5: the
     CIELAB lattice x1.14): below it the 64-bit nodes are used, above it the
     fp32 planes.  Either way |interp - oracle| <= 1.5 * 5e-5 (pyramid sum|w|)
     plus fp32 rounding of the values."""
     import dataclasses
-    lt = P["lut"].build_lut("lab", 17)
+    lt = P["lut"].build_lut("lab", n)
     sc = dataclasses.replace(lt, values=lt.values * scale, _device={})
     img = np.random.default_rng(11).integers(0, 256, (1 << 18, 3), dtype=np.uint8)
     got = P["lut"].interpolate(sc, dev(img), method).cpu().numpy().astype(np.float64)
