@@ -343,17 +343,43 @@ struct OpLut {
 // The 33^3 lattice as 64-bit fixed-point nodes (LutQuant) is 287 KB -- more
 // than one CTA's 227 KB -- but HALF of it by r-planes is not: a 2-CTA cluster
 // holds planes 0..16 in rank 0 and planes 16..32 in rank 1 (17 x 33^2 x 8 B =
-// 148 KB each, plane 16 in both).  A cell with base_r <= 15 then has all its
-// nodes in rank 0's planes, one with base_r >= 16 all in rank 1's, so every
-// pixel gathers its K nodes from ONE CTA's shared memory: its own, or its
-// partner's through distributed shared memory (ld.shared::cluster on the
-// mapa address).  Each CTA streams its own tiles through the skeleton; cell
-// and simplex selection run once per pixel (the component-split cluster ran
-// them in all three CTAs).  Lattices the fixed-point format cannot hold
-// (LutQuant off: wide ranges, non-finite nodes) gather the fp32 lattice from
-// L2 instead, decided per launch by the same arithmetic in every CTA.
+// 148 KB each, plane 16 in both).  A cell with base_r <= 15 (r <= 127) has
+// all its nodes in rank 0's planes, one with base_r >= 16 (r >= 128) all in
+// rank 1's, so the pixel's bit 7 of r names the CTA that can interpolate it
+// from its OWN shared memory.  (Gathering the other half's nodes through
+// distributed shared memory instead -- ld.shared::cluster per node -- measured
+// 22-43 Gpix/s: DSMEM serves scattered 8-byte requests slowly; it is used
+// here only for one contiguous bulk copy per warp and slice.)
+//
+// Warp w of rank 0 and warp w of rank 1 work on the same 256-pixel slices.
+// Per slice, each warp:
+//   1. loads the slice (6 words per lane, prefetched one slice ahead) and
+//      compacts ITS pixels (r >> 7 == rank) into a list, in pixel order, with
+//      ballots and prefix popcounts;
+//   2. interpolates the list, 32 entries per round (the 17^3 code: integer
+//      cell location and selection, LDS.64 fixed-point nodes, FFMA2), writing
+//      results for its own half of the slice (rank 0: pixels 0..127, rank 1:
+//      128..255) to `own` and those for the partner's half to `send`, both in
+//      list order;
+//   3. ships `send` with ONE bulk copy into the partner warp's `recv`
+//      (cp.async.bulk shared::cta -> shared::cluster, completing on the
+//      partner's mbarrier);
+//   4. merges its half from `own` and `recv` by the same ballots (a pixel's
+//      rank among ours / theirs) and stores it with STG.128;
+//   5. tells the partner its `recv` is free (remote mbarrier arrive).
+// Both sides know every count from the same input bytes, so the receiver
+// arms its barrier with exactly the bytes the sender will ship.  Selection
+// runs once per pixel; each CTA does half the interpolation work plus
+// ~1/4 of the output bytes over DSMEM (bulk).
 constexpr int kL33Planes = 17;
 constexpr int kL33Plane = 33 * 33;
+#ifndef MACT_LUT33_NW
+#define MACT_LUT33_NW 12
+#endif
+constexpr int kP33NW = MACT_LUT33_NW;          // warps per CTA (smem: 148 KB planes + 5.5 KB per warp)
+constexpr int kP33Slice = 256;                 // pixels per warp slice
+constexpr int kP33Half = 128;
+
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -364,42 +390,27 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
 }
-__device__ __forceinline__ uint2 ld_cluster_v2(uint32_t addr) {
-  uint2 v;
-  asm volatile("ld.shared::cluster.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
-  return v;
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+// local shared -> a cluster peer's shared, completing bytes on the peer's mbarrier
+__device__ __forceinline__ void bulk_s2cluster(uint32_t dst_cluster, uint32_t src_cta, uint32_t bytes,
+                                               uint32_t mbar_cluster) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst_cluster),
+      "r"(src_cta), "r"(bytes), "r"(mbar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
+// Selection of one pixel on the 33^3 lattice, as the pair kernel runs it.
 template <int METHOD>
-struct OpLut33Pair {
-  static constexpr int NOUT = 1;
-  static constexpr bool kCluster = true;
-  using Params = LutParams;
-  struct Shared {
-    uint2 pk[kL33Planes * kL33Plane];
-    LutQuant q;
-    float red[32][6];
-  };
-  static __device__ __forceinline__ void init(Shared* s, const Params& p) {
-    lut_quant_setup(p.lat, 33 * 33 * 33, &s->q, s->red);   // ends with __syncthreads
-    const LutQuant q = s->q;
-    if (!q.on) return;
-    const int first = 16 * kL33Plane * (int)cluster_rank();
-    for (int i = threadIdx.x; i < kL33Planes * kL33Plane; i += blockDim.x)
-      s->pk[i] = lut_quant_pack(q, __ldg(p.lat + first + i));
-  }
-  struct Ctx {
-    LutQuant q;
-    uint32_t base[2];   // cluster address of node 0 of the lattice as seen through rank k's planes
-  };
-  static __device__ __forceinline__ Ctx ctx(const Shared* s, const Params&) {
-    Ctx c;
-    c.q = s->q;
-    const uint32_t a = smem_u32(s->pk);
-    c.base[0] = mapa_shared(a, 0);
-    c.base[1] = mapa_shared(a, 1) - 16u * kL33Plane * 8u;
-    return c;
-  }
+struct Lut33Sel {
   template <bool = true>
   static __device__ __forceinline__ void select(uint32_t r, uint32_t g, uint32_t b,
                                                 int (&idx)[LutK<METHOD>::K], float (&w)[LutK<METHOD>::K]) {
@@ -409,58 +420,274 @@ struct OpLut33Pair {
     lut_locate<33>(b, bb, rb);
     lut_nodes_at<33, METHOD, float, false>((br * 33 + bg) * 33 + bb, rr, rg, rb, idx, w);
   }
-  static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
-                                            uint32_t lane, const Params& p, float (*o)[3]) {
-    OpLut<33, METHOD>::px(r, g, b, nullptr, lane, p, o);   // per-pixel fallback: L2 gathers
+};
+
+struct alignas(16) P33Warp {
+  uint32_t list[kP33Slice];     // packed r | g << 8 | b << 16 of this CTA's pixels, slice order
+  float own[kP33Half * 3];      // results for my half of the slice, list order
+  float send[kP33Half * 3];     // results for the partner's half, list order (bulk-copied)
+  float recv[kP33Half * 3];     // the partner's results for my half, its list order
+};
+struct P33Shared {
+  P33Warp wb[kP33NW];
+  uint2 pk[kL33Planes * kL33Plane];
+  uint64_t rfull[kP33NW];       // my recv landed (partner's bulk copy + my expect_tx arrive)
+  uint64_t sfree[kP33NW];       // the partner consumed what I sent (its remote arrive)
+  LutQuant q;
+  float red[32][6];
+};
+constexpr size_t kP33Smem = sizeof(P33Shared);
+
+// node value: fixed-point from my planes (PK) or fp32 from the L2 lattice
+template <bool PK>
+__device__ __forceinline__ Node2 p33_node(uint32_t pk_base, const float4* lat4, const LutQuant& q, int i) {
+  if constexpr (PK) {
+    uint2 w;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w.x), "=r"(w.y) : "r"(pk_base + ((uint32_t)i << 3)));
+    return lut_quant_unpack2(q, w);
+  } else {
+    const float4 t = __ldg(lat4 + i);
+    return Node2{make_float2(t.x, t.y), t.z};
   }
-  static __device__ __forceinline__ void px4w_ctx(uint32_t w0, uint32_t w1, uint32_t w2, const Shared* s,
-                                                  uint32_t lane, const Params& p, const Ctx& c,
-                                                  float (*o)[1][3]) {
-    if (c.q.on) px4w_t<true>(w0, w1, w2, p, c, o);
-    else px4w_t<false>(w0, w1, w2, p, c, o);
-  }
-  template <bool PK>
-  static __device__ __forceinline__ void px4w_t(uint32_t w0, uint32_t w1, uint32_t w2, const Params& p,
-                                                const Ctx& c, float (*o)[1][3]) {
-    constexpr int K = LutK<METHOD>::K;
-    constexpr int PB = K > 6 ? 2 : 4;
-    const uint32_t ch[12] = {byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2), byte_of(w0, 3),
-                             byte_of(w1, 0), byte_of(w1, 1), byte_of(w1, 2), byte_of(w1, 3),
-                             byte_of(w2, 0), byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3)};
+}
+
+// Interpolate list entries lane + 32 q (q < Q) and file each result in own / send.
+template <int METHOD, bool PK>
+__device__ __forceinline__ void p33_rounds(P33Warp& B, int M, int T0, uint32_t rank, uint32_t lane,
+                                           uint32_t pk_base, const float4* lat4, const LutQuant& q) {
+  constexpr int K = LutK<METHOD>::K;
+  constexpr int PB = K > 6 ? 2 : 4;              // entries per lane in flight
+  const int Q = (M + 31) >> 5;
+  for (int q0 = 0; q0 < Q; q0 += PB) {
+    int idx[PB][K];
+    float w[PB][K];
+    Node2 v[PB][K];
 #pragma unroll
-    for (int q0 = 0; q0 < 4; q0 += PB) {
-      int idx[PB][K];
-      float w[PB][K];
-      uint32_t base[PB];
-      Node2 v[PB][K];
+    for (int t = 0; t < PB; ++t) {
+      const int j = (int)lane + 32 * (q0 + t);
+      const uint32_t e = j < M ? B.list[j] : 0u;
+      Lut33Sel<METHOD>::template select<true>(e & 0xFFu, (e >> 8) & 0xFFu, e >> 16, idx[t], w[t]);
+    }
 #pragma unroll
-      for (int q = 0; q < PB; ++q) {
-        select<>(ch[3 * (q0 + q)], ch[3 * (q0 + q) + 1], ch[3 * (q0 + q) + 2], idx[q], w[q]);
-        base[q] = idx[q][0] >= 16 * kL33Plane ? c.base[1] : c.base[0];   // base_r >= 16: rank 1's planes
+    for (int t = 0; t < PB; ++t)
+#pragma unroll
+      for (int k = 0; k < K; ++k) v[t][k] = p33_node<PK>(pk_base, lat4, q, idx[t][k]);
+#pragma unroll
+    for (int t = 0; t < PB; ++t) {
+      float2 a01 = __fmul2_rn(make_float2(w[t][0], w[t][0]), v[t][0].xy);
+      float a2 = w[t][0] * v[t][0].z;
+#pragma unroll
+      for (int k = 1; k < K; ++k) {   // out += w_k V[node_k], node order (lut.py:233-236)
+        a01 = __ffma2_rn(make_float2(w[t][k], w[t][k]), v[t][k].xy, a01);
+        a2 = fmaf(w[t][k], v[t][k].z, a2);
       }
-#pragma unroll
-      for (int q = 0; q < PB; ++q)
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-          if constexpr (PK) {
-            v[q][j] = lut_quant_unpack2(c.q, ld_cluster_v2(base[q] + ((uint32_t)idx[q][j] << 3)));
-          } else {
-            const float4 t = __ldg(p.lat + idx[q][j]);
-            v[q][j] = Node2{make_float2(t.x, t.y), t.z};
-          }
-        }
-#pragma unroll
-      for (int q = 0; q < PB; ++q) {
-        float2 a01 = __fmul2_rn(make_float2(w[q][0], w[q][0]), v[q][0].xy);
-        float a2 = w[q][0] * v[q][0].z;
-#pragma unroll
-        for (int j = 1; j < K; ++j) {
-          a01 = __ffma2_rn(make_float2(w[q][j], w[q][j]), v[q][j].xy, a01);
-          a2 = fmaf(w[q][j], v[q][j].z, a2);
-        }
-        o[q0 + q][0][0] = a01.x; o[q0 + q][0][1] = a01.y; o[q0 + q][0][2] = a2;
+      const int j = (int)lane + 32 * (q0 + t);
+      if (j < M) {
+        const bool first = j < T0;                     // list entry of half 0
+        float* dst = (first == (rank == 0) ? B.own : B.send) + 3 * (first ? j : j - T0);
+        dst[0] = a01.x; dst[1] = a01.y; dst[2] = a2;
       }
     }
+  }
+}
+
+// vec: interleaved output 16-byte aligned (STG.128 per lane), or planar with n % 4 == 0 likewise
+template <int METHOD>
+__global__ void __launch_bounds__(kP33NW * 32, 1)
+    k_lut33_pair(const float4* __restrict__ lat4, const uint8_t* __restrict__ rgb, float* __restrict__ out,
+                 int64_t n, int64_t nslices, int planar) {
+  extern __shared__ __align__(128) uint8_t smem_p33[];
+  P33Shared* S = reinterpret_cast<P33Shared*>(smem_p33);
+  const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kP33NW; ++i) {
+      mbar_init(&S->rfull[i], 1);
+      mbar_init(&S->sfree[i], 1);
+    }
+    fence_mbar_init();
+  }
+  // first slice's input words in flight while the CTA stages its planes
+  const uint32_t* in_w = reinterpret_cast<const uint32_t*>(rgb);
+  const int64_t nbytes = 3 * n;
+  auto load = [&](int64_t sl, uint32_t (&wd)[2][3]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int64_t wi = sl * (kP33Slice * 3 / 4) + h * 96 + 3 * lane + c;   // word index
+        if (4 * wi + 3 < nbytes) {
+          wd[h][c] = __ldg(in_w + wi);
+        } else {                                        // the ragged end of the buffer
+          uint32_t v = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (4 * wi + k < nbytes) v |= (uint32_t)rgb[4 * wi + k] << (8 * k);
+          wd[h][c] = v;
+        }
+      }
+  };
+  int64_t sl = cl * kP33NW + warp;
+  uint32_t nxt[2][3] = {};
+  if (sl < nslices) load(sl, nxt);
+  lut_quant_setup(lat4, 33 * 33 * 33, &S->q, S->red);   // ends with __syncthreads
+  const LutQuant q = S->q;
+  if (q.on) {
+    const int first = 16 * kL33Plane * (int)rank;
+    for (int i = threadIdx.x; i < kL33Planes * kL33Plane; i += blockDim.x)
+      S->pk[i] = lut_quant_pack(q, __ldg(lat4 + first + i));
+  }
+  cluster_sync_all();   // both CTAs: barriers initialised, planes staged
+
+  P33Warp& B = S->wb[warp];
+  const uint32_t recv_peer = mapa_shared(smem_u32(B.recv), peer);
+  const uint32_t rfull_peer = mapa_shared(smem_u32(&S->rfull[warp]), peer);
+  const uint32_t sfree_peer = mapa_shared(smem_u32(&S->sfree[warp]), peer);
+  // node index (whole lattice) -> shared address in my planes
+  const uint32_t pk_base = smem_u32(S->pk) - rank * (16u * kL33Plane * 8u);
+  const uint32_t lt = lanemask_lt();
+  for (int64_t i = 0; sl < nslices; ++i, sl += ncl * kP33NW) {
+    uint32_t wd[2][3];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) wd[h][c] = nxt[h][c];
+    if (sl + ncl * kP33NW < nslices) load(sl + ncl * kP33NW, nxt);
+    const int64_t px0 = sl * kP33Slice;
+    // ---- 1. my pixels of the slice, compacted in pixel order
+    uint32_t bal[2][4];
+    int T[2], pre[2], valid[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t left = n - (px0 + kP33Half * h);
+      valid[h] = left <= 0 ? 0 : (left >= kP33Half ? kP33Half : (int)left);
+      T[h] = 0;
+      pre[h] = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t r = byte_of(wd[h][(3 * k) >> 2], (3 * k) & 3);
+        const bool mine = (r >> 7) == rank && (int)(4 * lane) + k < valid[h];
+        bal[h][k] = __ballot_sync(0xffffffffu, mine);
+        T[h] += __popc(bal[h][k]);
+        pre[h] += __popc(bal[h][k] & lt);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      int j = (h ? T[0] : 0) + pre[h];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if ((bal[h][k] >> lane) & 1u) {
+          const int b0 = 3 * k;   // byte offset of the pixel in the lane's 12 bytes
+          const uint32_t r = byte_of(wd[h][b0 >> 2], b0 & 3), g = byte_of(wd[h][(b0 + 1) >> 2], (b0 + 1) & 3),
+                         b = byte_of(wd[h][(b0 + 2) >> 2], (b0 + 2) & 3);
+          B.list[j++] = r | g << 8 | b << 16;
+        }
+      }
+    }
+    const int M = T[0] + T[1];
+    // my half of the slice (register selects, no dynamically indexed arrays)
+    const int Tm = rank ? T[1] : T[0], Tp = rank ? T[0] : T[1];
+    const int vm = rank ? valid[1] : valid[0], prem = rank ? pre[1] : pre[0];
+    uint32_t balm[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) balm[k] = rank ? bal[1][k] : bal[0][k];
+    const uint32_t in_bytes = (uint32_t)(12 * (vm - Tm) + 15) & ~15u;
+    const uint32_t out_bytes = (uint32_t)(12 * Tp + 15) & ~15u;
+    if (lane == 0) mbar_arrive_expect_tx(&S->rfull[warp], in_bytes);
+    if (i > 0) mbar_wait(&S->sfree[warp], (uint32_t)((i - 1) & 1));   // my send buffer is free again
+    __syncwarp();
+    // ---- 2. interpolate my pixels
+    if (q.on) p33_rounds<METHOD, true>(B, M, T[0], rank, lane, pk_base, lat4, q);
+    else p33_rounds<METHOD, false>(B, M, T[0], rank, lane, pk_base, lat4, q);
+    // ---- 3. the partner's half to the partner
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0 && out_bytes) bulk_s2cluster(recv_peer, smem_u32(B.send), out_bytes, rfull_peer);
+    // ---- 4. merge my half: ours from own, theirs from recv
+    mbar_wait(&S->rfull[warp], (uint32_t)(i & 1));
+    {
+      float o[12];
+      int ours = prem;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool m = (balm[k] >> lane) & 1u;
+        const int theirs = 4 * (int)lane + k - ours;
+        const float* src = m ? B.own + 3 * ours : B.recv + 3 * theirs;
+        o[3 * k] = src[0]; o[3 * k + 1] = src[1]; o[3 * k + 2] = src[2];
+        ours += m;
+      }
+      const int64_t p = px0 + kP33Half * rank + 4 * lane;
+      if (!planar) {
+        if (4 * (int)lane + 4 <= vm) {
+          float4* d = reinterpret_cast<float4*>(out + 3 * p);
+          d[0] = make_float4(o[0], o[1], o[2], o[3]);
+          d[1] = make_float4(o[4], o[5], o[6], o[7]);
+          d[2] = make_float4(o[8], o[9], o[10], o[11]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (4 * (int)lane + k < vm)
+#pragma unroll
+              for (int c = 0; c < 3; ++c) out[3 * (p + k) + c] = o[3 * k + c];
+        }
+      } else {
+        if (4 * (int)lane + 4 <= vm && (n & 3) == 0) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            *reinterpret_cast<float4*>(out + c * n + p) = make_float4(o[c], o[3 + c], o[6 + c], o[9 + c]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (4 * (int)lane + k < vm)
+#pragma unroll
+              for (int c = 0; c < 3; ++c) out[c * n + p + k] = o[3 * k + c];
+        }
+      }
+    }
+    // ---- 5. my recv is free for the partner's next slice
+    __syncwarp();
+    if (lane == 0) mbar_arrive_remote(sfree_peer);
+  }
+  cluster_sync_all();   // the partner may still copy into / arrive on my shared memory
+}
+
+// Per-pixel 33^3 path for unaligned buffers: the same selection and the same
+// node arithmetic as the pair kernel (fixed-point nodes quantised on the fly
+// from the L2 lattice with the same LutQuant), so every path is bit-identical.
+template <int METHOD>
+struct OpLut33Gen {
+  static constexpr int NOUT = 1;
+  using Params = LutParams;
+  struct Shared {
+    LutQuant q;
+    float red[32][6];
+  };
+  static __device__ __forceinline__ void init(Shared* s, const Params& p) {
+    lut_quant_setup(p.lat, 33 * 33 * 33, &s->q, s->red);
+  }
+  static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
+                                            uint32_t, const Params& p, float (*o)[3]) {
+    constexpr int K = LutK<METHOD>::K;
+    int idx[K];
+    float w[K];
+    Lut33Sel<METHOD>::template select<true>(r, g, b, idx, w);
+    const LutQuant q = s->q;
+    auto nd = [&](int i) {
+      const float4 t = __ldg(p.lat + i);
+      return q.on ? lut_quant_unpack2(q, lut_quant_pack(q, t)) : Node2{make_float2(t.x, t.y), t.z};
+    };
+    Node2 v = nd(idx[0]);
+    float2 a01 = __fmul2_rn(make_float2(w[0], w[0]), v.xy);
+    float a2 = w[0] * v.z;
+#pragma unroll
+    for (int k = 1; k < K; ++k) {
+      v = nd(idx[k]);
+      a01 = __ffma2_rn(make_float2(w[k], w[k]), v.xy, a01);
+      a2 = fmaf(w[k], v.z, a2);
+    }
+    o[0][0] = a01.x; o[0][1] = a01.y; o[0][2] = a2;
   }
 };
 
@@ -635,7 +862,7 @@ template <int N, int METHOD>
 __global__ void k_lut_nodes_timed(const uint8_t* __restrict__ rgb, int64_t n, int32_t* __restrict__ nodes,
                                   float* __restrict__ weights) {
   constexpr int K = LutK<METHOD>::K;
-  using Sel = std::conditional_t<N == 33, OpLut33Pair<METHOD>, OpLut<N, METHOD>>;
+  using Sel = std::conditional_t<N == 33, Lut33Sel<METHOD>, OpLut<N, METHOD>>;
   constexpr int NG = N == 33 ? 33 : OpLut<N, METHOD>::NG;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -1007,61 +1234,51 @@ static int launch_lut33_comp(const float* lat, const uint8_t* rgb, float* out, i
   return MACT_OK;
 }
 
-#ifndef MACT_LUT33_NW
-#define MACT_LUT33_NW 16
-#endif
-#ifndef MACT_LUT33_SIN
-#define MACT_LUT33_SIN 3
-#endif
-// 33^3 on r-split CTA pairs (OpLut33Pair): whole tiles on k_ws launched as
-// 2-CTA clusters, the tail (and unaligned buffers) on the L2-gather kernel.
+// 33^3 on r-split CTA pairs (k_lut33_pair); unaligned buffers take the
+// per-pixel kernel with the same arithmetic.
 template <int METHOD>
 static int launch_lut33_pair(const float* lat, const uint8_t* rgb, float* out, int64_t n, int planar,
                              cudaStream_t st) {
-  using Op = OpLut33Pair<METHOD>;
-  constexpr int NW = MACT_LUT33_NW, G = 1, SIN = MACT_LUT33_SIN, NOB = 1;
-  using L = WsLayout<Op, NW, G, SIN, NOB>;
   NvtxRange range("lut33_interp");
-  Outs outs{{out, nullptr, nullptr}};
   LutParams p{reinterpret_cast<const float4*>(lat)};
-  const bool aligned = (uintptr_t)rgb % 16 == 0 && (uintptr_t)out % 16 == 0 && (!planar || n % 4 == 0);
-  const int64_t ntiles = aligned ? n / L::TP : 0;
-  if (ntiles > 0) {
-    auto kfn = k_ws<Op, NW, G, SIN, NOB>;
-    const int mc = max_clusters((const void*)kfn, 2, L::threads, L::bytes);
-    if (mc < 0) return MACT_ECUDA;
-    int64_t grid = 2LL * mc;
-    if (grid > ntiles) grid = ntiles + (ntiles & 1);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(L::threads);
-    cfg.dynamicSmemBytes = L::bytes;
-    cfg.stream = st;
-    cudaLaunchAttribute attr;
-    attr.id = cudaLaunchAttributeClusterDimension;
-    attr.val.clusterDim.x = 2;
-    attr.val.clusterDim.y = 1;
-    attr.val.clusterDim.z = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, rgb, outs, n, ntiles, planar, p);
-    if (e != cudaSuccess) return set_error(MACT_ECUDA, "lut33_pair launch: %s", cudaGetErrorString(e));
-    count_launch();
-    if (int rc = check_launch("lut33_pair")) return rc;
-  }
-  const int64_t done = ntiles * L::TP;
-  if (done < n) {
-    auto kfn = k_generic<OpLut<33, METHOD>, 256>;
-    const size_t sb = sizeof(typename OpLut<33, METHOD>::Shared);
+  const bool aligned = (uintptr_t)rgb % 16 == 0 && (uintptr_t)out % 16 == 0;
+  if (!aligned) {
+    Outs outs{{out, nullptr, nullptr}};
+    auto kfn = k_generic<OpLut33Gen<METHOD>, 256>;
+    const size_t sb = sizeof(typename OpLut33Gen<METHOD>::Shared);
     const int64_t cap = persistent_grid((const void*)kfn, 256, sb);
     if (cap <= 0) return MACT_ECUDA;
-    int64_t grid = (n - done + 255) / 256;
+    int64_t grid = (n + 255) / 256;
     if (grid > cap) grid = cap;
-    kfn<<<(unsigned)grid, 256, sb, st>>>(rgb, outs, done, n, planar, p);
+    kfn<<<(unsigned)grid, 256, sb, st>>>(rgb, outs, 0, n, planar, p);
     count_launch();
     return check_launch("lut_interp");
   }
-  return MACT_OK;
+  const int64_t nslices = (n + kP33Slice - 1) / kP33Slice;
+  auto kfn = k_lut33_pair<METHOD>;
+  const int mc = max_clusters((const void*)kfn, 2, kP33NW * 32, kP33Smem);
+  if (mc < 0) return MACT_ECUDA;
+  int64_t clusters = mc;
+  const int64_t need = (nslices + kP33NW - 1) / kP33NW;   // clusters with at least one slice per warp
+  if (clusters > need) clusters = need;
+  if (clusters < 1) clusters = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * clusters));
+  cfg.blockDim = dim3(kP33NW * 32);
+  cfg.dynamicSmemBytes = kP33Smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = 2;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, reinterpret_cast<const float4*>(lat), rgb, out, n, nslices,
+                                           planar);
+  if (e != cudaSuccess) return set_error(MACT_ECUDA, "lut33_pair launch: %s", cudaGetErrorString(e));
+  count_launch();
+  return check_launch("lut33_pair");
 }
 
 // MACT_LUT33_KERNEL=comp selects the R01 component-split kernels (A/B only).
