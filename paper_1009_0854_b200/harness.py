@@ -165,12 +165,17 @@ def reduce_partials(space: str, candidate, reference, pixels=None, *, cube_start
         spec.candidate = _lib.CAND_FAST_F64 if kind == "fast64" else _lib.CAND_FAST
         cfg = payload
     elif kind == "lut":
-        spec.candidate = _lib.CAND_LUT
+        # score the THROUGHPUT kernel's own fp32 output (mact_lut_interp, the kernel bench.py
+        # times), not a re-implementation: run it over the shard, then reduce the array
+        px = t if t is not None else cube_chunk(cube_start, n, device=str(device))
+        c = torch.empty((n, 3), dtype=torch.float32, device=device)
         lat = payload.lut.lattice(device)
-        keep.append(lat)
-        spec.lut_lattice = lat.data_ptr()
-        spec.lut_grid_n = payload.lut.grid_n
-        spec.lut_method = _lib.METHODS[payload.method]
+        _lib.call("mact_lut_interp", lat.data_ptr(), payload.lut.grid_n, _lib.METHODS[payload.method],
+                  px.data_ptr(), c.data_ptr(), n, _lib.LAYOUTS["interleaved"], _dev.stream_ptr())
+        keep += [px, c, lat]
+        spec.candidate = _lib.CAND_ARRAY
+        spec.cand_array = c.data_ptr()
+        spec.cand_dtype = _lib.DTYPE_F32
     else:
         px = t if t is not None else cube_chunk(cube_start, n, device=str(device))
         c = candidate(px)

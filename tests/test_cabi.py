@@ -161,3 +161,18 @@ def test_lab_eval_path_env_switch(lib, monkeypatch):
     assert lib.mact_lab_eval_path(C.byref(fast.DEFAULT_CONFIG._pack())) == _lib.LAB_PATH_MONIC
     monkeypatch.delenv("MACT_LAB_EVAL")
     assert lib.mact_lab_eval_path(C.byref(fast.DEFAULT_CONFIG._pack())) == _lib.LAB_PATH_SEG
+
+
+def test_integration_stub_binds_only_exported_symbols(lib):
+    """INTEGRATION.md §2's mact/_b200.py (run inside the real reference by
+    test_gpu_reference_seam.py) is valid Python and calls only symbols the library exports."""
+    import ast
+
+    from tests.test_gpu_reference_seam import _stub_source
+
+    src = _stub_source()
+    ast.parse(src)
+    used = set(re.findall(r"_lib\.(mact_\w+)", src))
+    assert {"mact_transform_host", "mact_host_ctx_create", "mact_last_error"} <= used
+    for name in used:
+        assert hasattr(lib, name), name

@@ -183,8 +183,8 @@ def test_lut_interp_host_executor(grid, method):
 @pytest.mark.parametrize("n", [4096 * 37 + 8, 4096 * 5 + 3, 1000])
 @pytest.mark.parametrize("method", ["trilinear", "tetrahedral"])
 def test_lut33_planar_equals_interleaved(n, method):
-    """33^3 planar output == interleaved output (the r-split pair kernel writes
-    either layout through the streaming skeleton; tails take the L2 kernel)."""
+    """33^3 planar output == interleaved output (the default component-split
+    kernels write either layout; tails and odd sizes take the per-pixel kernel)."""
     from paper_1009_0854_b200 import lut
     px = torch.from_numpy(np.random.default_rng(n).integers(0, 256, (n, 3), dtype=np.uint8)).cuda()
     L = lut.build_lut("lab", 33)
@@ -231,7 +231,7 @@ def test_lut_beyond_int32_pixel_count(grid):
 @pytest.mark.parametrize("method", O.METHODS)
 def test_lut_interp_full_cube(P, n, method):
     """The TIMED uint8 kernels (9^3 bank-private copies, 17^3 fixed-point nodes
-    with ghost planes, 33^3 r-split CTA pairs) on all 2^24 colours vs the oracle
+    with ghost planes, 33^3 component-split clusters) on all 2^24 colours vs the oracle
     on the same fp32 lattice values, interleaved; planar output bit-identical
     to interleaved.  The fixed-point formats stay inside 1e-4 (quantisation
     half-step <= 4.4e-5)."""
@@ -307,10 +307,13 @@ def test_lut_nonfinite_lattice(P, n):
         np.testing.assert_allclose(got[fin], ref[fin], rtol=2e-6, atol=1e-4, err_msg=method)
 
 
-def test_lut33_wide_range_lattice_falls_back(P):
-    """33^3 lattice too wide for the fixed-point nodes (x1000): the pair kernel
-    gathers the fp32 lattice from L2 and still matches the oracle."""
+@pytest.mark.parametrize("kernel", ["comp", "pair"])
+def test_lut33_wide_range_lattice_falls_back(P, monkeypatch, kernel):
+    """33^3 lattice too wide for the fixed-point nodes (x1000): the default
+    kernels stage fp32 components, the pair kernel (MACT_LUT33_KERNEL=pair) gathers
+    the fp32 lattice from L2; both match the oracle."""
     import dataclasses
+    monkeypatch.setenv("MACT_LUT33_KERNEL", kernel)
     lt = P["lut"].build_lut("lab", 33)
     wide = dataclasses.replace(lt, values=lt.values * 1000.0, _device={})
     img = np.random.default_rng(5).integers(0, 256, (1 << 18, 3), dtype=np.uint8)
@@ -351,3 +354,25 @@ def test_lut_error_bound_either_format(P, n, scale, method):
     ref = O.interpolate(vals, img, method)
     bound = 1.5 * 5e-5 + 4e-7 * np.abs(ref).max()
     assert np.abs(got - ref).max() <= bound
+
+
+@pytest.mark.parametrize("kernel", ["comp", "pair"])
+@pytest.mark.parametrize("method", O.METHODS)
+def test_lut33_both_kernels(P, monkeypatch, kernel, method):
+    """Both 33^3 interpolation kernels -- the component-split clusters (default)
+    and the r-split CTA pairs (MACT_LUT33_KERNEL=pair) -- against the oracle on the
+    same fp32 lattice: 2^20 random colours plus the cube's corners and faces,
+    interleaved, planar and unaligned (per-pixel kernel) outputs."""
+    monkeypatch.setenv("MACT_LUT33_KERNEL", kernel)
+    lt = P["lut"].build_lut("lab", 33)
+    rng = np.random.default_rng(33)
+    edge = np.array([[a, b, c] for a in (0, 127, 128, 255) for b in (0, 128, 255) for c in (0, 1, 254, 255)], np.uint8)
+    img = np.concatenate([rng.integers(0, 256, ((1 << 20) + 5, 3), dtype=np.uint8), edge])
+    ref = O.interpolate(lt.values.astype(np.float32).astype(np.float64), img, method)
+    d = dev(img)
+    got = P["lut"].interpolate(lt, d, method).cpu().numpy()
+    check_lab(got, ref)
+    n4 = img.shape[0] // 4 * 4
+    planar = P["lut"].interpolate(lt, d[:n4], method, layout="planar").cpu().numpy()
+    check_lab(planar.T, ref[:n4])
+    check_lab(P["lut"].interpolate(lt, d[1:], method).cpu().numpy(), ref[1:])
