@@ -32,6 +32,9 @@
 #ifndef MACT_LUT_NW
 #define MACT_LUT_NW 16
 #endif
+#ifndef MACT_LUT_NW_TRI17     // 17^3 trilinear (93 KB pair lattice, one CTA per SM): 24 or 31 warps measured slower (138 vs 153 Gpix/s)
+#define MACT_LUT_NW_TRI17 16
+#endif
 #ifndef MACT_LUT_SIN
 #define MACT_LUT_SIN 3
 #endif
@@ -59,6 +62,7 @@ struct LutParams {
 constexpr double kLutQuantTol = 5e-5;
 struct LutQuant {
   float s[3], k[3];
+  float s255[3];   // S_c / 255 (the 17^3 trilinear lerps scale code differences by S_c rb / 255)
   int on;
 };
 // q_c = rint((v_c - lo_c) / S_c), the quotient taken as a product with the
@@ -83,6 +87,14 @@ __device__ __forceinline__ uint32_t mad_hi_u32(uint32_t a, uint32_t b, uint32_t 
   uint32_t r;   // hi(a * b) + c on the FMA pipe (IMAD.HI), where a shift + add would take the ALU pipe
   asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
   return r;
+}
+// F_c = 2^23 + q_c of one node (exact floats), the integer part of the decode below.
+__device__ __forceinline__ void lut_quant_f(uint2 w, float2& f01, float& f2) {
+  uint32_t t0;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(t0) : "r"(w.x), "r"(1u << 11));
+  f01.x = __uint_as_float(mad_hi_u32(t0, 1u << 21, 0x4B000000u));
+  f01.y = __uint_as_float((__funnelshift_r(w.x, w.y, 21) & 0x1FFFFFu) | 0x4B000000u);
+  f2 = __uint_as_float(mad_hi_u32(w.y, 1u << 22, 0x4B000000u));
 }
 __device__ __forceinline__ Node2 lut_quant_unpack2(const LutQuant& q, uint2 w) {
   // The kernel is ALU-pipe bound, so q0 and q2 are extracted on the FMA pipe
@@ -136,6 +148,7 @@ __device__ __forceinline__ void lut_quant_setup(const float4* lat, int nn, LutQu
       const float kc = __double2float_rd(lo - (double)sc * 8388608.0);
       q.s[c] = sc;
       q.k[c] = kc;
+      q.s255[c] = (float)((double)sc / 255.0);
       const double top = ((double)m[c + 3] - ((double)kc + (double)sc * 8388608.0)) / (double)sc;
       if (!((double)sc * 0.5 <= kLutQuantTol) || !isfinite(kc) || !(top <= (double)(1u << bits[c]) - 1.5))
         q.on = 0;
@@ -163,6 +176,11 @@ struct OpLut {
   // fp32 planes.  The choice is made per CTA from the lattice itself, by the
   // same deterministic arithmetic in every CTA.
   static constexpr bool PACK = SMEM && !PRIV;
+  // 17^3 trilinear: b-pair entries e = (node e, node e + 1), 16 bytes, so the 8
+  // corners of a cell are 4 LDS.128 (random LDS.128 9.4 smem cycles against
+  // 2 x 5.2 for the two LDS.64 it replaces) and the interpolation runs as 7
+  // lerps instead of 8 weight products (tri_px below).
+  static constexpr bool PAIR = PACK && METHOD == MACT_LUT_TRILINEAR;
   // 17^3 is staged with one ghost plane per axis (18^3 nodes, copies of the
   // edge nodes), so cell location needs no clamp: p = 255 lands in cell 16 at
   // offset 0, where the ghost nodes carry weight exactly 0 -- the same point
@@ -193,7 +211,8 @@ struct OpLut {
         float2 c01[PACK ? NNG : 1];
         float c2[PACK ? NNG : 1];
       } f;
-      uint2 pk[PACK ? NNG : 1];
+      uint2 pk[PACK && !PAIR ? NNG : 1];
+      uint4 pk2[PAIR ? NNG : 1];
     } u;
     LutQuant q;
     float red[32][6];
@@ -207,7 +226,11 @@ struct OpLut {
       for (int i = threadIdx.x; i < NNG; i += blockDim.x) {   // ghost nodes copy the edge
         const int ir = min(i / (NG * NG), N - 1), ig = min((i / NG) % NG, N - 1), ib = min(i % NG, N - 1);
         const float4 v = __ldg(p.lat + (ir * N + ig) * N + ib);
-        if (q.on) {
+        if (q.on && PAIR) {   // node i and its b neighbour (the last b plane pairs with itself; never used)
+          const float4 v1 = __ldg(p.lat + (ir * N + ig) * N + min(i % NG + 1, N - 1));
+          const uint2 a = lut_quant_pack(q, v), b = lut_quant_pack(q, v1);
+          s->u.pk2[i] = make_uint4(a.x, a.y, b.x, b.y);
+        } else if (q.on) {
           s->u.pk[i] = lut_quant_pack(q, v);
         } else {
           s->u.f.c01[i] = make_float2(v.x, v.y);
@@ -273,6 +296,13 @@ struct OpLut {
     int idx[K];
     float w[K];
     const LutQuant q = quant(s);
+    if constexpr (PAIR) {
+      if (q.on) {
+        const uint32_t c[1][3] = {{r, g, b}};
+        tri_px<1>(c, s, q, o);
+        return;
+      }
+    }
     if (q.on) select<true>(r, g, b, idx, w);
     else select<false>(r, g, b, idx, w);
     auto nd = [&](int i) { return q.on ? node<true>(s, p, i, lane, q) : node<false>(s, p, i, lane, q); };
@@ -296,8 +326,81 @@ struct OpLut {
   static __device__ __forceinline__ void px4w_ctx(uint32_t w0, uint32_t w1, uint32_t w2,
                                                   const Shared* s, uint32_t lane, const Params& p,
                                                   const Ctx& qt, float (*o)[1][3]) {
+    if constexpr (PAIR) {
+      if (qt.on) {
+        const uint32_t c[4][3] = {{byte_of(w0, 0), byte_of(w0, 1), byte_of(w0, 2)},
+                                  {byte_of(w0, 3), byte_of(w1, 0), byte_of(w1, 1)},
+                                  {byte_of(w1, 2), byte_of(w1, 3), byte_of(w2, 0)},
+                                  {byte_of(w2, 1), byte_of(w2, 2), byte_of(w2, 3)}};
+        float r[4][3];
+        tri_px<4>(c, s, qt, r);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          o[t][0][0] = r[t][0]; o[t][0][1] = r[t][1]; o[t][0][2] = r[t][2];
+        }
+        return;
+      }
+    }
     if (PACK && qt.on) px4w_t<PACK>(w0, w1, w2, s, lane, p, qt, o);
     else px4w_t<false>(w0, w1, w2, s, lane, p, qt, o);
+  }
+  // 17^3 trilinear on the b-pair entries.  Along b the lerp runs on the codes:
+  // D = F(b-node) - F(a-node) is exact (integers below 2^24), so
+  //   P_c = (S_c F_a + K_c) + (S_c rb / 255) D_c
+  // is the decoded a-node plus one rounded correction; then g and r lerp the
+  // decoded values, P0 + t (P1 - P0).  Rounding stays far below the fixed-point
+  // half-step.  All loads of the batch are issued before any math.
+  template <int PB>
+  static __device__ __forceinline__ void tri_px(const uint32_t (&c)[PB][3], const Shared* s, const LutQuant& q,
+                                                float (*o)[3]) {
+    constexpr uint32_t SR = NG * NG * 16u, SG = NG * 16u;   // byte strides of the pair entries
+    constexpr float inv255 = 1.0f / 255.0f;
+    uint4 e[PB][4];
+    float tb[PB], tg[PB], tr[PB];
+#pragma unroll
+    for (int t = 0; t < PB; ++t) {
+      int bf, rr, rg, rb;
+      locate_g(c[t][0], c[t][1], c[t][2], bf, rr, rg, rb);
+      tb[t] = (float)rb;
+      tg[t] = (float)rg * inv255;
+      tr[t] = (float)rr * inv255;
+      const uint32_t a = smem_u32(s->u.pk2) + ((uint32_t)bf << 4);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t ak = a + (k >> 1) * SR + (k & 1) * SG;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(e[t][k].x), "=r"(e[t][k].y), "=r"(e[t][k].z), "=r"(e[t][k].w) : "r"(ak));
+      }
+    }
+    const float2 s01 = make_float2(q.s[0], q.s[1]), k01 = make_float2(q.k[0], q.k[1]);
+    const float2 m1 = make_float2(-1.0f, -1.0f);
+#pragma unroll
+    for (int t = 0; t < PB; ++t) {
+      const float2 st01 = __fmul2_rn(make_float2(q.s255[0], q.s255[1]), make_float2(tb[t], tb[t]));
+      const float st2 = q.s255[2] * tb[t];
+      float2 p01[4];
+      float p2[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float2 fa01, fb01;
+        float fa2, fb2;
+        lut_quant_f(make_uint2(e[t][k].x, e[t][k].y), fa01, fa2);
+        lut_quant_f(make_uint2(e[t][k].z, e[t][k].w), fb01, fb2);
+        const float2 va01 = __ffma2_rn(fa01, s01, k01);
+        const float va2 = fmaf(fa2, q.s[2], q.k[2]);
+        p01[k] = __ffma2_rn(st01, __ffma2_rn(fa01, m1, fb01), va01);
+        p2[k] = fmaf(st2, fb2 - fa2, va2);
+      }
+      const float2 g2 = make_float2(tg[t], tg[t]);
+      const float2 q0 = __ffma2_rn(g2, __ffma2_rn(p01[0], m1, p01[1]), p01[0]);
+      const float2 q1 = __ffma2_rn(g2, __ffma2_rn(p01[2], m1, p01[3]), p01[2]);
+      const float q02 = fmaf(tg[t], p2[1] - p2[0], p2[0]);
+      const float q12 = fmaf(tg[t], p2[3] - p2[2], p2[2]);
+      const float2 r01 = __ffma2_rn(make_float2(tr[t], tr[t]), __ffma2_rn(q0, m1, q1), q0);
+      o[t][0] = r01.x;
+      o[t][1] = r01.y;
+      o[t][2] = fmaf(tr[t], q12 - q02, q02);
+    }
   }
   static __device__ __forceinline__ void px4w(uint32_t w0, uint32_t w1, uint32_t w2,
                                               const Shared* s, uint32_t lane, const Params& p,
@@ -1312,7 +1415,8 @@ static int launch_interp(const float* lat, const uint8_t* rgb, float* out, int64
     return lut33_legacy() ? launch_lut33_comp<METHOD>(lat, rgb, out, n, planar, st)
                           : launch_lut33_pair<METHOD>(lat, rgb, out, n, planar, st);
   else
-    return launch_stream_t<OpLut<N, METHOD>, MACT_LUT_NW, (N <= 9 ? 2 : 1), MACT_LUT_SIN, 1>(
+    return launch_stream_t<OpLut<N, METHOD>, (OpLut<N, METHOD>::PAIR ? MACT_LUT_NW_TRI17 : MACT_LUT_NW),
+                           (N <= 9 ? 2 : 1), MACT_LUT_SIN, 1>(
         rgb, outs, n, planar, p, st, "lut_interp");
 }
 

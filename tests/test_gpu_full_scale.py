@@ -4,7 +4,7 @@ grays included, all three transforms), the fused GPU reduction against the CPU o
 on the same bytes ("oracle ε computed once on CPU", harness.py:77-122).
 
 - the fp64 fidelity candidate (the reference's own arithmetic) must reproduce the
-  oracle's figures: identical count / NaN count / argmax, mean and max to 1e-12;
+  oracle's figures: identical count / NaN count / argmax, max to 1e-12 and mean to 1e-9;
 - the fp32 throughput outputs may move each pixel by the north-star tolerance
   (1e-4 on L*a*b*, 1e-5 normalised on H/S/I and SCT), so each figure is checked
   to that tolerance (x sqrt(3) for the ΔE*ab distance).
@@ -80,8 +80,9 @@ def _check(space, gpu32, gpu64, ref):
         # fidelity mode: the reference's figures (the per-pixel outputs are bit-identical;
         # the ΔE*ab square root / sum order of the device distance may move the last bits)
         assert (b["count"], b["nan"], b["argmax"]) == (r["count"], r["nan"], r["argmax"]), (space, c, b, r)
-        for k in ("mean", "max"):
-            assert abs(b[k] - r[k]) <= 1e-12 * max(abs(r[k]), 1e-300), (space, c, k, b, r)
+        # (max: one distance; mean: a 10^8-term fp64 sum, tree order vs pairwise numpy)
+        for k, rt in (("mean", 1e-9), ("max", 1e-12)):
+            assert abs(b[k] - r[k]) <= rt * max(abs(r[k]), 1e-300), (space, c, k, b, r)
         # throughput mode: within the per-pixel tolerance
         t = _tol(space, c)
         assert (a["count"], a["nan"]) == (r["count"], r["nan"]), (space, c, a, r)
