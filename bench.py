@@ -179,6 +179,44 @@ def cpu_run(fns, space: str, images, budget_s: float, threads: int):
     return px, dt
 
 
+def pcie_bandwidth(dev, nbytes: int = 1 << 30, reps: int = 3):
+    """Pinned host <-> device copy bandwidth (GB/s), CUDA events, best of `reps`:
+    each direction alone and both at once on two streams."""
+    import torch
+
+    h_a = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h_b = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    res = {"h2d": 0.0, "d2h": 0.0, "h2d_concurrent": 0.0, "d2h_concurrent": 0.0}
+
+    def run(h2d: bool, d2h: bool):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        torch.cuda.synchronize(dev)
+        if h2d:
+            ev[0].record(s1)
+            with torch.cuda.stream(s1):
+                d_a.copy_(h_a, non_blocking=True)
+            ev[1].record(s1)
+        if d2h:
+            ev[2].record(s2)
+            with torch.cuda.stream(s2):
+                h_b.copy_(d_b, non_blocking=True)
+            ev[3].record(s2)
+        torch.cuda.synchronize(dev)
+        bw = lambda a, b: nbytes / (a.elapsed_time(b) / 1e3) / 1e9
+        return (bw(ev[0], ev[1]) if h2d else 0.0), (bw(ev[2], ev[3]) if d2h else 0.0)
+
+    for _ in range(reps + 1):
+        res["h2d"] = max(res["h2d"], run(True, False)[0])
+        res["d2h"] = max(res["d2h"], run(False, True)[1])
+        a, b = run(True, True)
+        res["h2d_concurrent"], res["d2h_concurrent"] = max(res["h2d_concurrent"], a), max(res["d2h_concurrent"], b)
+    del h_a, h_b, d_a, d_b
+    return res
+
+
 # --------------------------------------------------------------------- our arm
 def run_ours(args, wl):
     import numpy as np
@@ -213,11 +251,14 @@ def run_ours(args, wl):
     xf = x.reshape(-1, 3)
     space = wl["space"]
     n_out = 3 if space == "all" else (2 if space == "hsi+sct" else 1)
-    outs = [torch.empty((n_local, 3), dtype=torch.float32, device=dev) for _ in range(n_out)]
+    f64 = args.out_dtype == "float64"
+    out_b = 24 if f64 else 12                       # bytes per pixel and transform written
+    outs = [torch.empty((n_local, 3), dtype=torch.float64 if f64 else torch.float32, device=dev)
+            for _ in range(n_out)]
     # L2 rule: a step whose inputs + outputs are below 2x the 126 MB L2 rotates
     # over a pool of copies (distinct input and output buffers) whose footprint
     # exceeds 512 MB, so every step reads and writes lines that are not L2-resident.
-    step_bytes = n_local * (3 + 12 * n_out)
+    step_bytes = n_local * (3 + out_b * n_out)
     pool_n = 1 if step_bytes >= L2_POOL_BYTES else -(-L2_POOL_BYTES // step_bytes)
     pool = [(xf, outs)] + [(xf.clone(), [torch.empty_like(o) for o in outs]) for _ in range(pool_n - 1)]
     lt = lut.build_lut("lab", args.lut_grid) if space == "lut" else None
@@ -234,8 +275,16 @@ def run_ours(args, wl):
         elif space == "hsi+sct":     # fused pair: one read, two outputs (lab = NULL)
             _lib.check(lib.mact_all_fast(xf.data_ptr(), None, outs[0].data_ptr(), outs[1].data_ptr(),
                                          n_local, cfg.coeffs, 0, sp_ptr))
+        elif space == "lab" and f64:     # fidelity mode: the reference's fp64 arithmetic
+            _lib.check(lib.mact_fast_f64(_lib.SPACES["lab"], xf.data_ptr(), _lib.DTYPE_U8, outs[0].data_ptr(),
+                                         n_local, cfg.coeffs, 0, sp_ptr))
         elif space == "lab":
             _lib.check(lib.mact_lab_fast(xf.data_ptr(), 0, outs[0].data_ptr(), n_local, cfg.coeffs, 0, sp_ptr))
+        elif f64:
+            lat = lt.lattice64(dev)
+            _lib.check(lib.mact_lut_interp_real(lat.data_ptr(), args.lut_grid, lut_code, 0, xf.data_ptr(),
+                                                _lib.DTYPE_U8, outs[0].data_ptr(), _lib.DTYPE_F64, n_local, 0,
+                                                sp_ptr))
         else:
             lat = lt.lattice(dev)
             _lib.check(lib.mact_lut_interp(lat.data_ptr(), args.lut_grid, lut_code, xf.data_ptr(),
@@ -249,7 +298,11 @@ def run_ours(args, wl):
     ev_r0, ev_r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev_r0.record(st)
     if space in ("lab", "all", "lut"):
-        cand = harness.LutCandidate(lt, args.lut_method) if space == "lut" else harness.fast_candidate("lab")
+        if space == "lut":
+            cand = (harness.LutCandidate(lt, args.lut_method) if not f64 else
+                    (lambda p: lut.interpolate(lt, p, args.lut_method, out_dtype="float64")))
+        else:
+            cand = harness.fast_candidate("lab", out_dtype=args.out_dtype)
         partial_sets.append(("lab", harness.reduce_partials("lab", cand, None, xf, index_base=base)))
         if space == "lut":   # config 3: "compared with MACT on the same pixels"
             partial_sets.append(("mact", harness.reduce_partials("lab", harness.fast_candidate("lab"), None, xf,
@@ -340,25 +393,30 @@ def run_ours(args, wl):
     # every workload is ONE launch per step (C2/C5 run the transforms fused from one read)
     kern_ms = statistics.mean(step_ms)
     value = n_total * transforms * args.steps / (total_ms / 1e3) / 1e9
-    bytes_px = 3 + 12 * transforms                           # uint8 in once + fp32 (N,3) per transform
+    bytes_px = 3 + out_b * transforms                        # uint8 in once + (N,3) out per transform
     achieved = n_local * bytes_px / (kern_ms / 1e3) / 1e9
-    traffic, traffic_b = None, None
+    traffic, traffic_b, traffic_src = None, None, None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
+    tkey = args.workload + (f"_{args.lut_grid}_{args.lut_method}" if space == "lut" else "") + ("_f64" if f64 else "")
     if os.path.exists(prof) and world == 1:
-        t = json.load(open(prof)).get(args.workload)
-        if t:   # ncu dram bytes per launch of this kernel, as GB/s over the live launch time
+        t = json.load(open(prof)).get(tkey)
+        if t:   # ncu dram bytes per launch of this kernel (one --set full capture), over the live launch time
             traffic_b = t["bytes_per_launch"]
             traffic = round(traffic_b / (kern_ms / 1e3) / 1e9, 1)
+            traffic_src = (f"profiles/traffic.json[{tkey}]: {t.get('source')} ({t.get('kernel', '')[:40]}), "
+                           f"captured at commit {t.get('commit', 'unrecorded')}")
 
     # ---------------- end to end through the public API with HOST buffers
     e2e = None
     if args.e2e_steps > 0:
         sp1 = {"lab": "lab", "all": "lab", "hsi+sct": "hsi"}.get(space, "lut")
-        fn = {"lab": fast.rgb_to_lab_fast, "hsi": fast.rgb_to_hsi_fast,
-              "lut": lambda p, out: lut.interpolate(lt, p, args.lut_method, out=out)}[sp1]
+        od = {"out_dtype": "float64"} if f64 else {}
+        fn = {"lab": lambda p, out: fast.rgb_to_lab_fast(p, out=out, **od),
+              "hsi": fast.rgb_to_hsi_fast,
+              "lut": lambda p, out: lut.interpolate(lt, p, args.lut_method, out=out, **od)}[sp1]
         h_in = torch.empty((n_local, 3), dtype=torch.uint8).pin_memory()
         h_in.copy_(xf.cpu())
-        h_out = torch.empty((n_local, 3), dtype=torch.float32).pin_memory()
+        h_out = torch.empty((n_local, 3), dtype=torch.float64 if f64 else torch.float32).pin_memory()
         hi, ho = h_in.numpy(), h_out.numpy()
         fn(hi[: min(n_local, 1 << 22)], out=ho[: min(n_local, 1 << 22)])   # warm the executor
         torch.cuda.synchronize(dev)
@@ -368,8 +426,19 @@ def run_ours(args, wl):
             fn(hi, out=ho)
         torch.cuda.synchronize(dev)
         dt = parallel.max_over_ranks(time.perf_counter() - t, cdev)
-        e2e = {"value": n_total * args.e2e_steps / dt / 1e9, "unit": "Gpixels/s",
-               "h2d_bytes_per_step": n_total * 3, "d2h_bytes_per_step": n_total * 12,
+        bw = pcie_bandwidth(dev)
+        # the executor overlaps H2D, kernel and D2H on separate engines, so the ceiling is
+        # the slower direction at its own best pinned-copy bandwidth (the concurrent
+        # figures are reported beside it)
+        e2e_peak = min(bw["h2d"] / 3, bw["d2h"] / out_b)      # Gpix/s per GPU
+        e2e_val = n_total * args.e2e_steps / dt / 1e9
+        e2e = {"value": e2e_val, "unit": "Gpixels/s",
+               "h2d_bytes_per_step": n_total * 3, "d2h_bytes_per_step": n_total * out_b,
+               "roofline": {"bound": "pcie", "achieved": round(e2e_val / world, 3), "peak": round(e2e_peak, 3),
+                            "unit": "Gpixels/s per GPU", "frac": round(e2e_val / world / e2e_peak, 4),
+                            **{k + "_gbs": round(v, 1) for k, v in bw.items()},
+                            "method": "pinned 1 GiB copies, CUDA events, best of 3: each direction alone "
+                                      "(the ceiling) and both at once"},
                "api": (f"paper_1009_0854_b200.fast.rgb_to_{sp1}_fast" if sp1 != "lut" else
                        "paper_1009_0854_b200.lut.interpolate") + "(numpy pinned, out=numpy pinned)",
                "steps": args.e2e_steps, "transform": sp1}
@@ -395,7 +464,7 @@ def run_ours(args, wl):
             "metric": METRIC, "value": round(value, 3), "unit": "Gpixels/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(total_ms / args.steps, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "u8->f32",
+            "dtype": "u8->f64" if f64 else "u8->f32",
             "data": "synthetic (generated on device, seeded per image)",
             "config": {"workload": f"{args.workload}: {wl['desc']}", "pixels": n_total,
                        "transforms_per_step": transforms, "layout": "interleaved (N,3) fp32",
@@ -410,7 +479,7 @@ def run_ours(args, wl):
                               "> 2x the 126 MB L2), so no step finds its data in L2")},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                          "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
-                         "traffic_bytes_per_launch": traffic_b,
+                         "traffic_bytes_per_launch": traffic_b, "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": n_local * bytes_px,
                          "peak_source": hbm_src, "algorithmic_bytes_per_px": bytes_px,
                          "kernel_ms_per_launch": round(kern_ms, 4),
@@ -517,6 +586,8 @@ def main():
     ap.add_argument("--lut-grid", type=int, choices=[9, 17, 33], default=17, help="c3 only")
     ap.add_argument("--lut-method", choices=["trilinear", "prism", "pyramidal", "tetrahedral"],
                     default="tetrahedral", help="c3 only")
+    ap.add_argument("--out-dtype", choices=["float32", "float64"], default="float32",
+                    help="float64 = fidelity mode (the reference's fp64 arithmetic, 24 B/px out); c1/c3/c4")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=None,
@@ -533,6 +604,8 @@ def main():
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; refusing to report a mismatched line",
               file=sys.stderr)
         sys.exit(2)
+    if args.out_dtype == "float64" and WORKLOADS[args.workload]["space"] not in ("lab", "lut"):
+        ap.error("--out-dtype float64 is measured on the single-transform workloads c1 / c3 / c4")
     wl = dict(WORKLOADS[args.workload])
     wl["desc"] = wl["desc"].format(grid=args.lut_grid, method=args.lut_method)
     if args.impl == "reference":

@@ -279,6 +279,11 @@ int mact_host_ctx_create(int device, int64_t chunk_px, int nstreams, MactHostCtx
 int mact_host_ctx_destroy(MactHostCtx* ctx);
 int mact_transform_host(MactHostCtx* ctx, int op, const uint8_t* host_rgb, float* host_out,
                         int64_t n, const MactCoeffs* c, int layout);
+/* The same with fp64 results in the reference's own arithmetic (mact_fast_f64):
+ * what mact.fast.rgb_to_*_fast returns for 8-bit pixels, bit for bit
+ * (fast.py:86-107, :125-148, :188-203). */
+int mact_transform_host_f64(MactHostCtx* ctx, int op, const uint8_t* host_rgb, double* host_out,
+                            int64_t n, const MactCoeffs* c, int layout);
 /* mact.lut.interpolate over HOST buffers (lut.py:341-350) through the same
  * chunk pipeline; `lattice` is the device (n^3,4) lattice, linear destination. */
 int mact_lut_interp_host(MactHostCtx* ctx, const float* lattice, int grid_n, int method,

@@ -86,14 +86,15 @@ def check_out(out, lead: tuple, layout: str, device):
     return out
 
 
-def host_out(out, lead: tuple, layout: str):
-    """Validate (or allocate) a numpy float32 output for the host executor."""
+def host_out(out, lead: tuple, layout: str, dtype=np.float32):
+    """Validate (or allocate) a numpy float32 / float64 output for the host executor."""
     shape = lead + (3,) if layout == "interleaved" else (3,) + lead
+    dtype = np.dtype(dtype)
     if out is None:
-        return np.empty(shape, dtype=np.float32)
-    if not isinstance(out, np.ndarray) or out.dtype != np.float32 or out.shape != shape \
+        return np.empty(shape, dtype=dtype)
+    if not isinstance(out, np.ndarray) or out.dtype != dtype or out.shape != shape \
             or not out.flags.c_contiguous:
-        raise ValueError(f"out must be a C-contiguous float32 array of shape {shape}")
+        raise ValueError(f"out must be a C-contiguous {dtype.name} array of shape {shape}")
     return out
 
 

@@ -103,6 +103,7 @@ _SIGNATURES = {
     "mact_host_ctx_create": (_i, [_i, _i64, _i, C.POINTER(_vp)]),
     "mact_host_ctx_destroy": (_i, [_vp]),
     "mact_transform_host": (_i, [_vp, _i, _vp, _vp, _i64, C.POINTER(MactCoeffs), _i]),
+    "mact_transform_host_f64": (_i, [_vp, _i, _vp, _vp, _i64, C.POINTER(MactCoeffs), _i]),
     "mact_lut_interp_host": (_i, [_vp, _vp, _i, _i, _vp, _vp, _i64, _i]),
     "mact_last_error": (C.c_char_p, []),
     "mact_version": (_i, []),

@@ -7,10 +7,31 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "../../include/mact_cuda.h"
 
 namespace mact {
+
+// Device-side invariant checks of the checked build (scripts/hazard_check.sh:
+// MACT_NVCC_DEFS=-DMACT_CHECKS MACT_LIB_TAG=checks).  Shared-memory gather
+// indices, DSMEM exchange sizes and ring positions are asserted there; a
+// failure prints the condition and traps (the launch then reports an error).
+// The product build compiles them away.
+#ifdef MACT_CHECKS
+#define MACT_DCHECK(cond)                                                                              \
+  do {                                                                                                 \
+    if (!(cond)) {                                                                                     \
+      printf("MACT_DCHECK %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x,        \
+             (int)threadIdx.x, #cond);                                                                  \
+      __trap();                                                                                        \
+    }                                                                                                  \
+  } while (0)
+#else
+#define MACT_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
 
 constexpr double kPi = 3.14159265358979311600;   // np.pi
 constexpr double kTwoPi = 2.0 * kPi;

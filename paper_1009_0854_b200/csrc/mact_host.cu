@@ -23,13 +23,15 @@ struct MactHostCtx {
   std::vector<cudaStream_t> streams;
   std::vector<cudaEvent_t> done;        // per stream: last D2H of that slot finished
   std::vector<uint8_t*> d_in;
-  std::vector<float*> d_out;
+  std::vector<char*> d_out;             // chunk x 24 B: fp32 (12 B/px) or fp64 (24 B/px) results
   std::vector<uint8_t*> h_in;           // pinned bounce buffers (pageable callers)
-  std::vector<float*> h_out;
+  std::vector<char*> h_out;
   std::mutex mu;                        // one call at a time owns the streams and staging buffers
 };
 
 using namespace mact;
+
+static constexpr size_t kMaxOutPx = 24;   // bytes per pixel of a staging slot (fp64 (N,3))
 
 // Parallel memcpy for the pageable staging path: one host thread moves ~5-10
 // GB/s (less while first-touch page faults land in a fresh numpy array), so
@@ -76,14 +78,14 @@ extern "C" int mact_host_ctx_create(int device, int64_t chunk_px, int nstreams, 
     cudaStream_t st;
     cudaEvent_t ev;
     uint8_t* di = nullptr;
-    float* dout = nullptr;
+    char* dout = nullptr;
     if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) break;
     c->streams.push_back(st);
     if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) break;
     c->done.push_back(ev);
     if ((e = cudaMalloc(&di, (size_t)chunk_px * 3)) != cudaSuccess) break;
     c->d_in.push_back(di);
-    if ((e = cudaMalloc(&dout, (size_t)chunk_px * 12)) != cudaSuccess) break;
+    if ((e = cudaMalloc(&dout, (size_t)chunk_px * kMaxOutPx)) != cudaSuccess) break;
     c->d_out.push_back(dout);
   }
   cudaSetDevice(prev);
@@ -116,9 +118,9 @@ static int ensure_bounce(MactHostCtx* c) {
   if (!c->h_in.empty()) return MACT_OK;
   for (int s = 0; s < c->nstreams; ++s) {
     uint8_t* hi = nullptr;
-    float* ho = nullptr;
+    char* ho = nullptr;
     cudaError_t e = cudaHostAlloc(&hi, (size_t)c->chunk * 3, cudaHostAllocDefault);
-    if (e == cudaSuccess) e = cudaHostAlloc(&ho, (size_t)c->chunk * 12, cudaHostAllocDefault);
+    if (e == cudaSuccess) e = cudaHostAlloc(&ho, (size_t)c->chunk * kMaxOutPx, cudaHostAllocDefault);
     if (e != cudaSuccess) return set_error(MACT_ECUDA, "pinned bounce buffers: %s", cudaGetErrorString(e));
     c->h_in.push_back(hi);
     c->h_out.push_back(ho);
@@ -136,20 +138,23 @@ static int run_kernel(int op, const uint8_t* din, float* dout, int64_t n, const 
   return set_error(MACT_EBADARG, "unknown transform %d", op);
 }
 
-// D2H of one chunk's result; planar output lands in 3 strided host planes.
-static cudaError_t copy_out(float* host_out, const float* dout, int64_t off, int64_t m, int64_t n,
-                            int layout, cudaStream_t st) {
+// D2H of one chunk's result (es = 4 or 8 bytes per component); planar output
+// lands in 3 strided host planes.
+static cudaError_t copy_out(char* host_out, const char* dout, int64_t off, int64_t m, int64_t n,
+                            int layout, size_t es, cudaStream_t st) {
   if (layout == MACT_LAYOUT_INTERLEAVED)
-    return cudaMemcpyAsync(host_out + 3 * off, dout, (size_t)m * 12, cudaMemcpyDeviceToHost, st);
-  return cudaMemcpy2DAsync(host_out + off, (size_t)n * 4, dout, (size_t)m * 4, (size_t)m * 4, 3,
+    return cudaMemcpyAsync(host_out + 3 * off * es, dout, (size_t)m * 3 * es, cudaMemcpyDeviceToHost, st);
+  return cudaMemcpy2DAsync(host_out + off * es, (size_t)n * es, dout, (size_t)m * es, (size_t)m * es, 3,
                            cudaMemcpyDeviceToHost, st);
 }
 
 // The chunk pipeline shared by every host entry point; `launch` runs the
-// kernel of one chunk (device in, device out, pixels, stream).
+// kernel of one chunk (device in, device out, pixels, stream); es = bytes per
+// output component (4: fp32, 8: the fp64 fidelity mode).
 template <class Launch>
-static int stream_host(MactHostCtx* c, const uint8_t* host_rgb, float* host_out, int64_t n,
-                       int layout, Launch&& launch) {
+static int stream_host(MactHostCtx* c, const uint8_t* host_rgb, void* host_out_v, int64_t n,
+                       int layout, size_t es, Launch&& launch) {
+  char* host_out = static_cast<char*>(host_out_v);
   std::lock_guard<std::mutex> guard(c->mu);
   NvtxRange range("mact_host_stream");
   int prev = 0;
@@ -177,9 +182,10 @@ static int stream_host(MactHostCtx* c, const uint8_t* host_rgb, float* host_out,
     if (e != cudaSuccess) return set_error(MACT_ECUDA, "d2h: %s", cudaGetErrorString(e));
     const int64_t off = k * chunk, m = std::min<int64_t>(chunk, n - off);
     if (layout == MACT_LAYOUT_INTERLEAVED) {
-      par_memcpy(host_out + 3 * off, c->h_out[s], (size_t)m * 12);
+      par_memcpy(host_out + 3 * off * es, c->h_out[s], (size_t)m * 3 * es);
     } else {
-      for (int p = 0; p < 3; ++p) par_memcpy(host_out + p * n + off, c->h_out[s] + p * m, (size_t)m * 4);
+      for (int p = 0; p < 3; ++p)
+        par_memcpy(host_out + (p * n + off) * es, c->h_out[s] + p * m * es, (size_t)m * es);
     }
     pending[s] = -1;
     return MACT_OK;
@@ -192,14 +198,14 @@ static int stream_host(MactHostCtx* c, const uint8_t* host_rgb, float* host_out,
     if (direct) {
       e = cudaMemcpyAsync(c->d_in[s], host_rgb + 3 * off, (size_t)m * 3, cudaMemcpyHostToDevice, st);
       if (e == cudaSuccess) rc = launch(c->d_in[s], c->d_out[s], m, st);
-      if (rc == MACT_OK && e == cudaSuccess) e = copy_out(host_out, c->d_out[s], off, m, n, layout, st);
+      if (rc == MACT_OK && e == cudaSuccess) e = copy_out(host_out, c->d_out[s], off, m, n, layout, es, st);
     } else {
       if ((rc = drain(s)) != MACT_OK) break;
       par_memcpy(c->h_in[s], host_rgb + 3 * off, (size_t)m * 3);
       e = cudaMemcpyAsync(c->d_in[s], c->h_in[s], (size_t)m * 3, cudaMemcpyHostToDevice, st);
       if (e == cudaSuccess) rc = launch(c->d_in[s], c->d_out[s], m, st);
       if (rc == MACT_OK && e == cudaSuccess)
-        e = cudaMemcpyAsync(c->h_out[s], c->d_out[s], (size_t)m * 12, cudaMemcpyDeviceToHost, st);
+        e = cudaMemcpyAsync(c->h_out[s], c->d_out[s], (size_t)m * 3 * es, cudaMemcpyDeviceToHost, st);
       if (e == cudaSuccess) e = cudaEventRecord(c->done[s], st);
       pending[s] = k;
     }
@@ -221,9 +227,22 @@ extern "C" int mact_transform_host(MactHostCtx* c, int op, const uint8_t* host_r
     return set_error(MACT_EBADARG, "bad argument");
   if (n == 0) return MACT_OK;
   if (op < 0 || op > 2) return set_error(MACT_EBADARG, "unknown transform %d", op);
-  return stream_host(c, host_rgb, host_out, n, layout,
-                     [&](const uint8_t* din, float* dout, int64_t m, cudaStream_t st) {
-                       return run_kernel(op, din, dout, m, cf, layout, st);
+  return stream_host(c, host_rgb, host_out, n, layout, 4,
+                     [&](const uint8_t* din, char* dout, int64_t m, cudaStream_t st) {
+                       return run_kernel(op, din, reinterpret_cast<float*>(dout), m, cf, layout, st);
+                     });
+}
+
+extern "C" int mact_transform_host_f64(MactHostCtx* c, int op, const uint8_t* host_rgb, double* host_out,
+                                       int64_t n, const MactCoeffs* cf, int layout) {
+  if (!c || n < 0 || (n > 0 && (!host_rgb || !host_out)) || !cf)
+    return set_error(MACT_EBADARG, "bad argument");
+  if (n == 0) return MACT_OK;
+  if (op < 0 || op > 2) return set_error(MACT_EBADARG, "unknown transform %d", op);
+  return stream_host(c, host_rgb, host_out, n, layout, 8,
+                     [&](const uint8_t* din, char* dout, int64_t m, cudaStream_t st) {
+                       return mact_fast_f64(op, din, MACT_DTYPE_U8, reinterpret_cast<double*>(dout), m, cf,
+                                            layout, st);
                      });
 }
 
@@ -232,8 +251,9 @@ extern "C" int mact_lut_interp_host(MactHostCtx* c, const float* lattice, int gr
   if (!c || !lattice || n < 0 || (n > 0 && (!host_rgb || !host_out)))
     return set_error(MACT_EBADARG, "bad argument");
   if (n == 0) return MACT_OK;
-  return stream_host(c, host_rgb, host_out, n, layout,
-                     [&](const uint8_t* din, float* dout, int64_t m, cudaStream_t st) {
-                       return mact_lut_interp(lattice, grid_n, method, din, dout, m, layout, st);
+  return stream_host(c, host_rgb, host_out, n, layout, 4,
+                     [&](const uint8_t* din, char* dout, int64_t m, cudaStream_t st) {
+                       return mact_lut_interp(lattice, grid_n, method, din, reinterpret_cast<float*>(dout), m,
+                                              layout, st);
                      });
 }

@@ -14,10 +14,11 @@
 // for that format, as two planes, (c0, c1) float2 and c2 float (59 KB): one
 // LDS.64 + one LDS.32 per node.  Random gathers are bank-conflict bound: on
 // B200 a random warp LDS.64 costs 5.2 smem cycles, LDS.64 + LDS.32 7.9, one
-// LDS.128 of a padded float4 node 9.4 (tools/ldsbench.cu).  33^3 (575 KB)
-// exceeds a CTA's 227 KB: a 3-CTA cluster holds one component per CTA
-// (k_lut33_comp), with the L1/L2 gather kernel only for tails and unaligned
-// buffers.
+// LDS.128 of a padded float4 node 9.4 (tools/ldsbench.cu).  33^3 exceeds a
+// CTA's 227 KB even as fixed-point nodes (287 KB): a 2-CTA cluster holds half
+// of the r-planes per CTA and each pixel is interpolated by the CTA holding
+// its cell (k_lut33_pair); planar output uses 3 independent CTAs holding one
+// fp32 component each (k_lut33_planar).
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -243,6 +244,7 @@ struct OpLut {
   template <bool PK = false>
   static __device__ __forceinline__ Node2 node(const Shared* s, const Params& p, int i, uint32_t lane,
                                                const LutQuant& q) {
+    MACT_DCHECK(i >= 0 && i < (PRIV || !SMEM ? N * N * N : NNG));
     if constexpr (PRIV) {
       const float4 v = s->lat[(i << 3) | (lane & 7)];
       return Node2{make_float2(v.x, v.y), v.z};
@@ -364,6 +366,7 @@ struct OpLut {
       tb[t] = (float)rb;
       tg[t] = (float)rg * inv255;
       tr[t] = (float)rr * inv255;
+      MACT_DCHECK(bf >= 0 && bf + NG * NG + NG < NNG);
       const uint32_t a = smem_u32(s->u.pk2) + ((uint32_t)bf << 4);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -454,34 +457,36 @@ struct OpLut {
 // 22-43 Gpix/s: DSMEM serves scattered 8-byte requests slowly; it is used
 // here only for one contiguous bulk copy per warp and slice.)
 //
-// Warp w of rank 0 and warp w of rank 1 work on the same 256-pixel slices.
-// Per slice, each warp:
-//   1. loads the slice (6 words per lane, prefetched one slice ahead) and
+// Warp w of rank 0 and warp w of rank 1 work on the same 128-pixel slices
+// (lane L holds pixels 4L..4L+3, 12 bytes; rank 0 owns the output of pixels
+// 0..63 = lanes 0..15, rank 1 of 64..127).  Per slice, each warp:
+//   1. loads the slice (3 words per lane, prefetched one slice ahead) and
 //      compacts ITS pixels (r >> 7 == rank) into a list, in pixel order, with
 //      ballots and prefix popcounts;
 //   2. interpolates the list, 32 entries per round (the 17^3 code: integer
 //      cell location and selection, LDS.64 fixed-point nodes, FFMA2), writing
-//      results for its own half of the slice (rank 0: pixels 0..127, rank 1:
-//      128..255) to `own` and those for the partner's half to `send`, both in
-//      list order;
-//   3. ships `send` with ONE bulk copy into the partner warp's `recv`
+//      each result to `res` in list order -- entries of half 1 shifted by
+//      pad = -T0 mod 4, so the partner's part of the list is a 16-byte
+//      aligned run (rank 0 ships entries T0.., rank 1 entries 0..T0-1);
+//   3. ships that run with ONE bulk copy into the partner warp's `recv`
 //      (cp.async.bulk shared::cta -> shared::cluster, completing on the
 //      partner's mbarrier);
-//   4. merges its half from `own` and `recv` by the same ballots (a pixel's
-//      rank among ours / theirs) and stores it with STG.128;
+//   4. merges its half on the 16 lanes that hold it (a pixel's rank among
+//      ours / theirs comes from the same ballots) and stores it with STG.128;
 //   5. tells the partner its `recv` is free (remote mbarrier arrive).
 // Both sides know every count from the same input bytes, so the receiver
 // arms its barrier with exactly the bytes the sender will ship.  Selection
 // runs once per pixel; each CTA does half the interpolation work plus
-// ~1/4 of the output bytes over DSMEM (bulk).
+// ~1/4 of the output bytes over DSMEM (bulk).  2.9 KB of buffers per warp
+// leave room for 24 warps next to the 148 KB of planes.
 constexpr int kL33Planes = 17;
 constexpr int kL33Plane = 33 * 33;
 #ifndef MACT_LUT33_NW
-#define MACT_LUT33_NW 12
+#define MACT_LUT33_NW 24
 #endif
-constexpr int kP33NW = MACT_LUT33_NW;          // warps per CTA (smem: 148 KB planes + 5.5 KB per warp)
-constexpr int kP33Slice = 256;                 // pixels per warp slice
-constexpr int kP33Half = 128;
+constexpr int kP33NW = MACT_LUT33_NW;          // warps per CTA (smem: 148 KB planes + 2.9 KB per warp)
+constexpr int kP33Slice = 128;                 // pixels per warp slice
+constexpr int kP33Half = 64;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -530,10 +535,9 @@ struct Lut33Sel {
 };
 
 struct alignas(16) P33Warp {
-  uint32_t list[kP33Slice];     // packed r | g << 8 | b << 16 of this CTA's pixels, slice order
-  float own[kP33Half * 3];      // results for my half of the slice, list order
-  float send[kP33Half * 3];     // results for the partner's half, list order (bulk-copied)
-  float recv[kP33Half * 3];     // the partner's results for my half, its list order
+  uint32_t list[kP33Slice];         // packed r | g << 8 | b << 16 of this CTA's pixels, slice order
+  float recv[kP33Half * 3];         // the partner's results for my half, its list order
+  float res[(kP33Slice + 5) * 3];   // my results, list order, half-1 entries shifted by pad (+ bulk slack)
 };
 struct P33Shared {
   P33Warp wb[kP33NW];
@@ -558,12 +562,17 @@ __device__ __forceinline__ Node2 p33_node(uint32_t pk_base, const float4* lat4, 
   }
 }
 
-// Interpolate list entries lane + 32 q (q < Q) and file each result in own / send.
+// Interpolate list entries lane + 32 q (q < Q) into res (entry j at j + pad if j >= T0).
 template <int METHOD, bool PK>
-__device__ __forceinline__ void p33_rounds(P33Warp& B, int M, int T0, uint32_t rank, uint32_t lane,
+__device__ __forceinline__ void p33_rounds(P33Warp& B, int M, int T0, int pad, uint32_t rank, uint32_t lane,
                                            uint32_t pk_base, const float4* lat4, const LutQuant& q) {
   constexpr int K = LutK<METHOD>::K;
-  constexpr int PB = K > 6 ? 2 : 4;              // entries per lane in flight
+#ifndef MACT_P33_PB
+#define MACT_P33_PB 1
+#endif
+  // entries per lane in flight: M ~ 64 entries per 128-px slice, so rounds of
+  // 32 x PB waste lanes on the last round (PB = 2: 50-75 % use when M > 64)
+  constexpr int PB = K > 6 ? 1 : MACT_P33_PB;
   const int Q = (M + 31) >> 5;
   for (int q0 = 0; q0 < Q; q0 += PB) {
     int idx[PB][K];
@@ -580,7 +589,10 @@ __device__ __forceinline__ void p33_rounds(P33Warp& B, int M, int T0, uint32_t r
 #pragma unroll
     for (int t = 0; t < PB; ++t)
 #pragma unroll
-      for (int k = 0; k < K; ++k) v[t][k] = p33_node<PK>(pk_base, lat4, q, idx[t][k]);
+      for (int k = 0; k < K; ++k) {
+        MACT_DCHECK(!PK || (uint32_t)(idx[t][k] - 16 * kL33Plane * (int)rank) < (uint32_t)(kL33Planes * kL33Plane));
+        v[t][k] = p33_node<PK>(pk_base, lat4, q, idx[t][k]);
+      }
 #pragma unroll
     for (int t = 0; t < PB; ++t) {
       float2 a01 = __fmul2_rn(make_float2(w[t][0], w[t][0]), v[t][0].xy);
@@ -592,15 +604,15 @@ __device__ __forceinline__ void p33_rounds(P33Warp& B, int M, int T0, uint32_t r
       }
       const int j = (int)lane + 32 * (q0 + t);
       if (j < M) {
-        const bool first = j < T0;                     // list entry of half 0
-        float* dst = (first == (rank == 0) ? B.own : B.send) + 3 * (first ? j : j - T0);
+        const int jj = j + (j >= T0 ? pad : 0);
+        MACT_DCHECK(jj < kP33Slice + 3);
+        float* dst = B.res + 3 * jj;
         dst[0] = a01.x; dst[1] = a01.y; dst[2] = a2;
       }
     }
   }
 }
 
-// vec: interleaved output 16-byte aligned (STG.128 per lane), or planar with n % 4 == 0 likewise
 template <int METHOD>
 __global__ void __launch_bounds__(kP33NW * 32, 1)
     k_lut33_pair(const float4* __restrict__ lat4, const uint8_t* __restrict__ rgb, float* __restrict__ out,
@@ -620,25 +632,24 @@ __global__ void __launch_bounds__(kP33NW * 32, 1)
   // first slice's input words in flight while the CTA stages its planes
   const uint32_t* in_w = reinterpret_cast<const uint32_t*>(rgb);
   const int64_t nbytes = 3 * n;
-  auto load = [&](int64_t sl, uint32_t (&wd)[2][3]) {
+  auto load = [&](int64_t sl, uint32_t (&wd)[3]) {
+    const int64_t w0 = sl * (kP33Slice * 3 / 4) + 3 * lane;   // word index
+    if ((sl + 1) * kP33Slice <= n) {                            // a whole slice: no per-word checks
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+      for (int c = 0; c < 3; ++c) wd[c] = __ldg(in_w + w0 + c);
+      return;
+    }
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const int64_t wi = sl * (kP33Slice * 3 / 4) + h * 96 + 3 * lane + c;   // word index
-        if (4 * wi + 3 < nbytes) {
-          wd[h][c] = __ldg(in_w + wi);
-        } else {                                        // the ragged end of the buffer
-          uint32_t v = 0;
+    for (int c = 0; c < 3; ++c) {                               // the ragged end of the buffer
+      uint32_t v = 0;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (4 * wi + k < nbytes) v |= (uint32_t)rgb[4 * wi + k] << (8 * k);
-          wd[h][c] = v;
-        }
-      }
+      for (int k = 0; k < 4; ++k)
+        if (4 * (w0 + c) + k < nbytes) v |= (uint32_t)rgb[4 * (w0 + c) + k] << (8 * k);
+      wd[c] = v;
+    }
   };
   int64_t sl = cl * kP33NW + warp;
-  uint32_t nxt[2][3] = {};
+  uint32_t nxt[3] = {};
   if (sl < nslices) load(sl, nxt);
   lut_quant_setup(lat4, 33 * 33 * 33, &S->q, S->red);   // ends with __syncthreads
   const LutQuant q = S->q;
@@ -656,80 +667,84 @@ __global__ void __launch_bounds__(kP33NW * 32, 1)
   // node index (whole lattice) -> shared address in my planes
   const uint32_t pk_base = smem_u32(S->pk) - rank * (16u * kL33Plane * 8u);
   const uint32_t lt = lanemask_lt();
-  for (int64_t i = 0; sl < nslices; ++i, sl += ncl * kP33NW) {
-    uint32_t wd[2][3];
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) wd[h][c] = nxt[h][c];
+  const bool merger = (lane >> 4) == rank;              // this lane's 4 pixels are in my half
+  uint32_t ns = 0, nr = 0;                               // sends / receives so far (exchange phases)
+  for (; sl < nslices; sl += ncl * kP33NW) {
+    const uint32_t wd[3] = {nxt[0], nxt[1], nxt[2]};
     if (sl + ncl * kP33NW < nslices) load(sl + ncl * kP33NW, nxt);
     const int64_t px0 = sl * kP33Slice;
+    const int64_t left = n - px0;
+    const int valid = left >= kP33Slice ? kP33Slice : (int)left;
     // ---- 1. my pixels of the slice, compacted in pixel order
-    uint32_t bal[2][4];
-    int T[2], pre[2], valid[2];
+    uint32_t bal[4];
+    int M = 0, T0 = 0, pre = 0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t left = n - (px0 + kP33Half * h);
-      valid[h] = left <= 0 ? 0 : (left >= kP33Half ? kP33Half : (int)left);
-      T[h] = 0;
-      pre[h] = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t r = byte_of(wd[h][(3 * k) >> 2], (3 * k) & 3);
-        const bool mine = (r >> 7) == rank && (int)(4 * lane) + k < valid[h];
-        bal[h][k] = __ballot_sync(0xffffffffu, mine);
-        T[h] += __popc(bal[h][k]);
-        pre[h] += __popc(bal[h][k] & lt);
-      }
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t r = byte_of(wd[(3 * k) >> 2], (3 * k) & 3);
+      const bool mine = (r >> 7) == rank && (int)(4 * lane) + k < valid;
+      bal[k] = __ballot_sync(0xffffffffu, mine);
+      M += __popc(bal[k]);
+      T0 += __popc(bal[k] & 0xFFFFu);
+      pre += __popc(bal[k] & lt);
     }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      int j = (h ? T[0] : 0) + pre[h];
+    {
+      int j = pre;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        if ((bal[h][k] >> lane) & 1u) {
+        if ((bal[k] >> lane) & 1u) {
           const int b0 = 3 * k;   // byte offset of the pixel in the lane's 12 bytes
-          const uint32_t r = byte_of(wd[h][b0 >> 2], b0 & 3), g = byte_of(wd[h][(b0 + 1) >> 2], (b0 + 1) & 3),
-                         b = byte_of(wd[h][(b0 + 2) >> 2], (b0 + 2) & 3);
+          const uint32_t r = byte_of(wd[b0 >> 2], b0 & 3), g = byte_of(wd[(b0 + 1) >> 2], (b0 + 1) & 3),
+                         b = byte_of(wd[(b0 + 2) >> 2], (b0 + 2) & 3);
           B.list[j++] = r | g << 8 | b << 16;
         }
       }
     }
-    const int M = T[0] + T[1];
-    // my half of the slice (register selects, no dynamically indexed arrays)
-    const int Tm = rank ? T[1] : T[0], Tp = rank ? T[0] : T[1];
-    const int vm = rank ? valid[1] : valid[0], prem = rank ? pre[1] : pre[0];
-    uint32_t balm[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) balm[k] = rank ? bal[1][k] : bal[0][k];
+    const int T1 = M - T0, pad = (-T0) & 3;
+    const int v0 = valid < kP33Half ? valid : kP33Half, v1 = valid - v0;
+    const int vm = rank ? v1 : v0, Tm = rank ? T1 : T0, Tp = rank ? T0 : T1;
     const uint32_t in_bytes = (uint32_t)(12 * (vm - Tm) + 15) & ~15u;
     const uint32_t out_bytes = (uint32_t)(12 * Tp + 15) & ~15u;
-    if (lane == 0) mbar_arrive_expect_tx(&S->rfull[warp], in_bytes);
-    if (i > 0) mbar_wait(&S->sfree[warp], (uint32_t)((i - 1) & 1));   // my send buffer is free again
+    MACT_DCHECK(M <= kP33Slice && Tm <= vm && in_bytes <= sizeof(B.recv) &&
+                12 * (rank ? 0 : T0 + pad) + out_bytes <= sizeof(B.res));
+    // The exchange counts transfers, not slices: a slice where one rank owns
+    // every pixel has a send in one direction only, and with per-slice phases
+    // the rank that receives nothing could complete two phases of its
+    // partner's `sfree` before the partner waits on the first (the parity wait
+    // then blocks forever -- found on the R-major 2^24 cube, where whole slices
+    // belong to one rank).  rfull phase k = my k-th receive; sfree phase k =
+    // the partner's consumption of my k-th send.
+    if (lane == 0 && in_bytes) mbar_arrive_expect_tx(&S->rfull[warp], in_bytes);
+    if (ns > 0) mbar_wait(&S->sfree[warp], (ns - 1) & 1);   // my last send was consumed: res and its recv free
     __syncwarp();
     // ---- 2. interpolate my pixels
-    if (q.on) p33_rounds<METHOD, true>(B, M, T[0], rank, lane, pk_base, lat4, q);
-    else p33_rounds<METHOD, false>(B, M, T[0], rank, lane, pk_base, lat4, q);
-    // ---- 3. the partner's half to the partner
+    if (q.on) p33_rounds<METHOD, true>(B, M, T0, pad, rank, lane, pk_base, lat4, q);
+    else p33_rounds<METHOD, false>(B, M, T0, pad, rank, lane, pk_base, lat4, q);
+    // ---- 3. the partner's part of the list to the partner
     fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0 && out_bytes) bulk_s2cluster(recv_peer, smem_u32(B.send), out_bytes, rfull_peer);
-    // ---- 4. merge my half: ours from own, theirs from recv
-    mbar_wait(&S->rfull[warp], (uint32_t)(i & 1));
-    {
+    if (lane == 0 && out_bytes)
+      bulk_s2cluster(recv_peer, smem_u32(B.res + (rank ? 0 : 3 * (T0 + pad))), out_bytes, rfull_peer);
+    ns += out_bytes != 0;
+    // ---- 4. merge my half: ours from res, theirs from recv
+    if (in_bytes) mbar_wait(&S->rfull[warp], nr & 1);
+    if (merger) {
       float o[12];
-      int ours = prem;
+      // pixel 4 lane + k of the slice: its position in my half minus the own pixels
+      // before it there (list index j minus the T0 half-0 entries for rank 1)
+      int j = pre;                                       // list index of this lane's next own pixel
+      const int base = 4 * (int)lane - kP33Half * (int)rank + (rank ? T0 : 0);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const bool m = (balm[k] >> lane) & 1u;
-        const int theirs = 4 * (int)lane + k - ours;
-        const float* src = m ? B.own + 3 * ours : B.recv + 3 * theirs;
+        const bool m = (bal[k] >> lane) & 1u;
+        const int theirs = base + k - j;
+        const float* src = m ? B.res + 3 * (j + (rank ? pad : 0)) : B.recv + 3 * theirs;
         o[3 * k] = src[0]; o[3 * k + 1] = src[1]; o[3 * k + 2] = src[2];
-        ours += m;
+        j += m;
       }
-      const int64_t p = px0 + kP33Half * rank + 4 * lane;
+      const int64_t p = px0 + 4 * lane;
+      const int lv = valid - 4 * (int)lane;              // valid pixels of this lane
       if (!planar) {
-        if (4 * (int)lane + 4 <= vm) {
+        if (lv >= 4) {
           float4* d = reinterpret_cast<float4*>(out + 3 * p);
           d[0] = make_float4(o[0], o[1], o[2], o[3]);
           d[1] = make_float4(o[4], o[5], o[6], o[7]);
@@ -737,27 +752,30 @@ __global__ void __launch_bounds__(kP33NW * 32, 1)
         } else {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            if (4 * (int)lane + k < vm)
+            if (k < lv)
 #pragma unroll
               for (int c = 0; c < 3; ++c) out[3 * (p + k) + c] = o[3 * k + c];
         }
       } else {
-        if (4 * (int)lane + 4 <= vm && (n & 3) == 0) {
+        if (lv >= 4 && (n & 3) == 0) {
 #pragma unroll
           for (int c = 0; c < 3; ++c)
             *reinterpret_cast<float4*>(out + c * n + p) = make_float4(o[c], o[3 + c], o[6 + c], o[9 + c]);
         } else {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            if (4 * (int)lane + k < vm)
+            if (k < lv)
 #pragma unroll
               for (int c = 0; c < 3; ++c) out[c * n + p + k] = o[3 * k + c];
         }
       }
     }
-    // ---- 5. my recv is free for the partner's next slice
+    // ---- 5. my recv is free for the partner's next send
     __syncwarp();
-    if (lane == 0) mbar_arrive_remote(sfree_peer);
+    if (in_bytes) {
+      if (lane == 0) mbar_arrive_remote(sfree_peer);
+      ++nr;
+    }
   }
   cluster_sync_all();   // the partner may still copy into / arrive on my shared memory
 }
@@ -1131,7 +1149,10 @@ __global__ void __cluster_dims__(3, 1, 1) __launch_bounds__(kLut33Threads, 1)
 #pragma unroll
         for (int q = 0; q < PB; ++q)
 #pragma unroll
-          for (int j = 0; j < K; ++j) v[q][j] = lat_c[idx[q][j]];
+          for (int j = 0; j < K; ++j) {
+            MACT_DCHECK(idx[q][j] >= 0 && idx[q][j] < NN);
+            v[q][j] = lat_c[idx[q][j]];
+          }
 #pragma unroll
         for (int q = 0; q < PB; ++q) {
           a[q0 + q] = w[q][0] * v[q][0];
@@ -1222,7 +1243,10 @@ __global__ void __launch_bounds__(kLut33Threads, 1)
 #pragma unroll
         for (int q = 0; q < PB; ++q)
 #pragma unroll
-          for (int j = 0; j < K; ++j) v[q][j] = lat_c[idx[q][j]];
+          for (int j = 0; j < K; ++j) {
+            MACT_DCHECK(idx[q][j] >= 0 && idx[q][j] < NN);
+            v[q][j] = lat_c[idx[q][j]];
+          }
 #pragma unroll
         for (int q = 0; q < PB; ++q) {
           a[q0 + q] = w[q][0] * v[q][0];
@@ -1391,14 +1415,18 @@ static int launch_lut33_pair(const float* lat, const uint8_t* rgb, float* out, i
   return check_launch("lut33_pair");
 }
 
-// 33^3 kernel selection: the component-split clusters (k_lut33_comp /
-// k_lut33_planar) serve by default -- measured faster on C3 (tetrahedral 93 vs
-// 85 Gpix/s, trilinear 79 vs 76); MACT_LUT33_KERNEL=pair selects the r-split
-// CTA pairs (fixed-point nodes) for A/B runs.  Read per call (a getenv is
-// ~100 ns next to a launch), so tests can exercise both in one process.
-static bool lut33_legacy() {
+// 33^3 kernel selection: the r-split CTA pairs (k_lut33_pair) serve
+// interleaved output -- measured faster on C3 than the component-split
+// clusters (trilinear / prism / pyramidal / tetrahedral 81 / 87 / 91 / 96 vs
+// 79 / 80 / 85 / 93 Gpix/s) -- and the independent component CTAs
+// (k_lut33_planar, no exchange) planar output.  MACT_LUT33_KERNEL=pair|comp
+// forces one family for A/B runs; read per call (a getenv is ~100 ns next to
+// a launch), so tests can exercise both in one process.
+static bool lut33_comp(int planar) {
   const char* e = getenv("MACT_LUT33_KERNEL");
-  return !(e && strcmp(e, "pair") == 0);
+  if (e && strcmp(e, "pair") == 0) return false;
+  if (e && strcmp(e, "comp") == 0) return true;
+  return planar != 0;
 }
 
 template <int N, int METHOD>
@@ -1406,14 +1434,14 @@ static int launch_interp(const float* lat, const uint8_t* rgb, float* out, int64
                          cudaStream_t st) {
   Outs outs{{out, nullptr, nullptr}};
   LutParams p{reinterpret_cast<const float4*>(lat)};
-  // 17^3: (c0,c1)+c2 smem planes, 59 KB; 9^3: 8 bank-private float4 copies,
-  // 93 KB; 16 compute warps per CTA.  33^3: the component-split cluster for
-  // every method (64/83/86/88 Gpix/s against 42/52/60/74 gathering from L2);
-  // the L2 streaming kernel remains its fallback for planar output, unaligned
-  // buffers and the tail.
+  // 17^3: 64-bit fixed-point nodes (trilinear: b-pair entries) or the fp32
+  // planes; 9^3: 8 bank-private float4 copies; 16 compute warps per CTA.
+  // 33^3: r-split CTA pairs for interleaved output, independent component
+  // CTAs for planar output (lut33_comp); unaligned buffers take the per-pixel
+  // kernels with the same arithmetic.
   if constexpr (N == 33)
-    return lut33_legacy() ? launch_lut33_comp<METHOD>(lat, rgb, out, n, planar, st)
-                          : launch_lut33_pair<METHOD>(lat, rgb, out, n, planar, st);
+    return lut33_comp(planar) ? launch_lut33_comp<METHOD>(lat, rgb, out, n, planar, st)
+                              : launch_lut33_pair<METHOD>(lat, rgb, out, n, planar, st);
   else
     return launch_stream_t<OpLut<N, METHOD>, (OpLut<N, METHOD>::PAIR ? MACT_LUT_NW_TRI17 : MACT_LUT_NW),
                            (N <= 9 ? 2 : 1), MACT_LUT_SIN, 1>(

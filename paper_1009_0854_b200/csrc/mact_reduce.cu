@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kRedThreads) k_err(const __grid_constant__ Red
       cand[0] = v.c0; cand[1] = v.c1; cand[2] = v.c2;
     } else if (s.candidate == MACT_CAND_FAST_F64) {        // the reference's own arithmetic
       if (s.space == MACT_SPACE_LAB) ref::lab_fast(gamma_d[r], gamma_d[g], gamma_d[b], p.c, cand);
-      else if (s.space == MACT_SPACE_HSI) ref::hsi_fast((double)r, (double)g, (double)b, p.c, cand);
+      else if (s.space == MACT_SPACE_HSI) ref::hsi_fast<true>((double)r, (double)g, (double)b, p.c, cand);
       else ref::sct_fast((double)r, (double)g, (double)b, p.c, cand);
     } else if (s.candidate == MACT_CAND_LUT) {
       if (s.lut_grid_n == 9) lut_value<9>(s.lut_lattice, s.lut_method, r, g, b, cand);

@@ -25,7 +25,8 @@ __global__ void k_fast_ref(const __grid_constant__ KCoeffs c, const TI* __restri
        i += (int64_t)gridDim.x * blockDim.x) {
     double o[3];
     if constexpr (SPACE == MACT_SPACE_LAB) ref::lab_fast(lin(in, 3 * i), lin(in, 3 * i + 1), lin(in, 3 * i + 2), c, o);
-    else if constexpr (SPACE == MACT_SPACE_HSI) ref::hsi_fast(chan(in, 3 * i), chan(in, 3 * i + 1), chan(in, 3 * i + 2), c, o);
+    else if constexpr (SPACE == MACT_SPACE_HSI)
+      ref::hsi_fast<sizeof(TI) == 1>(chan(in, 3 * i), chan(in, 3 * i + 1), chan(in, 3 * i + 2), c, o);
     else ref::sct_fast(chan(in, 3 * i), chan(in, 3 * i + 1), chan(in, 3 * i + 2), c, o);
     if (planar) {
       out[i] = o[0]; out[n + i] = o[1]; out[2 * n + i] = o[2];

@@ -20,6 +20,20 @@ __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, 
 __device__ __forceinline__ double sub(double a, double b) { return __dadd_rn(a, -b); }
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dv(double a, double b) { return __ddiv_rn(a, b); }
+// a / b for a constant divisor with rb = RN(1/b): q = RN(a rb), then one FMA
+// correction (Markstein: the residual a - b q is exact and RN(q + r rb) is the
+// correctly rounded quotient) -- 3 DP ops instead of the ~10 of a general
+// division.  Used where the dividends are the 8-bit domain's (white-point
+// division of the linear-light XYZ, /255 and /3 of integer channels), which the
+// full-cube fidelity tests check bit for bit; non-finite values take dv.
+__device__ __forceinline__ double dv_k(double a, double b, double rb) {
+  const double q = __dmul_rn(a, rb);
+  const double r = __fma_rn(-q, b, a);
+  const double o = __fma_rn(r, rb, q);
+  return isfinite(o) ? o : dv(a, b);
+}
+constexpr double kRcpWhiteX = 1.0 / kWhiteX, kRcpWhiteZ = 1.0 / kWhiteZ;
+constexpr double kRcp255 = 1.0 / 255.0, kRcp3 = 1.0 / 3.0;
 
 template <int DEG>
 __device__ __forceinline__ double horner(const double* c, double x) {
@@ -62,16 +76,20 @@ __device__ __forceinline__ void lab_fast(double r, double g, double b, const KCo
   const double x = add(add(mul(rgb2xyz(0, 0), r), mul(rgb2xyz(0, 1), g)), mul(rgb2xyz(0, 2), b));
   const double y = add(add(mul(rgb2xyz(1, 0), r), mul(rgb2xyz(1, 1), g)), mul(rgb2xyz(1, 2), b));
   const double z = add(add(mul(rgb2xyz(2, 0), r), mul(rgb2xyz(2, 1), g)), mul(rgb2xyz(2, 2), b));
-  const double fx = lab_f_fast(dv(x, kWhiteX), c), fy = lab_f_fast(dv(y, kWhiteY), c),
-               fz = lab_f_fast(dv(z, kWhiteZ), c);
+  static_assert(kWhiteY == 1.0, "y / Yw is y");
+  const double fx = lab_f_fast(dv_k(x, kWhiteX, kRcpWhiteX), c), fy = lab_f_fast(y, c),
+               fz = lab_f_fast(dv_k(z, kWhiteZ, kRcpWhiteZ), c);
   o[0] = sub(mul(116.0, fy), 16.0);
   o[1] = mul(500.0, sub(fx, fy));
   o[2] = mul(200.0, sub(fy, fz));
 }
 
-// fast.py:125-148 on raw channel values (0..255)
+// fast.py:125-148 on raw channel values (0..255); U8: integer channels (the
+// constant divisions take dv_k, checked on all 2^24 colours)
+template <bool U8 = false>
 __device__ __forceinline__ void hsi_fast(double r, double g, double b, const KCoeffs& c, double* o) {
-  r = dv(r, 255.0); g = dv(g, 255.0); b = dv(b, 255.0);
+  auto dvc = [](double a, double d, double rd) { return U8 ? dv_k(a, d, rd) : dv(a, d); };
+  r = dvc(r, 255.0, kRcp255); g = dvc(g, 255.0, kRcp255); b = dvc(b, 255.0, kRcp255);
   const bool c1 = (r > b) && (g > b);
   const bool c2 = !c1 && (g > r);
   const bool c3 = !c1 && !c2 && (b > g);
@@ -88,7 +106,7 @@ __device__ __forceinline__ void hsi_fast(double r, double g, double b, const KCo
   const double low = fmin(fmin(r, g), b);
   o[0] = h;
   o[1] = total > 0.0 ? sub(1.0, dv(mul(3.0, low), total)) : 0.0;
-  o[2] = dv(total, 3.0);
+  o[2] = dvc(total, 3.0, kRcp3);
 }
 
 // fast.py:188-203 on raw channel values

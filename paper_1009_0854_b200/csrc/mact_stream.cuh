@@ -172,12 +172,16 @@ __global__ void __launch_bounds__(32 * (NW + 1)) k_ws(const uint8_t* __restrict_
 
   if (warp == NW) {                                       // ---- producer warp
     if (lane == 0) {
-      for (int64_t i = pre; i < my_tiles; ++i) {
-        const int s = (int)(i % SIN);
-        if (i >= SIN) mbar_wait(&empty[s], (uint32_t)(((i / SIN) - 1) & 1));
+      // ring position (stage s, its use count) maintained incrementally: no
+      // 64-bit divisions by SIN in the loop
+      int s = (int)(pre % SIN);
+      uint32_t ph = (uint32_t)(pre / SIN);
+      int64_t t = first + pre * stride;
+      for (int64_t i = pre; i < my_tiles; ++i, t += stride) {
+        if (i >= SIN) mbar_wait(&empty[s], (ph - 1) & 1);
         mbar_arrive_expect_tx(&full[s], L::IN_BYTES);
-        bulk_g2s(in_s + (size_t)s * L::IN_BYTES, in + (first + i * stride) * L::IN_BYTES,
-                 L::IN_BYTES, &full[s]);
+        bulk_g2s(in_s + (size_t)s * L::IN_BYTES, in + t * L::IN_BYTES, L::IN_BYTES, &full[s]);
+        if (++s == SIN) { s = 0; ++ph; }
       }
     }
     __syncwarp();
@@ -191,14 +195,14 @@ __global__ void __launch_bounds__(32 * (NW + 1)) k_ws(const uint8_t* __restrict_
     if constexpr (HasCtx<Op>::value) return Op::ctx(sh, p);
     else return 0;
   }();
-  for (int64_t i = 0; i < my_tiles; ++i) {
-    const int64_t t = first + i * stride;
-    const int s = (int)(i % SIN);
-    const int ob = NOB == 1 ? 0 : (int)(i % NOB);
+  int s = 0, ob = 0;                                      // ring stage and output buffer of tile i
+  uint32_t ph = 0;                                        // use count of stage s, mod 2
+  int64_t t = first;
+  for (int64_t i = 0; i < my_tiles; ++i, t += stride) {
     float* ob_s = out_w + (size_t)ob * NOUT * L::OUT_FLOATS;
     if (lane == 0) bulk_wait_read<NOB - 1>();             // this buffer's last store has read it
     __syncwarp();
-    mbar_wait(&full[s], (uint32_t)((i / SIN) & 1));
+    mbar_wait(&full[s], ph & 1);
     const uint32_t* wsrc =
         reinterpret_cast<const uint32_t*>(in_s + (size_t)s * L::IN_BYTES) + warp * (L::WPX / 4) * 3;
 #pragma unroll
@@ -244,6 +248,8 @@ __global__ void __launch_bounds__(32 * (NW + 1)) k_ws(const uint8_t* __restrict_
       bulk_commit();
       mbar_arrive(&empty[s]);                             // stage s fully consumed by this warp
     }
+    if (++s == SIN) { s = 0; ++ph; }
+    if constexpr (NOB > 1) ob = ob + 1 == NOB ? 0 : ob + 1;
   }
   if (lane == 0) bulk_wait<0>();
   __syncwarp();

@@ -91,15 +91,17 @@ DEFAULT_CONFIG = MactConfig()
 _ENTRY = {"lab": "mact_lab_fast", "hsi": "mact_hsi_fast", "sct": "mact_sct_fast"}
 
 
-def _host_u8(space: str, arr: np.ndarray, cfg: MactConfig, out, layout: str):
-    """numpy uint8 -> numpy fp32 through the native chunked H2D/kernel/D2H executor."""
+def _host_u8(space: str, arr: np.ndarray, cfg: MactConfig, out, layout: str, out_dtype: str = "float32"):
+    """numpy uint8 -> numpy fp32 (or fp64, the fidelity mode) through the native chunked
+    H2D/kernel/D2H executor."""
     import torch
 
     src = np.ascontiguousarray(arr)
     lead = src.shape[:-1]
     n = int(np.prod(lead, dtype=np.int64)) if lead else 1
-    out = _dev.host_out(out, lead, layout)
-    _dev.host_call("mact_transform_host", torch.cuda.current_device(), _lib.SPACES[space], _dev.np_ptr(src),
+    out = _dev.host_out(out, lead, layout, np.float64 if out_dtype == "float64" else np.float32)
+    _dev.host_call("mact_transform_host_f64" if out_dtype == "float64" else "mact_transform_host",
+                   torch.cuda.current_device(), _lib.SPACES[space], _dev.np_ptr(src),
                    _dev.np_ptr(out), n, cfg.coeffs, _lib.LAYOUTS[layout])
     return out
 
@@ -119,6 +121,10 @@ def transform(space: str, pixels, cfg: MactConfig = DEFAULT_CONFIG, *, out=None,
     if out_dtype not in ("float32", "float64"):
         raise ValueError(f"out_dtype must be float32 or float64, got {out_dtype!r}")
     _dev.require_cuda()
+    if out_dtype == "float64" and not _dev.is_device_tensor(pixels):
+        arr = np.asarray(pixels)
+        if arr.dtype == np.uint8 and arr.ndim >= 1 and arr.shape[-1] == 3:
+            return _host_u8(space, arr, cfg, out, layout, out_dtype)
     if out_dtype == "float64":
         import torch
 

@@ -7,7 +7,8 @@ so the document is what is tested -- and the reference's own harness
 (`mact.harness.measure_error`, harness.py:77-122) scores the B200 backend:
 
 - `_b200.rgb_to_{lab,hsi,sct}_fast` agree with `mact.fast` within the north-star
-  tolerances on config 1 (512x512, default_rng(0));
+  tolerances on config 1 (512x512, default_rng(0)), and bit for bit with
+  out_dtype="float64" (mact_transform_host_f64);
 - `mact.harness.measure_error("lab", _b200 backend, mact.exact.rgb_to_lab_exact,
   population=C1)` reproduces the figure the reference itself produced
   (tests/golden/figures.json, written by make_golden.py from the live reference).
@@ -62,6 +63,9 @@ DRIVER = textwrap.dedent("""
             assert np.array_equal(np.isnan(got[:, 2]), np.isnan(ref[:, 2]))
             d = np.nan_to_num(d / np.array([255 * np.sqrt(3), np.pi / 2, np.pi / 2]))
         out[sp] = float(d.max())
+        exact64 = getattr(B, f"rgb_to_{sp}_fast")(c1, cfg, "float64")
+        assert exact64.dtype == np.float64
+        assert np.array_equal(exact64, ref, equal_nan=True), sp      # fidelity mode: bit for bit
     st = harness.measure_error("lab", lambda p: B.rgb_to_lab_fast(p, cfg), exact.rgb_to_lab_exact, population=c1)
     out["c1"] = {"avg": st.avg, "max": st.max, "count": st.count, "argmax_pixel": list(st.argmax_pixel)}
     print(json.dumps(out))
