@@ -780,6 +780,199 @@ __global__ void __launch_bounds__(kP33NW * 32, 1)
   cluster_sync_all();   // the partner may still copy into / arrive on my shared memory
 }
 
+// ------------------------------------------ 33^3: r-split INDEPENDENT CTAs
+// The same r-split of the fixed-point lattice (CTA b holds planes 0..16 if
+// b is even, 16..32 if odd: 148 KB), but with no exchange at all: CTA 2c and
+// CTA 2c+1 both scan the same slices, each keeps only ITS pixels (r bit 7 ==
+// b & 1), interpolates them from its own shared memory and writes the 12-byte
+// results straight to global memory at the pixel's position.  The two CTAs
+// never talk -- no cluster, no DSMEM copy, no merge, no mbarrier -- and run at
+// the same pace over the same addresses, so L2 serves the second reader of a
+// slice and merges the two CTAs' partial sector writes before they reach DRAM.
+//
+// Per warp: a ring `list` of pending own pixels (r | g << 8 | b << 16 |
+// pos << 24 | slice parity << 31).  A 128-px slice appends ~64 entries in pixel
+// order (ballot + prefix popcount); the warp then interpolates FULL rounds of
+// 32 entries (the 17^3 code: integer selection, LDS.64 fixed-point nodes,
+// FFMA2) and carries the remainder (< 32) into the next slice, so no lane idles
+// on a ragged last round; an entry never survives more than one slice boundary
+// (a remainder older than that is flushed as a partial round), which is why
+// one parity bit names its slice.  SORTED: the 96 result words of a round go
+// through a per-warp transpose buffer so that store j writes words 32 j ..
+// 32 j + 31 of the round in address order (each STG.32 covers a third of the
+// round's span, ~8 sectors) instead of one component of every entry (~24
+// sectors per STG.32).
+#ifndef MACT_LUT33S_NW
+#define MACT_LUT33S_NW 32
+#endif
+#ifndef MACT_LUT33S_SORTED
+#define MACT_LUT33S_SORTED 1
+#endif
+constexpr int kS33NW = MACT_LUT33S_NW;
+constexpr int kS33Ring = 256;                  // >= 31 carried + 128 appended
+struct alignas(16) S33Warp {
+  uint32_t list[kS33Ring];
+  float tr[96];
+};
+struct S33Shared {
+  S33Warp wb[kS33NW];
+  uint2 pk[kL33Planes * kL33Plane];
+  LutQuant q;
+  float red[32][6];
+};
+constexpr size_t kS33Smem = sizeof(S33Shared);
+
+template <int METHOD, bool PK, bool SORTED>
+__device__ __forceinline__ void s33_round(S33Warp& B, uint32_t head, int m, uint32_t rank, uint32_t lane,
+                                          uint32_t pk_base, const float4* lat4, const LutQuant& q,
+                                          int64_t b0, int64_t b1, float* __restrict__ out, int64_t n, int planar) {
+  constexpr int K = LutK<METHOD>::K;
+  const bool act = (int)lane < m;
+  // padding lanes take a colour of MY half: a node outside my planes would
+  // address shared memory outside the CTA's window
+  const uint32_t e = act ? B.list[(head + lane) & (kS33Ring - 1)] : (rank << 7);
+  int idx[K];
+  float w[K];
+  Node2 v[K];
+  Lut33Sel<METHOD>::template select<true>(e & 0xFFu, (e >> 8) & 0xFFu, (e >> 16) & 0xFFu, idx, w);
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    MACT_DCHECK(!PK || (uint32_t)(idx[k] - 16 * kL33Plane * (int)rank) < (uint32_t)(kL33Planes * kL33Plane));
+    v[k] = p33_node<PK>(pk_base, lat4, q, idx[k]);
+  }
+  float2 a01 = __fmul2_rn(make_float2(w[0], w[0]), v[0].xy);
+  float a2 = w[0] * v[0].z;
+#pragma unroll
+  for (int k = 1; k < K; ++k) {   // out += w_k V[node_k], node order (lut.py:233-236)
+    a01 = __ffma2_rn(make_float2(w[k], w[k]), v[k].xy, a01);
+    a2 = fmaf(w[k], v[k].z, a2);
+  }
+  const int64_t P = ((int32_t)e < 0 ? b1 : b0) + (int64_t)((e >> 24) & 127u);
+  if (planar) {                   // one plane per store: list order is address order
+    if (act) {
+      out[P] = a01.x; out[n + P] = a01.y; out[2 * n + P] = a2;
+    }
+    return;
+  }
+  if constexpr (!SORTED) {
+    if (act) {
+      float* d = out + 3 * P;
+      d[0] = a01.x; d[1] = a01.y; d[2] = a2;
+    }
+  } else {
+    float* t = B.tr + 3 * lane;   // stride 3 words: conflict-free
+    t[0] = a01.x; t[1] = a01.y; t[2] = a2;
+    __syncwarp();
+    const uint32_t plo = (uint32_t)P, phi = (uint32_t)((uint64_t)P >> 32);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const uint32_t k = 32u * j + lane, slot = (k * 171u) >> 9, comp = k - 3u * slot;   // k / 3 for k < 96
+      const float val = B.tr[k];
+      const uint32_t slo = __shfl_sync(0xffffffffu, plo, slot), shi = __shfl_sync(0xffffffffu, phi, slot);
+      const int64_t Ps = (int64_t)(((uint64_t)shi << 32) | slo);
+      if ((int)slot < m) out[3 * Ps + comp] = val;
+    }
+    __syncwarp();                 // tr is rewritten by the next round
+  }
+}
+
+template <int METHOD, bool SORTED>
+__global__ void __launch_bounds__(kS33NW * 32, 1)
+    k_lut33_split(const float4* __restrict__ lat4, const uint8_t* __restrict__ rgb, float* __restrict__ out,
+                  int64_t n, int64_t nslices, int planar) {
+  extern __shared__ __align__(128) uint8_t smem_s33[];
+  S33Shared* S = reinterpret_cast<S33Shared*>(smem_s33);
+  const uint32_t rank = blockIdx.x & 1u;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const uint32_t* in_w = reinterpret_cast<const uint32_t*>(rgb);
+  const int64_t nbytes = 3 * n;
+  auto load = [&](int64_t sl, uint32_t (&wd)[3]) {
+    const int64_t w0 = sl * (kP33Slice * 3 / 4) + 3 * lane;   // word index
+    if ((sl + 1) * kP33Slice <= n) {                            // a whole slice: no per-word checks
+#pragma unroll
+      for (int c = 0; c < 3; ++c) wd[c] = __ldg(in_w + w0 + c);
+      return;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {                               // the ragged end of the buffer
+      uint32_t v = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (4 * (w0 + c) + k < nbytes) v |= (uint32_t)rgb[4 * (w0 + c) + k] << (8 * k);
+      wd[c] = v;
+    }
+  };
+  const int64_t stride = ncl * kS33NW;
+  int64_t sl = cl * kS33NW + warp;
+  uint32_t nxt[3] = {};
+  if (sl < nslices) load(sl, nxt);     // first slice in flight while the CTA stages its planes
+  lut_quant_setup(lat4, 33 * 33 * 33, &S->q, S->red);   // ends with __syncthreads
+  const LutQuant q = S->q;
+  if (q.on) {
+    const int first = 16 * kL33Plane * (int)rank;
+    for (int i = threadIdx.x; i < kL33Planes * kL33Plane; i += blockDim.x)
+      S->pk[i] = lut_quant_pack(q, __ldg(lat4 + first + i));
+  }
+  __syncthreads();
+  S33Warp& B = S->wb[warp];
+  const uint32_t pk_base = smem_u32(S->pk) - rank * (16u * kL33Plane * 8u);
+  const uint32_t lt = lanemask_lt();
+  uint32_t head = 0, par = 0;
+  int cnt = 0;
+  int64_t b0 = 0, b1 = 0;              // first pixel of the latest slice of parity 0 / 1
+  auto round = [&](int m) {
+    if (q.on) s33_round<METHOD, true, SORTED>(B, head, m, rank, lane, pk_base, lat4, q, b0, b1, out, n, planar);
+    else s33_round<METHOD, false, SORTED>(B, head, m, rank, lane, pk_base, lat4, q, b0, b1, out, n, planar);
+    head = (head + (uint32_t)m) & (kS33Ring - 1);
+    cnt -= m;
+  };
+  for (; sl < nslices; sl += stride) {
+    const uint32_t wd[3] = {nxt[0], nxt[1], nxt[2]};
+    if (sl + stride < nslices) load(sl + stride, nxt);
+    const int64_t px0 = sl * kP33Slice;
+    const int64_t left = n - px0;
+    const int valid = left >= kP33Slice ? kP33Slice : (int)left;
+    if (par) b1 = px0; else b0 = px0;
+    const int old = cnt;
+    // ---- my pixels of the slice, appended in pixel order
+    uint32_t bal[4];
+    int pre = 0, M = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t r = byte_of(wd[(3 * k) >> 2], (3 * k) & 3);
+      const bool mine = (r >> 7) == rank && (int)(4 * lane) + k < valid;
+      bal[k] = __ballot_sync(0xffffffffu, mine);
+      M += __popc(bal[k]);
+      pre += __popc(bal[k] & lt);
+    }
+    {
+      uint32_t j = head + (uint32_t)cnt + (uint32_t)pre;
+      const uint32_t tag = (par << 31) | ((4u * lane) << 24);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if ((bal[k] >> lane) & 1u) {
+          const int o = 3 * k;   // byte offset of the pixel in the lane's 12 bytes
+          const uint32_t r = byte_of(wd[o >> 2], o & 3), g = byte_of(wd[(o + 1) >> 2], (o + 1) & 3),
+                         b = byte_of(wd[(o + 2) >> 2], (o + 2) & 3);
+          B.list[j++ & (kS33Ring - 1)] = (r | g << 8 | b << 16) | (tag + ((uint32_t)k << 24));
+        }
+      }
+    }
+    cnt += M;
+    MACT_DCHECK(cnt <= kS33Ring);
+    __syncwarp();
+    // ---- full rounds; a remainder from before this slice goes out now
+    if (cnt >= 32) {
+      do round(32); while (cnt >= 32);
+    } else if (old > 0) {
+      round(cnt);
+    }
+    par ^= 1u;
+  }
+  if (cnt > 0) round(cnt);
+}
+
 // Per-pixel 33^3 path for unaligned buffers: the same selection and the same
 // node arithmetic as the pair kernel (fixed-point nodes quantised on the fly
 // from the L2 lattice with the same LutQuant), so every path is bit-identical.
@@ -1415,6 +1608,40 @@ static int launch_lut33_pair(const float* lat, const uint8_t* rgb, float* out, i
   return check_launch("lut33_pair");
 }
 
+// 33^3 on r-split independent CTAs (k_lut33_split): interleaved or planar
+// output, any 4-byte aligned input; other buffers take the per-pixel kernel
+// with the same arithmetic.
+template <int METHOD>
+static int launch_lut33_split(const float* lat, const uint8_t* rgb, float* out, int64_t n, int planar,
+                              cudaStream_t st) {
+  NvtxRange range("lut33_interp");
+  LutParams p{reinterpret_cast<const float4*>(lat)};
+  if ((uintptr_t)rgb % 4 != 0) {
+    Outs outs{{out, nullptr, nullptr}};
+    auto kfn = k_generic<OpLut33Gen<METHOD>, 256>;
+    const size_t sb = sizeof(typename OpLut33Gen<METHOD>::Shared);
+    const int64_t cap = persistent_grid((const void*)kfn, 256, sb);
+    if (cap <= 0) return MACT_ECUDA;
+    int64_t grid = (n + 255) / 256;
+    if (grid > cap) grid = cap;
+    kfn<<<(unsigned)grid, 256, sb, st>>>(rgb, outs, 0, n, planar, p);
+    count_launch();
+    return check_launch("lut_interp");
+  }
+  const int64_t nslices = (n + kP33Slice - 1) / kP33Slice;
+  auto kfn = k_lut33_split<METHOD, MACT_LUT33S_SORTED != 0>;
+  const int64_t cap = persistent_grid((const void*)kfn, kS33NW * 32, kS33Smem);
+  if (cap <= 0) return MACT_ECUDA;
+  int64_t pairs = cap / 2;
+  const int64_t need = (nslices + kS33NW - 1) / kS33NW;   // pairs with at least one slice per warp
+  if (pairs > need) pairs = need;
+  if (pairs < 1) pairs = 1;
+  kfn<<<(unsigned)(2 * pairs), kS33NW * 32, kS33Smem, st>>>(reinterpret_cast<const float4*>(lat), rgb, out, n,
+                                                           nslices, planar);
+  count_launch();
+  return check_launch("lut33_split");
+}
+
 // 33^3 kernel selection: the r-split CTA pairs (k_lut33_pair) serve
 // interleaved output -- measured faster on C3 than the component-split
 // clusters (trilinear / prism / pyramidal / tetrahedral 81 / 87 / 91 / 96 vs
@@ -1422,11 +1649,13 @@ static int launch_lut33_pair(const float* lat, const uint8_t* rgb, float* out, i
 // (k_lut33_planar, no exchange) planar output.  MACT_LUT33_KERNEL=pair|comp
 // forces one family for A/B runs; read per call (a getenv is ~100 ns next to
 // a launch), so tests can exercise both in one process.
-static bool lut33_comp(int planar) {
+enum { kLut33Split = 0, kLut33Pair = 1, kLut33Comp = 2 };
+static int lut33_kernel(int planar) {
   const char* e = getenv("MACT_LUT33_KERNEL");
-  if (e && strcmp(e, "pair") == 0) return false;
-  if (e && strcmp(e, "comp") == 0) return true;
-  return planar != 0;
+  if (e && strcmp(e, "split") == 0) return kLut33Split;
+  if (e && strcmp(e, "pair") == 0) return kLut33Pair;
+  if (e && strcmp(e, "comp") == 0) return kLut33Comp;
+  return planar != 0 ? kLut33Comp : kLut33Pair;
 }
 
 template <int N, int METHOD>
@@ -1439,10 +1668,12 @@ static int launch_interp(const float* lat, const uint8_t* rgb, float* out, int64
   // 33^3: r-split CTA pairs for interleaved output, independent component
   // CTAs for planar output (lut33_comp); unaligned buffers take the per-pixel
   // kernels with the same arithmetic.
-  if constexpr (N == 33)
-    return lut33_comp(planar) ? launch_lut33_comp<METHOD>(lat, rgb, out, n, planar, st)
-                              : launch_lut33_pair<METHOD>(lat, rgb, out, n, planar, st);
-  else
+  if constexpr (N == 33) {
+    const int k = lut33_kernel(planar);
+    return k == kLut33Comp   ? launch_lut33_comp<METHOD>(lat, rgb, out, n, planar, st)
+           : k == kLut33Pair ? launch_lut33_pair<METHOD>(lat, rgb, out, n, planar, st)
+                             : launch_lut33_split<METHOD>(lat, rgb, out, n, planar, st);
+  } else
     return launch_stream_t<OpLut<N, METHOD>, (OpLut<N, METHOD>::PAIR ? MACT_LUT_NW_TRI17 : MACT_LUT_NW),
                            (N <= 9 ? 2 : 1), MACT_LUT_SIN, 1>(
         rgb, outs, n, planar, p, st, "lut_interp");

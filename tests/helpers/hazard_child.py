@@ -41,7 +41,7 @@ def main():
     out["all_fused"] = h(torch.stack(res))
     for n in (9, 17, 33):
         lt = lut.build_lut("lab", n)
-        kernels = ("comp", "pair") if n == 33 else ("default",)
+        kernels = ("comp", "pair", "split") if n == 33 else ("default",)
         for k in kernels:
             if n == 33:
                 os.environ["MACT_LUT33_KERNEL"] = k

@@ -188,7 +188,7 @@ def test_lut_interp_host_executor(grid, method):
         np.testing.assert_array_equal(planar, ref[:5000])
 
 
-@pytest.mark.parametrize("kernel", ["pair", "comp"])
+@pytest.mark.parametrize("kernel", ["split", "pair", "comp"])
 @pytest.mark.parametrize("n", [4096 * 37 + 8, 4096 * 5 + 3, 1000])
 @pytest.mark.parametrize("method", ["trilinear", "tetrahedral"])
 def test_lut33_planar_equals_interleaved(monkeypatch, kernel, n, method):
@@ -323,7 +323,7 @@ def test_lut_nonfinite_lattice(P, n):
         np.testing.assert_allclose(got[fin], ref[fin], rtol=2e-6, atol=1e-4, err_msg=method)
 
 
-@pytest.mark.parametrize("kernel", ["comp", "pair"])
+@pytest.mark.parametrize("kernel", ["comp", "pair", "split"])
 def test_lut33_wide_range_lattice_falls_back(P, monkeypatch, kernel):
     """33^3 lattice too wide for the fixed-point nodes (x1000): the component
     kernels stage fp32 components, the pair kernel gathers the fp32 lattice from
@@ -372,7 +372,7 @@ def test_lut_error_bound_either_format(P, n, scale, method):
     assert np.abs(got - ref).max() <= bound
 
 
-@pytest.mark.parametrize("kernel", ["comp", "pair"])
+@pytest.mark.parametrize("kernel", ["comp", "pair", "split"])
 @pytest.mark.parametrize("method", O.METHODS)
 def test_lut33_both_kernels(P, monkeypatch, kernel, method):
     """Both 33^3 interpolation kernels -- the r-split CTA pairs (default for
@@ -423,8 +423,9 @@ print("ok")
 """
 
 
+@pytest.mark.parametrize("kernel", ["pair", "split"])
 @pytest.mark.parametrize("cap", ["", "2", "6"])
-def test_lut33_pair_one_sided_slices(cap):
+def test_lut33_pair_one_sided_slices(cap, kernel):
     """The r-split pairs on slices owned entirely by one rank (sends in one
     direction only), alternating with mixed and half/half slices, repeated
     launches and few clusters (MACT_GRID_CAP): the exchange must neither
@@ -433,7 +434,7 @@ def test_lut33_pair_one_sided_slices(cap):
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, MACT_LUT33_KERNEL="pair")
+    env = dict(os.environ, MACT_LUT33_KERNEL=kernel)
     if cap:
         env["MACT_GRID_CAP"] = cap
     r = subprocess.run([sys.executable, "-c", _SKEW_CHILD, root], env=env, capture_output=True, text=True,
