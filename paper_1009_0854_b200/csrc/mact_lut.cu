@@ -792,45 +792,48 @@ __global__ void __launch_bounds__(kP33NW * 32, 1)
 //
 // Per warp: a ring `list` of pending own pixels (r | g << 8 | b << 16 |
 // pos << 24 | slice parity << 31).  A 128-px slice appends ~64 entries in pixel
-// order (ballot + prefix popcount); the warp then interpolates FULL rounds of
-// 32 entries (the 17^3 code: integer selection, LDS.64 fixed-point nodes,
+// order (ballots + prefix popcounts, branch-free: one PRMT builds an entry, a
+// predicated STS appends it); the warp then interpolates FULL rounds
+// of 32 entries (the 17^3 code: integer selection, LDS.64 fixed-point nodes,
 // FFMA2) and carries the remainder (< 32) into the next slice, so no lane idles
 // on a ragged last round; an entry never survives more than one slice boundary
 // (a remainder older than that is flushed as a partial round), which is why
-// one parity bit names its slice.  SORTED: the 96 result words of a round go
-// through a per-warp transpose buffer so that store j writes words 32 j ..
-// 32 j + 31 of the round in address order (each STG.32 covers a third of the
-// round's span, ~8 sectors) instead of one component of every entry (~24
-// sectors per STG.32).
+// one parity bit names its slice.  Results go out as three STG.32 per entry
+// (routing the words through a transpose buffer so that each store covers a
+// contiguous third of the round measured slower: 109 vs 128 Gpix/s).
 #ifndef MACT_LUT33S_NW
 #define MACT_LUT33S_NW 32
 #endif
-#ifndef MACT_LUT33S_SORTED
-#define MACT_LUT33S_SORTED 1
-#endif
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 constexpr int kS33NW = MACT_LUT33S_NW;
 constexpr int kS33Ring = 256;                  // >= 31 carried + 128 appended
-struct alignas(16) S33Warp {
-  uint32_t list[kS33Ring];
-  float tr[96];
-};
 struct S33Shared {
-  S33Warp wb[kS33NW];
+  uint32_t list[kS33NW][kS33Ring];             // first: each warp's ring is 1 KB aligned (address = base | offset)
   uint2 pk[kL33Planes * kL33Plane];
   LutQuant q;
   float red[32][6];
 };
 constexpr size_t kS33Smem = sizeof(S33Shared);
 
-template <int METHOD, bool PK, bool SORTED>
-__device__ __forceinline__ void s33_round(S33Warp& B, uint32_t head, int m, uint32_t rank, uint32_t lane,
-                                          uint32_t pk_base, const float4* lat4, const LutQuant& q,
-                                          int64_t b0, int64_t b1, float* __restrict__ out, int64_t n, int planar) {
+// One round: entries head .. head + m - 1 of the ring (lane l takes entry l).
+// q0 / q1: output pointer of the first pixel of the latest slice of parity 0 / 1.
+template <int METHOD, bool PK, bool PLANAR>
+__device__ __forceinline__ void s33_round(uint32_t list_base, uint32_t head_b, int m, uint32_t rank, uint32_t lane,
+                                          uint32_t pk_base, const float4* lat4, const LutQuant& q, float* q0,
+                                          float* q1, int64_t n) {
   constexpr int K = LutK<METHOD>::K;
   const bool act = (int)lane < m;
   // padding lanes take a colour of MY half: a node outside my planes would
   // address shared memory outside the CTA's window
-  const uint32_t e = act ? B.list[(head + lane) & (kS33Ring - 1)] : (rank << 7);
+  uint32_t e = rank << 7;
+  if (act) e = lds_u32(list_base | ((head_b + 4u * lane) & (4u * kS33Ring - 4u)));
   int idx[K];
   float w[K];
   Node2 v[K];
@@ -847,49 +850,38 @@ __device__ __forceinline__ void s33_round(S33Warp& B, uint32_t head, int m, uint
     a01 = __ffma2_rn(make_float2(w[k], w[k]), v[k].xy, a01);
     a2 = fmaf(w[k], v[k].z, a2);
   }
-  const int64_t P = ((int32_t)e < 0 ? b1 : b0) + (int64_t)((e >> 24) & 127u);
-  if (planar) {                   // one plane per store: list order is address order
-    if (act) {
-      out[P] = a01.x; out[n + P] = a01.y; out[2 * n + P] = a2;
-    }
-    return;
-  }
-  if constexpr (!SORTED) {
-    if (act) {
-      float* d = out + 3 * P;
+  float* d = (int32_t)e < 0 ? q1 : q0;
+  const uint32_t pos = (e >> 24) & 127u;
+  if (act) {
+    if constexpr (PLANAR) {
+      d += pos;
+      d[0] = a01.x; d[n] = a01.y; d[2 * n] = a2;
+    } else {
+      d += 3u * pos;
       d[0] = a01.x; d[1] = a01.y; d[2] = a2;
     }
-  } else {
-    float* t = B.tr + 3 * lane;   // stride 3 words: conflict-free
-    t[0] = a01.x; t[1] = a01.y; t[2] = a2;
-    __syncwarp();
-    const uint32_t plo = (uint32_t)P, phi = (uint32_t)((uint64_t)P >> 32);
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      const uint32_t k = 32u * j + lane, slot = (k * 171u) >> 9, comp = k - 3u * slot;   // k / 3 for k < 96
-      const float val = B.tr[k];
-      const uint32_t slo = __shfl_sync(0xffffffffu, plo, slot), shi = __shfl_sync(0xffffffffu, phi, slot);
-      const int64_t Ps = (int64_t)(((uint64_t)shi << 32) | slo);
-      if ((int)slot < m) out[3 * Ps + comp] = val;
-    }
-    __syncwarp();                 // tr is rewritten by the next round
   }
 }
 
-template <int METHOD, bool SORTED>
+template <int METHOD, bool PLANAR>
 __global__ void __launch_bounds__(kS33NW * 32, 1)
     k_lut33_split(const float4* __restrict__ lat4, const uint8_t* __restrict__ rgb, float* __restrict__ out,
-                  int64_t n, int64_t nslices, int planar) {
-  extern __shared__ __align__(128) uint8_t smem_s33[];
+                  int64_t n, int64_t nslices) {
+  extern __shared__ __align__(1024) uint8_t smem_s33[];
   S33Shared* S = reinterpret_cast<S33Shared*>(smem_s33);
   const uint32_t rank = blockIdx.x & 1u;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const uint32_t list_base = smem_u32(S->list[warp]);
+  if (list_base & (4u * kS33Ring - 1u)) __trap();             // ring addressing ORs the offset into the base
   const uint32_t* in_w = reinterpret_cast<const uint32_t*>(rgb);
-  const int64_t nbytes = 3 * n;
+  const int64_t nbytes = 3 * n, nfull = n / kP33Slice;
+  // bytes past the end of the buffer read as a colour of the OTHER half, so the
+  // ragged last slice needs no bounds test in the scan
+  const uint32_t fill = rank ? 0u : 0x80u;
   auto load = [&](int64_t sl, uint32_t (&wd)[3]) {
     const int64_t w0 = sl * (kP33Slice * 3 / 4) + 3 * lane;   // word index
-    if ((sl + 1) * kP33Slice <= n) {                            // a whole slice: no per-word checks
+    if (sl < nfull) {                                           // a whole slice: no per-byte checks
 #pragma unroll
       for (int c = 0; c < 3; ++c) wd[c] = __ldg(in_w + w0 + c);
       return;
@@ -899,7 +891,7 @@ __global__ void __launch_bounds__(kS33NW * 32, 1)
       uint32_t v = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (4 * (w0 + c) + k < nbytes) v |= (uint32_t)rgb[4 * (w0 + c) + k] << (8 * k);
+        v |= (4 * (w0 + c) + k < nbytes ? (uint32_t)rgb[4 * (w0 + c) + k] : fill) << (8 * k);
       wd[c] = v;
     }
   };
@@ -915,51 +907,49 @@ __global__ void __launch_bounds__(kS33NW * 32, 1)
       S->pk[i] = lut_quant_pack(q, __ldg(lat4 + first + i));
   }
   __syncthreads();
-  S33Warp& B = S->wb[warp];
   const uint32_t pk_base = smem_u32(S->pk) - rank * (16u * kL33Plane * 8u);
   const uint32_t lt = lanemask_lt();
-  uint32_t head = 0, par = 0;
+  const uint32_t flip = rank ? 0u : 0x80808080u;   // after the flip, bit 7 of r set <=> the pixel is mine
+  uint32_t head_b = 0;                 // ring byte offset of the oldest pending entry
+  uint32_t tag0 = (4u * lane) << 24;   // pos << 24 | slice parity << 31 of the lane's first pixel
   int cnt = 0;
-  int64_t b0 = 0, b1 = 0;              // first pixel of the latest slice of parity 0 / 1
+  float *q0 = out, *q1 = out;
   auto round = [&](int m) {
-    if (q.on) s33_round<METHOD, true, SORTED>(B, head, m, rank, lane, pk_base, lat4, q, b0, b1, out, n, planar);
-    else s33_round<METHOD, false, SORTED>(B, head, m, rank, lane, pk_base, lat4, q, b0, b1, out, n, planar);
-    head = (head + (uint32_t)m) & (kS33Ring - 1);
+    if (q.on) s33_round<METHOD, true, PLANAR>(list_base, head_b, m, rank, lane, pk_base, lat4, q, q0, q1, n);
+    else s33_round<METHOD, false, PLANAR>(list_base, head_b, m, rank, lane, pk_base, lat4, q, q0, q1, n);
+    head_b += 4u * (uint32_t)m;
     cnt -= m;
   };
   for (; sl < nslices; sl += stride) {
-    const uint32_t wd[3] = {nxt[0], nxt[1], nxt[2]};
+    const uint32_t w0 = nxt[0], w1 = nxt[1], w2 = nxt[2];
     if (sl + stride < nslices) load(sl + stride, nxt);
-    const int64_t px0 = sl * kP33Slice;
-    const int64_t left = n - px0;
-    const int valid = left >= kP33Slice ? kP33Slice : (int)left;
-    if (par) b1 = px0; else b0 = px0;
+    float* qs = out + (PLANAR ? 1 : 3) * (sl * kP33Slice);
+    if ((int32_t)tag0 < 0) q1 = qs; else q0 = qs;
     const int old = cnt;
-    // ---- my pixels of the slice, appended in pixel order
-    uint32_t bal[4];
-    int pre = 0, M = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t r = byte_of(wd[(3 * k) >> 2], (3 * k) & 3);
-      const bool mine = (r >> 7) == rank && (int)(4 * lane) + k < valid;
-      bal[k] = __ballot_sync(0xffffffffu, mine);
-      M += __popc(bal[k]);
-      pre += __popc(bal[k] & lt);
-    }
-    {
-      uint32_t j = head + (uint32_t)cnt + (uint32_t)pre;
-      const uint32_t tag = (par << 31) | ((4u * lane) << 24);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if ((bal[k] >> lane) & 1u) {
-          const int o = 3 * k;   // byte offset of the pixel in the lane's 12 bytes
-          const uint32_t r = byte_of(wd[o >> 2], o & 3), g = byte_of(wd[(o + 1) >> 2], (o + 1) & 3),
-                         b = byte_of(wd[(o + 2) >> 2], (o + 2) & 3);
-          B.list[j++ & (kS33Ring - 1)] = (r | g << 8 | b << 16) | (tag + ((uint32_t)k << 24));
-        }
-      }
-    }
-    cnt += M;
+    // ---- my pixels of the slice: pixel column k = pixels 4 lane + k.  The r bytes
+    // of the four pixels sit at byte 0 / 3 of w0, byte 2 of w1, byte 1 of w2.
+    const uint32_t f0 = w0 ^ flip, f1 = w1 ^ flip, f2 = w2 ^ flip;
+    const bool m0 = f0 & 0x80u, m1 = f0 & 0x80000000u, m2 = f1 & 0x800000u, m3 = f2 & 0x8000u;
+    const uint32_t e0 = __byte_perm(w0, tag0, 0x7210);
+    const uint32_t e1 = (__byte_perm(w0, w1, 0x0543) & 0xFFFFFFu) | (tag0 + (1u << 24));
+    const uint32_t e2 = (__byte_perm(w1, w2, 0x0432) & 0xFFFFFFu) | (tag0 + (2u << 24));
+    const uint32_t e3 = __byte_perm(w2, tag0 + (3u << 24), 0x7321);
+    // list order = pixel order (lane-major): a round's 32 entries then cover ~64
+    // consecutive pixels, so its stores touch ~24 sectors; appending column by
+    // column (entries 16 B apart... one sector each) measured 116 vs 128 Gpix/s
+    const uint32_t bal0 = __ballot_sync(0xffffffffu, m0), bal1 = __ballot_sync(0xffffffffu, m1),
+                   bal2 = __ballot_sync(0xffffffffu, m2), bal3 = __ballot_sync(0xffffffffu, m3);
+    const int pre = __popc(bal0 & lt) + __popc(bal1 & lt) + __popc(bal2 & lt) + __popc(bal3 & lt);
+    uint32_t a = head_b + 4u * (uint32_t)(cnt + pre);
+    constexpr uint32_t RM = 4u * kS33Ring - 4u;
+    if (m0) sts_u32(list_base | (a & RM), e0);
+    a += m0 ? 4u : 0u;
+    if (m1) sts_u32(list_base | (a & RM), e1);
+    a += m1 ? 4u : 0u;
+    if (m2) sts_u32(list_base | (a & RM), e2);
+    a += m2 ? 4u : 0u;
+    if (m3) sts_u32(list_base | (a & RM), e3);
+    cnt += __popc(bal0) + __popc(bal1) + __popc(bal2) + __popc(bal3);
     MACT_DCHECK(cnt <= kS33Ring);
     __syncwarp();
     // ---- full rounds; a remainder from before this slice goes out now
@@ -968,7 +958,7 @@ __global__ void __launch_bounds__(kS33NW * 32, 1)
     } else if (old > 0) {
       round(cnt);
     }
-    par ^= 1u;
+    tag0 ^= 0x80000000u;
   }
   if (cnt > 0) round(cnt);
 }
@@ -1629,7 +1619,7 @@ static int launch_lut33_split(const float* lat, const uint8_t* rgb, float* out, 
     return check_launch("lut_interp");
   }
   const int64_t nslices = (n + kP33Slice - 1) / kP33Slice;
-  auto kfn = k_lut33_split<METHOD, MACT_LUT33S_SORTED != 0>;
+  auto kfn = planar ? k_lut33_split<METHOD, true> : k_lut33_split<METHOD, false>;
   const int64_t cap = persistent_grid((const void*)kfn, kS33NW * 32, kS33Smem);
   if (cap <= 0) return MACT_ECUDA;
   int64_t pairs = cap / 2;
@@ -1637,7 +1627,7 @@ static int launch_lut33_split(const float* lat, const uint8_t* rgb, float* out, 
   if (pairs > need) pairs = need;
   if (pairs < 1) pairs = 1;
   kfn<<<(unsigned)(2 * pairs), kS33NW * 32, kS33Smem, st>>>(reinterpret_cast<const float4*>(lat), rgb, out, n,
-                                                           nslices, planar);
+                                                           nslices);
   count_launch();
   return check_launch("lut33_split");
 }
