@@ -100,6 +100,7 @@ __device__ __forceinline__ void lut_quant_f(uint2 w, float2& f01, float& f2) {
 __device__ __forceinline__ Node2 lut_quant_unpack2(const LutQuant& q, uint2 w) {
   // The kernel is ALU-pipe bound, so q0 and q2 are extracted on the FMA pipe
   // (IMAD / IMAD.HI) rather than with LOP3 / SHF: 17^3 tetrahedral +5 %.
+  // (ptxas turns these mad.hi by powers of two into LEA.HI; forcing IMAD.HI measured slower)
   uint32_t t0;
   asm("mul.lo.u32 %0, %1, %2;" : "=r"(t0) : "r"(w.x), "r"(1u << 11));       // q0 to the top bits
   const float f0 = __uint_as_float(mad_hi_u32(t0, 1u << 21, 0x4B000000u));
@@ -195,7 +196,8 @@ struct OpLut {
   static __device__ __forceinline__ void locate_g(uint32_t r, uint32_t g, uint32_t b, int& bf, int& rr,
                                                   int& rg, int& rb) {
     const uint32_t xr = r * (N - 1), xg = g * (N - 1), xb = b * (N - 1);
-    uint32_t br = __umulhi(xr, 0x01010102u), bg = __umulhi(xg, 0x01010102u), bb = __umulhi(xb, 0x01010102u);
+    constexpr uint32_t MG = 0x01010102u * (uint32_t)(N - 1);   // the factor n-1 folded into the magic
+    uint32_t br = __umulhi(r, MG), bg = __umulhi(g, MG), bb = __umulhi(b, MG);
     if constexpr (METHOD == MACT_LUT_PYRAMIDAL) {
       // the pyramid scheme is not continuous across cells (its far faces are
       // triangulated, its near faces bilinear), so p = 255 keeps the
@@ -837,7 +839,7 @@ __device__ __forceinline__ void s33_round(uint32_t list_base, uint32_t head_b, i
   int idx[K];
   float w[K];
   Node2 v[K];
-  Lut33Sel<METHOD>::template select<true>(e & 0xFFu, (e >> 8) & 0xFFu, (e >> 16) & 0xFFu, idx, w);
+  Lut33Sel<METHOD>::template select<true>(byte_of(e, 0), byte_of(e, 1), byte_of(e, 2), idx, w);
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     MACT_DCHECK(!PK || (uint32_t)(idx[k] - 16 * kL33Plane * (int)rank) < (uint32_t)(kL33Planes * kL33Plane));

@@ -32,11 +32,11 @@ template <> struct LutK<MACT_LUT_TETRAHEDRAL> { static constexpr int K = 4; };
 template <int N>
 __device__ __forceinline__ void lut_locate(uint32_t p, int& base, int& rem) {
   static_assert(N >= 2 && N <= 33, "shift-free /255 is exact for p (n-1) <= 8160");
-  const uint32_t x = p * (uint32_t)(N - 1);
-  uint32_t bse = __umulhi(x, 0x01010102u);
+  // hi(p (n-1) * 0x01010102) with the factor n-1 folded into the magic (< 2^32 for n <= 33)
+  uint32_t bse = __umulhi(p, 0x01010102u * (uint32_t)(N - 1));
   bse = bse > (uint32_t)(N - 2) ? (uint32_t)(N - 2) : bse;
   base = (int)bse;
-  rem = (int)(x - 255u * bse);
+  rem = (int)(p * (uint32_t)(N - 1) - 255u * bse);
 }
 
 // Node flat indices and weights of one pixel.  rem values in [0,255].
@@ -93,14 +93,26 @@ __device__ __forceinline__ void lut_nodes_at(int bf, int rr, int rg, int rb,
     w[3] = (W)(u * v - 255 * m) * inv2;
     w[4] = (W)m * inv1;
   } else if constexpr (!TIES) {
-    const int d1 = max(rr, max(rg, rb)), d3 = min(rr, min(rg, rb)), d2 = rr + rg + rb - d1 - d3;
-    const int s1 = rr == d1 ? SR : rg == d1 ? SG : SB;     // stride of the largest offset
-    const int s3 = rb == d3 ? SB : rg == d3 ? SG : SR;     // ... of the smallest (!= s1 unless all equal)
+    // keys offset << 16 | stride: max3 / min3 give the largest / smallest offset
+    // together with its axis (under ties any of the tied axes: the node it
+    // selects carries weight 0): two 3-input min / max, two shifts and two masks
+    // in place of four compares and four selects.  (Routing the shifts and field
+    // extractions through IMAD.HI with multipliers ptxas cannot fold -- FMA pipe
+    // instead of ALU -- measured 20 % slower on every LUT kernel: IMAD.HI is not
+    // a full-rate instruction.)
+    static_assert(SR < 65536, "stride field");
+    const uint32_t kr = ((uint32_t)rr << 16) + (uint32_t)SR, kg = ((uint32_t)rg << 16) + (uint32_t)SG,
+                   kb = ((uint32_t)rb << 16) + (uint32_t)SB;
+    const uint32_t k1 = max(kr, max(kg, kb)), k3 = min(kr, min(kg, kb));
+    const int d1 = (int)(k1 >> 16), d3 = (int)(k3 >> 16);
+    const int s1 = (int)(k1 & 0xFFFFu), s3 = (int)(k3 & 0xFFFFu);
+    const int d2 = rr + rg + rb - d1 - d3;
     idx[0] = bf; idx[1] = bf + s1; idx[2] = bf + SR + SG + SB - s3; idx[3] = bf + SR + SG + SB;
-    w[0] = (W)(255 - d1) * inv1;
-    w[1] = (W)(d1 - d2) * inv1;
-    w[2] = (W)(d2 - d3) * inv1;
-    w[3] = (W)d3 * inv1;
+    const W f1 = (W)d1, f2 = (W)d2, f3 = (W)d3;              // integers <= 255: the differences are exact
+    w[0] = ((W)255 - f1) * inv1;
+    w[1] = (f1 - f2) * inv1;
+    w[2] = (f2 - f3) * inv1;
+    w[3] = f3 * inv1;
   } else {
     // stable argsort of -d (lut.py:185): ties keep r before g before b
     const int pos_r = (rg > rr) + (rb > rr);
