@@ -183,29 +183,19 @@ struct OpLut {
   // 2 x 5.2 for the two LDS.64 it replaces) and the interpolation runs as 7
   // lerps instead of 8 weight products (tri_px below).
   static constexpr bool PAIR = PACK && METHOD == MACT_LUT_TRILINEAR;
-  // 17^3 is staged with one ghost plane per axis (18^3 nodes, copies of the
-  // edge nodes), so cell location needs no clamp: p = 255 lands in cell 16 at
-  // offset 0, where the ghost nodes carry weight exactly 0 -- the same point
-  // of the interpolant as cell 15 at offset 255 for the schemes that are
-  // continuous across cells (trilinear, prism, tetrahedral).  base = x / 255 for
-  // x = 16 p <= 4080 is one IMAD.HI with the shift-free magic 0x01010102
-  // (exact on that range), so locating is FMA-pipe work in an ALU-bound kernel.
-  static constexpr int NG = PACK ? N + 1 : N;
+  // Cell location is the reference's (lut.py:98-105): for byte pixels
+  // min(p (n-1) div 255, n-2) is the shift p >> 4 (lut_locate), p = 255 in cell
+  // n-2 at offset 255 -- no clamp, no ghost planes (R01 staged 18^3 nodes to
+  // avoid the clamp of the /255 magic; the shift needs neither).
+  static constexpr int NG = N;
   static constexpr int NNG = NG * NG * NG;
-  static_assert(!PACK || N == 17, "shift-free /255 is exact for 16 p <= 4080 only");
   static __device__ __forceinline__ void locate_g(uint32_t r, uint32_t g, uint32_t b, int& bf, int& rr,
                                                   int& rg, int& rb) {
-    const uint32_t xr = r * (N - 1), xg = g * (N - 1), xb = b * (N - 1);
-    constexpr uint32_t MG = 0x01010102u * (uint32_t)(N - 1);   // the factor n-1 folded into the magic
-    uint32_t br = __umulhi(r, MG), bg = __umulhi(g, MG), bb = __umulhi(b, MG);
-    if constexpr (METHOD == MACT_LUT_PYRAMIDAL) {
-      // the pyramid scheme is not continuous across cells (its far faces are
-      // triangulated, its near faces bilinear), so p = 255 keeps the
-      // reference's cell N-2 at offset 255 (lut.py:98-105)
-      br = min(br, (uint32_t)(N - 2)); bg = min(bg, (uint32_t)(N - 2)); bb = min(bb, (uint32_t)(N - 2));
-    }
-    rr = (int)(xr - 255u * br); rg = (int)(xg - 255u * bg); rb = (int)(xb - 255u * bb);
-    bf = (int)(br * (NG * NG) + bg * NG + bb);
+    int br, bg, bb;
+    lut_locate<N>(r, br, rr);
+    lut_locate<N>(g, bg, rg);
+    lut_locate<N>(b, bb, rb);
+    bf = (br * NG + bg) * NG + bb;
   }
   struct Shared {
     float4 lat[PRIV ? 8 * N * N * N : 1];
@@ -226,11 +216,10 @@ struct OpLut {
     } else if constexpr (PACK) {
       lut_quant_setup(p.lat, N * N * N, &s->q, s->red);   // ends with __syncthreads
       const LutQuant q = s->q;
-      for (int i = threadIdx.x; i < NNG; i += blockDim.x) {   // ghost nodes copy the edge
-        const int ir = min(i / (NG * NG), N - 1), ig = min((i / NG) % NG, N - 1), ib = min(i % NG, N - 1);
-        const float4 v = __ldg(p.lat + (ir * N + ig) * N + ib);
+      for (int i = threadIdx.x; i < NNG; i += blockDim.x) {
+        const float4 v = __ldg(p.lat + i);
         if (q.on && PAIR) {   // node i and its b neighbour (the last b plane pairs with itself; never used)
-          const float4 v1 = __ldg(p.lat + (ir * N + ig) * N + min(i % NG + 1, N - 1));
+          const float4 v1 = __ldg(p.lat + min(i + 1, NNG - 1));
           const uint2 a = lut_quant_pack(q, v), b = lut_quant_pack(q, v1);
           s->u.pk2[i] = make_uint4(a.x, a.y, b.x, b.y);
         } else if (q.on) {
@@ -271,28 +260,13 @@ struct OpLut {
     else return LutQuant{};
   }
   // Cell location and node selection of one pixel exactly as the interpolation
-  // kernels run it (indices into the staged NG^3 lattice; mact_lut_nodes_timed
-  // emits them for the parity tests).
-  // GHOST = false (the fp32-plane fallback, i.e. lattices that may hold
-  // non-finite nodes) keeps the reference's clamped cell in the staged NG^3
-  // lattice, so p = 255 never puts a zero weight on an inf / NaN node the
-  // reference does not touch.
-  template <bool GHOST = true>
+  // kernels run it (mact_lut_nodes_timed emits them for the parity tests): the
+  // reference's cell, the reference's simplex; only the tetrahedral zero-weight
+  // middle node under ties may be another corner (lut_nodes_at, TIES = false).
+  template <bool = true>
   static __device__ __forceinline__ void select(uint32_t r, uint32_t g, uint32_t b,
                                                 int (&idx)[LutK<METHOD>::K], float (&w)[LutK<METHOD>::K]) {
-    if constexpr (PACK && GHOST) {
-      int bf, rr, rg, rb;
-      locate_g(r, g, b, bf, rr, rg, rb);
-      lut_nodes_at<NG, METHOD, float, false>(bf, rr, rg, rb, idx, w);
-    } else if constexpr (PACK) {
-      int br, bg, bb, rr, rg, rb;
-      lut_locate<N>(r, br, rr);
-      lut_locate<N>(g, bg, rg);
-      lut_locate<N>(b, bb, rb);
-      lut_nodes_at<NG, METHOD, float, false>((br * NG + bg) * NG + bb, rr, rg, rb, idx, w);
-    } else {
-      lut_nodes<N, METHOD, float, false>(r, g, b, idx, w);
-    }
+    lut_nodes<N, METHOD, float, false>(r, g, b, idx, w);
   }
   static __device__ __forceinline__ void px(uint32_t r, uint32_t g, uint32_t b, const Shared* s,
                                             uint32_t lane, const Params& p, float (*o)[3]) {
@@ -1167,9 +1141,8 @@ __global__ void k_lut_nodes(const uint8_t* __restrict__ rgb, int64_t n, int32_t*
   }
 }
 
-// The interpolation kernels' own selection (Op::select: TIES = false, the
-// 17^3 ghost planes), node indices mapped back to the n^3 lattice (a ghost
-// node is a copy of the edge node it maps to, and carries weight 0).
+// The interpolation kernels' own selection (Op::select: the reference's cells;
+// TIES = false, so a tie's zero-weight middle node may be another corner).
 template <int N, int METHOD>
 __global__ void k_lut_nodes_timed(const uint8_t* __restrict__ rgb, int64_t n, int32_t* __restrict__ nodes,
                                   float* __restrict__ weights) {

@@ -32,11 +32,22 @@ template <> struct LutK<MACT_LUT_TETRAHEDRAL> { static constexpr int K = 4; };
 template <int N>
 __device__ __forceinline__ void lut_locate(uint32_t p, int& base, int& rem) {
   static_assert(N >= 2 && N <= 33, "shift-free /255 is exact for p (n-1) <= 8160");
-  // hi(p (n-1) * 0x01010102) with the factor n-1 folded into the magic (< 2^32 for n <= 33)
-  uint32_t bse = __umulhi(p, 0x01010102u * (uint32_t)(N - 1));
-  bse = bse > (uint32_t)(N - 2) ? (uint32_t)(N - 2) : bse;
-  base = (int)bse;
-  rem = (int)(p * (uint32_t)(N - 1) - 255u * bse);
+  if constexpr (N == 9 || N == 17 || N == 33) {
+    // 256 / (n-1) = 2^S: min(p (n-1) div 255, n-2) == p >> S for every byte p,
+    // the clamp of p = 255 included (255 >> S = n-2), so the cell is one shift
+    // -- no IMAD.HI (not a full-rate instruction) and no clamp.  Checked
+    // exhaustively in tests/test_host_logic.py.
+    constexpr int S = N == 9 ? 5 : N == 17 ? 4 : 3;
+    const uint32_t bse = p >> S;
+    base = (int)bse;
+    rem = (int)(p * (uint32_t)(N - 1) - 255u * bse);
+  } else {
+    // hi(p (n-1) * 0x01010102) with the factor n-1 folded into the magic (< 2^32 for n <= 33)
+    uint32_t bse = __umulhi(p, 0x01010102u * (uint32_t)(N - 1));
+    bse = bse > (uint32_t)(N - 2) ? (uint32_t)(N - 2) : bse;
+    base = (int)bse;
+    rem = (int)(p * (uint32_t)(N - 1) - 255u * bse);
+  }
 }
 
 // Node flat indices and weights of one pixel.  rem values in [0,255].

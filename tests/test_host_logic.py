@@ -117,3 +117,12 @@ def test_shift_free_div255_magic():
     hi(x * 0x01010102) (csrc/mact_lut.cuh): exact for every x <= 8160 (33^3)."""
     x = np.arange(0, 8161, dtype=np.uint64)
     assert np.array_equal((x * np.uint64(0x01010102)) >> np.uint64(32), x // np.uint64(255))
+
+
+def test_lut_cell_is_a_shift_for_byte_pixels():
+    """lut_locate (csrc/mact_lut.cuh) for n = 9 / 17 / 33: the reference's cell
+    min(p (n-1) div 255, n-2) (lut.py:98-105) equals p >> log2(256 / (n-1)) for
+    every byte p, the clamp at p = 255 included."""
+    p = np.arange(256)
+    for n, s in ((9, 5), (17, 4), (33, 3)):
+        assert np.array_equal(np.minimum(p * (n - 1) // 255, n - 2), p >> s)
