@@ -15,10 +15,11 @@
 // LDS.64 + one LDS.32 per node.  Random gathers are bank-conflict bound: on
 // B200 a random warp LDS.64 costs 5.2 smem cycles, LDS.64 + LDS.32 7.9, one
 // LDS.128 of a padded float4 node 9.4 (tools/ldsbench.cu).  33^3 exceeds a
-// CTA's 227 KB even as fixed-point nodes (287 KB): a 2-CTA cluster holds half
-// of the r-planes per CTA and each pixel is interpolated by the CTA holding
-// its cell (k_lut33_pair); planar output uses 3 independent CTAs holding one
-// fp32 component each (k_lut33_planar).
+// CTA's 227 KB even as fixed-point nodes (287 KB): CTAs come in pairs, each
+// holding half of the r-planes (148 KB) and interpolating the pixels whose
+// cell lies in its half, results scattered straight to global memory
+// (k_lut33_split; the cluster version with a DSMEM exchange, k_lut33_pair, and
+// the component-split CTAs, k_lut33_comp / k_lut33_planar, remain selectable).
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -1607,20 +1608,23 @@ static int launch_lut33_split(const float* lat, const uint8_t* rgb, float* out, 
   return check_launch("lut33_split");
 }
 
-// 33^3 kernel selection: the r-split CTA pairs (k_lut33_pair) serve
-// interleaved output -- measured faster on C3 than the component-split
-// clusters (trilinear / prism / pyramidal / tetrahedral 81 / 87 / 91 / 96 vs
-// 79 / 80 / 85 / 93 Gpix/s) -- and the independent component CTAs
-// (k_lut33_planar, no exchange) planar output.  MACT_LUT33_KERNEL=pair|comp
-// forces one family for A/B runs; read per call (a getenv is ~100 ns next to
-// a launch), so tests can exercise both in one process.
+// 33^3 kernel selection: the r-split independent CTAs (k_lut33_split) serve
+// both layouts -- measured on C3 (trilinear / prism / pyramidal / tetrahedral):
+// split 117 / 135 / 142 / 156 Gpix/s interleaved and 116 / 132 / 132 / 145
+// planar, against 80 / 85 / 91 / 95 for the r-split cluster pairs
+// (k_lut33_pair, DSMEM exchange) and 80 / 97 / 107 / 126 planar for the
+// component CTAs (k_lut33_planar).  MACT_LUT33_KERNEL=split|pair|comp forces
+// one family for A/B runs and for the parity tests of the older kernels; read
+// per call (a getenv is ~100 ns next to a launch), so tests can exercise all
+// of them in one process.
 enum { kLut33Split = 0, kLut33Pair = 1, kLut33Comp = 2 };
 static int lut33_kernel(int planar) {
   const char* e = getenv("MACT_LUT33_KERNEL");
   if (e && strcmp(e, "split") == 0) return kLut33Split;
   if (e && strcmp(e, "pair") == 0) return kLut33Pair;
   if (e && strcmp(e, "comp") == 0) return kLut33Comp;
-  return planar != 0 ? kLut33Comp : kLut33Pair;
+  (void)planar;
+  return kLut33Split;
 }
 
 template <int N, int METHOD>

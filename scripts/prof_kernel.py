@@ -20,6 +20,7 @@ ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--method", default="tetrahedral")
 ap.add_argument("--input", default="random")
 ap.add_argument("--time", action="store_true")
+ap.add_argument("--planar", action="store_true")
 a = ap.parse_args()
 
 lib = _lib.load()
@@ -48,7 +49,7 @@ def run():
                                      outs[2].data_ptr(), n, cfg.coeffs, 0, st))
     elif a.op.startswith("exactf32_"):
         sp = {"exactf32_lab": 0, "exactf32_hsi": 1, "exactf32_sct": 2}[a.op]
-        _lib.check(lib.mact_exact_f32(sp, x.data_ptr(), outs[0].data_ptr(), n, 0, st))
+        _lib.check(lib.mact_exact_f32(sp, x.data_ptr(), outs[0].data_ptr(), n, int(a.planar), st))
     elif a.op.startswith("exact_"):
         sp = {"exact_lab": 0, "exact_hsi": 1, "exact_sct": 2}[a.op]
         _lib.check(lib.mact_exact(sp, x.data_ptr(), 0, outs[0].data_ptr(), 1, n, st))
@@ -60,7 +61,7 @@ def run():
     else:
         lat = lt.lattice()
         _lib.check(lib.mact_lut_interp(lat.data_ptr(), lt.grid_n, _lib.METHODS[a.method],
-                                       x.data_ptr(), outs[0].data_ptr(), n, 0, st))
+                                       x.data_ptr(), outs[0].data_ptr(), n, int(a.planar), st))
 
 
 for _ in range(2):

@@ -121,7 +121,7 @@ def test_lut_interp_c3_image(P, n, method):
     for r0 in (0, 3584):
         check_lab(got[r0:r0 + 512], O.interpolate(vals, img[r0:r0 + 512], method))
     part = P["lut"].interpolate(lt, d.reshape(-1, 3)[5:100005], method, layout="planar").cpu().numpy()
-    if n == 33:   # interleaved: the r-split pairs; planar: the component CTAs (fp32 nodes)
+    if n == 33:   # both layouts run the r-split CTAs (same arithmetic); kept as a tolerance check
         check_lab(part.T, O.interpolate(vals, img.reshape(-1, 3)[5:100005], method))
     else:
         np.testing.assert_array_equal(part.T, got.reshape(-1, 3)[5:100005])
@@ -182,7 +182,7 @@ def test_lut_interp_host_executor(grid, method):
     lut.interpolate(L, pin_in.numpy(), method, out=pin_out.numpy())
     np.testing.assert_array_equal(pin_out.numpy(), ref)
     planar = lut.interpolate(L, px[:5000], method, layout="planar").T
-    if grid == 33:   # planar 33^3 runs the component CTAs (fp32 nodes), interleaved the pairs
+    if grid == 33:   # (older 33^3 families mixed fp32 and fixed-point nodes; kept as a tolerance check)
         check_lab(planar, ref[:5000])
     else:
         np.testing.assert_array_equal(planar, ref[:5000])
@@ -194,8 +194,8 @@ def test_lut_interp_host_executor(grid, method):
 def test_lut33_planar_equals_interleaved(monkeypatch, kernel, n, method):
     """33^3 planar output == interleaved output within one kernel family (forced
     with MACT_LUT33_KERNEL; tails and odd sizes take the per-pixel kernel of the
-    same arithmetic).  By default interleaved runs the pairs and planar the
-    component CTAs: test_lut33_both_kernels checks each against the oracle."""
+    same arithmetic).  The default is "split" for both layouts;
+    test_lut33_both_kernels checks every family against the oracle."""
     from paper_1009_0854_b200 import lut
     monkeypatch.setenv("MACT_LUT33_KERNEL", kernel)
     px = torch.from_numpy(np.random.default_rng(n).integers(0, 256, (n, 3), dtype=np.uint8)).cuda()
@@ -243,7 +243,7 @@ def test_lut_beyond_int32_pixel_count(grid):
 @pytest.mark.parametrize("method", O.METHODS)
 def test_lut_interp_full_cube(P, n, method):
     """The TIMED uint8 kernels (9^3 bank-private copies, 17^3 fixed-point nodes
-    with ghost planes, 33^3 r-split CTA pairs; planar 33^3: component CTAs) on
+    in the reference's cells, 33^3 r-split independent CTAs for both layouts) on
     all 2^24 colours vs the oracle on the same fp32 lattice values; 9^3 / 17^3
     planar output bit-identical to interleaved.  The fixed-point formats stay
     inside 1e-4 (quantisation half-step <= 4.4e-5)."""
@@ -276,11 +276,11 @@ def _sorted_nonzero(nodes, w, tiny):
 @pytest.mark.parametrize("method", O.METHODS)
 def test_timed_kernel_selection_full_cube(P, n, method):
     """Cells and simplices of the INTERPOLATION kernels (their own select():
-    tetrahedral order from max/min/sum, 17^3 ghost cells at p = 255) on all 2^24
-    colours: the nodes carrying nonzero weight are exactly the reference's
-    (lut.py:98-199), with the same weights to fp32 rounding.  Only zero-weight
-    nodes may differ (a tie's middle corner, a ghost node = a copy of the edge
-    node); fmaf(0, v, a) == a, so they cannot change a sum of finite nodes."""
+    tetrahedral order from max/min keys) on all 2^24 colours: the cells are the
+    reference's, and the nodes carrying nonzero weight are exactly the
+    reference's (lut.py:98-199), with the same weights to fp32 rounding.  Only a
+    zero-weight node may differ (a tie's middle corner); fmaf(0, v, a) == a, so
+    it cannot change a sum of finite nodes."""
     from paper_1009_0854_b200 import _lib
     k = P["lut"].NEIGHBOR_COUNT[method]
     cube = P["harness"].cube_chunk(0, 1 << 24, device="cuda")
@@ -375,7 +375,8 @@ def test_lut_error_bound_either_format(P, n, scale, method):
 @pytest.mark.parametrize("kernel", ["comp", "pair", "split"])
 @pytest.mark.parametrize("method", O.METHODS)
 def test_lut33_both_kernels(P, monkeypatch, kernel, method):
-    """Both 33^3 interpolation kernels -- the r-split CTA pairs (default for
+    """Every 33^3 interpolation kernel family -- the r-split independent CTAs (the
+    default), the r-split cluster pairs (once the default for
     interleaved output) and the component-split clusters (MACT_LUT33_KERNEL=comp;
     default for planar output) -- against the oracle on the
     same fp32 lattice: 2^20 random colours plus the cube's corners and faces,
