@@ -85,6 +85,23 @@ struct Node2 {
   float2 xy;
   float z;
 };
+// (x & 0x1FFFFF) | 0x4B000000 as ONE LOP3: with both constants visible ptxas
+// emits two LOP3 (an instruction takes one immediate), so the magic comes from
+// constant memory, which it does not fold -- it is loaded into a register once
+// per kernel.  Read-only, never written.
+#ifndef MACT_LUT_FUSED_LOP
+#define MACT_LUT_FUSED_LOP 1
+#endif
+static __constant__ uint32_t kLutMagic23 = 0x4B000000u;
+__device__ __forceinline__ uint32_t lut_field21(uint32_t x) {
+#if MACT_LUT_FUSED_LOP
+  uint32_t r;
+  asm("lop3.b32 %0, %1, 0x1FFFFF, %2, 0xEA;" : "=r"(r) : "r"(x), "r"(kLutMagic23));
+  return r;
+#else
+  return (x & 0x1FFFFFu) | 0x4B000000u;
+#endif
+}
 __device__ __forceinline__ uint32_t mad_hi_u32(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t r;   // hi(a * b) + c on the FMA pipe (IMAD.HI), where a shift + add would take the ALU pipe
   asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
@@ -95,7 +112,7 @@ __device__ __forceinline__ void lut_quant_f(uint2 w, float2& f01, float& f2) {
   uint32_t t0;
   asm("mul.lo.u32 %0, %1, %2;" : "=r"(t0) : "r"(w.x), "r"(1u << 11));
   f01.x = __uint_as_float(mad_hi_u32(t0, 1u << 21, 0x4B000000u));
-  f01.y = __uint_as_float((__funnelshift_r(w.x, w.y, 21) & 0x1FFFFFu) | 0x4B000000u);
+  f01.y = __uint_as_float(lut_field21(__funnelshift_r(w.x, w.y, 21)));
   f2 = __uint_as_float(mad_hi_u32(w.y, 1u << 22, 0x4B000000u));
 }
 __device__ __forceinline__ Node2 lut_quant_unpack2(const LutQuant& q, uint2 w) {
@@ -106,7 +123,7 @@ __device__ __forceinline__ Node2 lut_quant_unpack2(const LutQuant& q, uint2 w) {
   asm("mul.lo.u32 %0, %1, %2;" : "=r"(t0) : "r"(w.x), "r"(1u << 11));       // q0 to the top bits
   const float f0 = __uint_as_float(mad_hi_u32(t0, 1u << 21, 0x4B000000u));
   // (q1 on the FMA pipe as well -- three IMADs -- measured within +-1 %: kept on the ALU)
-  const float f1 = __uint_as_float((__funnelshift_r(w.x, w.y, 21) & 0x1FFFFFu) | 0x4B000000u);
+  const float f1 = __uint_as_float(lut_field21(__funnelshift_r(w.x, w.y, 21)));
   const float f2 = __uint_as_float(mad_hi_u32(w.y, 1u << 22, 0x4B000000u));   // (w.y >> 10) + 2^23 bits
   Node2 n;
   n.xy = __ffma2_rn(make_float2(f0, f1), make_float2(q.s[0], q.s[1]), make_float2(q.k[0], q.k[1]));
@@ -851,31 +868,36 @@ __global__ void __launch_bounds__(kS33NW * 32, 1)
   const int64_t cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const uint32_t list_base = smem_u32(S->list[warp]);
   if (list_base & (4u * kS33Ring - 1u)) __trap();             // ring addressing ORs the offset into the base
-  const uint32_t* in_w = reinterpret_cast<const uint32_t*>(rgb);
-  const int64_t nbytes = 3 * n, nfull = n / kP33Slice;
+  // This warp's slices: sl0, sl0 + stride, ...  The loop runs on 32-bit counters
+  // and running pointers (no 64-bit index arithmetic per slice): iterations
+  // below `full` are whole slices, the one after (if any) is the ragged end.
+  const int64_t stride = ncl * kS33NW, sl0 = cl * kS33NW + warp;
+  const int iters = sl0 < nslices ? (int)((nslices - 1 - sl0) / stride) + 1 : 0;
+  const int64_t nfull = n / kP33Slice;
+  const int full = sl0 < nfull ? (int)((nfull - 1 - sl0) / stride) + 1 : 0;
+  const uint32_t* pin = reinterpret_cast<const uint32_t*>(rgb) + sl0 * (kP33Slice * 3 / 4) + 3 * lane;
+  const int64_t pin_step = stride * (kP33Slice * 3 / 4);
   // bytes past the end of the buffer read as a colour of the OTHER half, so the
   // ragged last slice needs no bounds test in the scan
   const uint32_t fill = rank ? 0u : 0x80u;
-  auto load = [&](int64_t sl, uint32_t (&wd)[3]) {
-    const int64_t w0 = sl * (kP33Slice * 3 / 4) + 3 * lane;   // word index
-    if (sl < nfull) {                                           // a whole slice: no per-byte checks
+  auto load = [&](int it, const uint32_t* p, uint32_t (&wd)[3]) {
+    if (it < full) {                                            // a whole slice: no per-byte checks
 #pragma unroll
-      for (int c = 0; c < 3; ++c) wd[c] = __ldg(in_w + w0 + c);
+      for (int c = 0; c < 3; ++c) wd[c] = __ldg(p + c);
       return;
     }
+    const int64_t b0 = reinterpret_cast<const uint8_t*>(p) - rgb, nbytes = 3 * n;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {                               // the ragged end of the buffer
       uint32_t v = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        v |= (4 * (w0 + c) + k < nbytes ? (uint32_t)rgb[4 * (w0 + c) + k] : fill) << (8 * k);
+        v |= (b0 + 4 * c + k < nbytes ? (uint32_t)rgb[b0 + 4 * c + k] : fill) << (8 * k);
       wd[c] = v;
     }
   };
-  const int64_t stride = ncl * kS33NW;
-  int64_t sl = cl * kS33NW + warp;
   uint32_t nxt[3] = {};
-  if (sl < nslices) load(sl, nxt);     // first slice in flight while the CTA stages its planes
+  if (iters > 0) load(0, pin, nxt);    // first slice in flight while the CTA stages its planes
   lut_quant_setup(lat4, 33 * 33 * 33, &S->q, S->red);   // ends with __syncthreads
   const LutQuant q = S->q;
   if (q.on) {
@@ -887,57 +909,64 @@ __global__ void __launch_bounds__(kS33NW * 32, 1)
   const uint32_t pk_base = smem_u32(S->pk) - rank * (16u * kL33Plane * 8u);
   const uint32_t lt = lanemask_lt();
   const uint32_t flip = rank ? 0u : 0x80808080u;   // after the flip, bit 7 of r set <=> the pixel is mine
-  uint32_t head_b = 0;                 // ring byte offset of the oldest pending entry
-  uint32_t tag0 = (4u * lane) << 24;   // pos << 24 | slice parity << 31 of the lane's first pixel
-  int cnt = 0;
-  float *q0 = out, *q1 = out;
-  auto round = [&](int m) {
-    if (q.on) s33_round<METHOD, true, PLANAR>(list_base, head_b, m, rank, lane, pk_base, lat4, q, q0, q1, n);
-    else s33_round<METHOD, false, PLANAR>(list_base, head_b, m, rank, lane, pk_base, lat4, q, q0, q1, n);
-    head_b += 4u * (uint32_t)m;
-    cnt -= m;
-  };
-  for (; sl < nslices; sl += stride) {
-    const uint32_t w0 = nxt[0], w1 = nxt[1], w2 = nxt[2];
-    if (sl + stride < nslices) load(sl + stride, nxt);
-    float* qs = out + (PLANAR ? 1 : 3) * (sl * kP33Slice);
-    if ((int32_t)tag0 < 0) q1 = qs; else q0 = qs;
-    const int old = cnt;
-    // ---- my pixels of the slice: pixel column k = pixels 4 lane + k.  The r bytes
-    // of the four pixels sit at byte 0 / 3 of w0, byte 2 of w1, byte 1 of w2.
-    const uint32_t f0 = w0 ^ flip, f1 = w1 ^ flip, f2 = w2 ^ flip;
-    const bool m0 = f0 & 0x80u, m1 = f0 & 0x80000000u, m2 = f1 & 0x800000u, m3 = f2 & 0x8000u;
-    const uint32_t e0 = __byte_perm(w0, tag0, 0x7210);
-    const uint32_t e1 = (__byte_perm(w0, w1, 0x0543) & 0xFFFFFFu) | (tag0 + (1u << 24));
-    const uint32_t e2 = (__byte_perm(w1, w2, 0x0432) & 0xFFFFFFu) | (tag0 + (2u << 24));
-    const uint32_t e3 = __byte_perm(w2, tag0 + (3u << 24), 0x7321);
-    // list order = pixel order (lane-major): a round's 32 entries then cover ~64
-    // consecutive pixels, so its stores touch ~24 sectors; appending column by
-    // column (entries 16 B apart... one sector each) measured 116 vs 128 Gpix/s
-    const uint32_t bal0 = __ballot_sync(0xffffffffu, m0), bal1 = __ballot_sync(0xffffffffu, m1),
-                   bal2 = __ballot_sync(0xffffffffu, m2), bal3 = __ballot_sync(0xffffffffu, m3);
-    const int pre = __popc(bal0 & lt) + __popc(bal1 & lt) + __popc(bal2 & lt) + __popc(bal3 & lt);
-    uint32_t a = head_b + 4u * (uint32_t)(cnt + pre);
-    constexpr uint32_t RM = 4u * kS33Ring - 4u;
-    if (m0) sts_u32(list_base | (a & RM), e0);
-    a += m0 ? 4u : 0u;
-    if (m1) sts_u32(list_base | (a & RM), e1);
-    a += m1 ? 4u : 0u;
-    if (m2) sts_u32(list_base | (a & RM), e2);
-    a += m2 ? 4u : 0u;
-    if (m3) sts_u32(list_base | (a & RM), e3);
-    cnt += __popc(bal0) + __popc(bal1) + __popc(bal2) + __popc(bal3);
-    MACT_DCHECK(cnt <= kS33Ring);
-    __syncwarp();
-    // ---- full rounds; a remainder from before this slice goes out now
-    if (cnt >= 32) {
-      do round(32); while (cnt >= 32);
-    } else if (old > 0) {
-      round(cnt);
+  // PK: fixed-point nodes from my planes, else fp32 nodes from the L2 lattice (decided once)
+  auto body = [&](auto pk_tag) {
+    constexpr bool PK = decltype(pk_tag)::value;
+    uint32_t head_b = 0;                 // ring byte offset of the oldest pending entry
+    uint32_t tag0 = (4u * lane) << 24;   // pos << 24 | slice parity << 31 of the lane's first pixel
+    int cnt = 0;
+    float* qs = out + (PLANAR ? 1 : 3) * (sl0 * kP33Slice);   // output of the slice's first pixel
+    const int64_t qs_step = (PLANAR ? 1 : 3) * (stride * kP33Slice);
+    float *q0 = out, *q1 = out;
+    auto round = [&](int m) {
+      s33_round<METHOD, PK, PLANAR>(list_base, head_b, m, rank, lane, pk_base, lat4, q, q0, q1, n);
+      head_b += 4u * (uint32_t)m;
+      cnt -= m;
+    };
+    for (int it = 0; it < iters; ++it, qs += qs_step) {
+      const uint32_t w0 = nxt[0], w1 = nxt[1], w2 = nxt[2];
+      pin += pin_step;
+      if (it + 1 < iters) load(it + 1, pin, nxt);
+      if ((int32_t)tag0 < 0) q1 = qs; else q0 = qs;
+      const int old = cnt;
+      // ---- my pixels of the slice: pixel column k = pixels 4 lane + k.  The r bytes
+      // of the four pixels sit at byte 0 / 3 of w0, byte 2 of w1, byte 1 of w2.
+      const uint32_t f0 = w0 ^ flip, f1 = w1 ^ flip, f2 = w2 ^ flip;
+      const bool m0 = f0 & 0x80u, m1 = f0 & 0x80000000u, m2 = f1 & 0x800000u, m3 = f2 & 0x8000u;
+      const uint32_t e0 = __byte_perm(w0, tag0, 0x7210);
+      const uint32_t e1 = (__byte_perm(w0, w1, 0x0543) & 0xFFFFFFu) | (tag0 + (1u << 24));
+      const uint32_t e2 = (__byte_perm(w1, w2, 0x0432) & 0xFFFFFFu) | (tag0 + (2u << 24));
+      const uint32_t e3 = __byte_perm(w2, tag0 + (3u << 24), 0x7321);
+      // list order = pixel order (lane-major): a round's 32 entries then cover ~64
+      // consecutive pixels, so its stores touch ~24 sectors; appending column by
+      // column (a round's entries 48 B apart, one sector each) measured 116 vs 128 Gpix/s
+      const uint32_t bal0 = __ballot_sync(0xffffffffu, m0), bal1 = __ballot_sync(0xffffffffu, m1),
+                     bal2 = __ballot_sync(0xffffffffu, m2), bal3 = __ballot_sync(0xffffffffu, m3);
+      const int pre = __popc(bal0 & lt) + __popc(bal1 & lt) + __popc(bal2 & lt) + __popc(bal3 & lt);
+      uint32_t a = head_b + 4u * (uint32_t)(cnt + pre);
+      constexpr uint32_t RM = 4u * kS33Ring - 4u;
+      if (m0) sts_u32(list_base | (a & RM), e0);
+      a += m0 ? 4u : 0u;
+      if (m1) sts_u32(list_base | (a & RM), e1);
+      a += m1 ? 4u : 0u;
+      if (m2) sts_u32(list_base | (a & RM), e2);
+      a += m2 ? 4u : 0u;
+      if (m3) sts_u32(list_base | (a & RM), e3);
+      cnt += __popc(bal0) + __popc(bal1) + __popc(bal2) + __popc(bal3);
+      MACT_DCHECK(cnt <= kS33Ring);
+      __syncwarp();
+      // ---- full rounds; a remainder from before this slice goes out now
+      if (cnt >= 32) {
+        do round(32); while (cnt >= 32);
+      } else if (old > 0) {
+        round(cnt);
+      }
+      tag0 ^= 0x80000000u;
     }
-    tag0 ^= 0x80000000u;
-  }
-  if (cnt > 0) round(cnt);
+    if (cnt > 0) round(cnt);
+  };
+  if (q.on) body(std::true_type{});
+  else body(std::false_type{});
 }
 
 // Per-pixel 33^3 path for unaligned buffers: the same selection and the same
