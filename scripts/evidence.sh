@@ -6,6 +6,7 @@ set -u
 O=gpurun_out/ev; R=/tmp/ev_reps; mkdir -p $O $R; : > $O/configs.jsonl
 run() { timeout 900 python bench.py "$@" 2>>$O/configs.err | tail -1 >> $O/configs.jsonl; }
 run --steps 50 --warmup 5
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 2>>$O/configs.err | tail -1 > $O/reference_arm.json
 run --steps 20 --warmup 3 --out-dtype float64 --no-cpu-baseline
 run --workload c1 --steps 200 --warmup 10 --no-cpu-baseline
 run --workload c2 --steps 50 --warmup 5 --no-cpu-baseline

@@ -1,5 +1,5 @@
 #!/bin/bash
-# ncu --set full of the split kernel (tet + tri) and build-variant A/B: bash scripts/r02_split_ncu.sh [tags...]
+# ncu --set full of the split kernel (tet + tri) and build-variant A/B: bash scripts/lut33_split_ncu.sh [tags...]
 mkdir -p gpurun_out /tmp/reps
 export MACT_LUT33_KERNEL=split
 for m in tetrahedral trilinear; do
