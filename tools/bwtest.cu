@@ -52,6 +52,33 @@ __global__ void k_expand_cs(const uint32_t* __restrict__ in, float4* __restrict_
   }
 }
 
+// 6) the same expand with the input wrapped onto a 32 MB window (L2-resident after the first pass): DRAM sees
+//    writes only, the SMs still issue every load -- separates the DRAM read/write mix from SM-side limits
+__global__ void k_expand_l2(const uint32_t* __restrict__ in, float4* __restrict__ out, int64_t nv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t w = __ldg(in + (i & ((8LL << 20) - 1)));
+    out[i] = make_float4((float)(w & 255), (float)((w >> 8) & 255), (float)((w >> 16) & 255), (float)(w >> 24));
+  }
+}
+// 7) read-only: sum of uint4 (checks the pure read rate)
+__global__ void k_read(const uint4* __restrict__ in, uint32_t* __restrict__ sink, int64_t nv) {
+  uint32_t acc = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = __ldg(in + i);
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x12345678u) *sink = acc;
+}
+// 8) mixes r : w = 1 : k by bytes, coalesced float4 both ways (k = 1 is the copy, k = 4 the expand ratio)
+template <int K>
+__global__ void k_mix(const float4* __restrict__ in, float4* __restrict__ out, int64_t nv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(in + i);
+#pragma unroll
+    for (int k = 0; k < K; ++k) out[(int64_t)k * nv + i] = make_float4(v.x + k, v.y, v.z, v.w);
+  }
+}
+
 template <class F>
 float timeit(F f, int iters = 10) {
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -84,6 +111,22 @@ int main() {
     printf("write     grid=%5d  %.3f ms  %.1f GB/s\n", grid, ms, npx * 12 / ms / 1e6);
     ms = timeit([&] { k_copy<<<grid, 256>>>((float4*)out, (float4*)out + npx * 6 / 16, npx * 6 / 16); });
     printf("copy      grid=%5d  %.3f ms  %.1f GB/s (r+w)\n", grid, ms, npx * 12 / ms / 1e6);
+  }
+  {
+    const int grid = sms * 16;
+    float ms = timeit([&] { k_expand_l2<<<grid, 256>>>((uint32_t*)in, (float4*)out, npx * 3 / 4); });
+    printf("expand_l2 (input L2-resident)  %.3f ms  %.1f GB/s algorithmic, %.1f GB/s of writes\n", ms,
+           npx * 15 / ms / 1e6, npx * 12 / ms / 1e6);
+    uint32_t* sink; CK(cudaMalloc(&sink, 4));
+    ms = timeit([&] { k_read<<<grid, 256>>>((uint4*)out, sink, npx * 12 / 16); });
+    printf("read      %.3f ms  %.1f GB/s\n", ms, npx * 12 / ms / 1e6);
+    const int64_t nv = npx * 12 / 16 / 5;    // in: nv float4, out: K nv float4, inside the 1.6 GB buffer
+    ms = timeit([&] { k_mix<1><<<grid, 256>>>((float4*)out, (float4*)out + nv, nv); });
+    printf("mix 1:1   %.3f ms  %.1f GB/s (r+w)\n", ms, nv * 16.0 * 2 / ms / 1e6);
+    ms = timeit([&] { k_mix<2><<<grid, 256>>>((float4*)out, (float4*)out + nv, nv); });
+    printf("mix 1:2   %.3f ms  %.1f GB/s (r+w)\n", ms, nv * 16.0 * 3 / ms / 1e6);
+    ms = timeit([&] { k_mix<4><<<grid, 256>>>((float4*)out, (float4*)out + nv, nv); });
+    printf("mix 1:4   %.3f ms  %.1f GB/s (r+w)\n", ms, nv * 16.0 * 5 / ms / 1e6);
   }
   float ms = timeit([&] { cudaMemsetAsync(out, 0, npx * 12); });
   printf("memset    %.3f ms  %.1f GB/s\n", ms, npx * 12 / ms / 1e6);
