@@ -8,6 +8,8 @@ run() { timeout 900 python bench.py "$@" 2>>$O/configs.err | tail -1 >> $O/confi
 run --steps 50 --warmup 5
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 2>>$O/configs.err | tail -1 > $O/reference_arm.json
 run --steps 20 --warmup 3 --out-dtype float64 --no-cpu-baseline
+# the minimax rational itself evaluated in fp64 (MACT_LAB_EVAL=fp64) instead of the segmented fp32 cubic of it
+MACT_LAB_EVAL=fp64 timeout 900 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 0 2>>$O/configs.err | tail -1 > $O/c4_rational_fp64.json
 run --workload c1 --steps 200 --warmup 10 --no-cpu-baseline
 run --workload c2 --steps 50 --warmup 5 --no-cpu-baseline
 for g in 17 33; do for m in trilinear prism pyramidal tetrahedral; do

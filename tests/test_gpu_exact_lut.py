@@ -376,9 +376,8 @@ def test_lut_error_bound_either_format(P, n, scale, method):
 @pytest.mark.parametrize("method", O.METHODS)
 def test_lut33_both_kernels(P, monkeypatch, kernel, method):
     """Every 33^3 interpolation kernel family -- the r-split independent CTAs (the
-    default), the r-split cluster pairs (once the default for
-    interleaved output) and the component-split clusters (MACT_LUT33_KERNEL=comp;
-    default for planar output) -- against the oracle on the
+    default for both layouts), the r-split cluster pairs and the component-split
+    CTAs (MACT_LUT33_KERNEL=pair / comp) -- against the oracle on the
     same fp32 lattice: 2^20 random colours plus the cube's corners and faces,
     interleaved, planar and unaligned (per-pixel kernel) outputs."""
     monkeypatch.setenv("MACT_LUT33_KERNEL", kernel)
