@@ -168,9 +168,9 @@ int mact_lut_interp_real(const double* lattice64, int grid_n, int method, int an
                          void* stream);
 /* Test/debug entry (no reference counterpart): the node indices and fp32
  * weights exactly as the uint8 INTERPOLATION kernels of mact_lut_interp select
- * them (their own device function: tetrahedral order from max/min/sum, 17^3
- * ghost cells at p = 255), indices mapped back to the n^3 lattice.  The parity
- * tests check that the nonzero-weight nodes equal lut.node_weights' (lut.py:115-199). */
+ * them (their own device function: the reference's cells; tetrahedral order
+ * from max / min keys, so a tie's zero-weight node may be another corner).  The
+ * parity tests check that the nonzero-weight nodes equal lut.node_weights' (lut.py:115-199). */
 int mact_lut_nodes_timed(int grid_n, int method, const uint8_t* rgb, int64_t n, int32_t* nodes,
                          float* weights, void* stream);
 /* replaces mact.lut.build_cache (lut.py:265-291): per cell of the (n-1)^3
