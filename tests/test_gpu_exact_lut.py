@@ -395,6 +395,35 @@ def test_lut33_both_kernels(P, monkeypatch, kernel, method):
     check_lab(P["lut"].interpolate(lt, d[1:], method).cpu().numpy(), ref[1:])
 
 
+@pytest.mark.parametrize("skew", ["dark", "bright", "mostly_dark", "half_image"])
+def test_lut33_split_skewed_images(P, skew):
+    """k_lut33_split on images whose pixels sit mostly or wholly in one r-half
+    (one CTA of each pair then only scans): all-dark, all-bright, 95 % dark and
+    dark-first-half images against the oracle, interleaved == planar bit for
+    bit, ragged size."""
+    lt = P["lut"].build_lut("lab", 33)
+    rng = np.random.default_rng(len(skew))
+    n = (1 << 21) + 77
+    img = rng.integers(0, 256, (n, 3), dtype=np.uint8)
+    if skew == "dark":
+        img[:, 0] &= 0x7F
+    elif skew == "bright":
+        img[:, 0] |= 0x80
+    elif skew == "mostly_dark":
+        img[rng.random(n) < 0.95, 0] &= 0x7F
+    else:
+        img[: n // 2, 0] &= 0x7F
+        img[n // 2:, 0] |= 0x80
+    vals = lt.values.astype(np.float32).astype(np.float64)
+    d = dev(img)
+    for method in ("trilinear", "tetrahedral"):
+        got = P["lut"].interpolate(lt, d, method).cpu().numpy()
+        check_lab(got, O.interpolate(vals, img, method))
+        n4 = n // 4 * 4
+        planar = P["lut"].interpolate(lt, d[:n4], method, layout="planar").cpu().numpy()
+        np.testing.assert_array_equal(planar.T, got[:n4])
+
+
 _SKEW_CHILD = r"""
 import sys, numpy as np, torch
 sys.path.insert(0, sys.argv[1])
