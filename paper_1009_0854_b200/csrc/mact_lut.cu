@@ -1706,6 +1706,7 @@ static int launch_interp(const float* lat, const uint8_t* rgb, float* out, int64
   // CTAs for planar output (lut33_comp); unaligned buffers take the per-pixel
   // kernels with the same arithmetic.
   if constexpr (N == 33) {
+    if (n <= 0) return MACT_OK;
     const int k = lut33_kernel(planar);
     return k == kLut33Comp   ? launch_lut33_comp<METHOD>(lat, rgb, out, n, planar, st)
            : k == kLut33Pair ? launch_lut33_pair<METHOD>(lat, rgb, out, n, planar, st)

@@ -395,6 +395,23 @@ def test_lut33_both_kernels(P, monkeypatch, kernel, method):
     check_lab(P["lut"].interpolate(lt, d[1:], method).cpu().numpy(), ref[1:])
 
 
+@pytest.mark.parametrize("layout", ["interleaved", "planar"])
+def test_lut33_tiny_and_ragged_sizes(P, layout):
+    """33^3 on sizes around the 128-pixel slice and the empty input (one launch
+    per size through the default kernel): every size matches the oracle."""
+    lt = P["lut"].build_lut("lab", 33)
+    vals = lt.values.astype(np.float32).astype(np.float64)
+    rng = np.random.default_rng(128)
+    for n in (0, 1, 2, 3, 5, 127, 128, 129, 255, 257, 4095, 4097):
+        img = rng.integers(0, 256, (n, 3), dtype=np.uint8)
+        got = P["lut"].interpolate(lt, dev(img), "tetrahedral", layout=layout).cpu().numpy()
+        if layout == "planar":
+            got = got.T
+        assert got.shape == (n, 3)
+        if n:
+            check_lab(got, O.interpolate(vals, img, "tetrahedral"))
+
+
 @pytest.mark.parametrize("skew", ["dark", "bright", "mostly_dark", "half_image"])
 def test_lut33_split_skewed_images(P, skew):
     """k_lut33_split on images whose pixels sit mostly or wholly in one r-half
