@@ -75,3 +75,46 @@ def test_permutation_equivariance(M, img, space):
     a = fn(flat)[perm]
     b = fn(np.ascontiguousarray(flat[perm]))
     np.testing.assert_array_equal(a, b)
+
+
+@st.composite
+def device_views(draw):
+    """A device image of 1 .. 400k pixels as a view at a byte offset of 0..3 into its buffer (16-byte
+    aligned, 4-byte aligned or unaligned input), with a colour distribution that is uniform, confined
+    to one r-half, or mostly in one r-half (the 33^3 kernel's CTAs split the pixels by bit 7 of r)."""
+    n = draw(st.one_of(st.integers(1, 700), st.integers(3000, 20000), st.integers(100_000, 400_000)))
+    off = draw(st.sampled_from([0, 0, 4, 8, 1, 3]))
+    kind = draw(st.sampled_from(["uniform", "dark", "bright", "mostly_dark", "runs"]))
+    seed = draw(st.integers(0, 2 ** 31 - 1))
+    rng = np.random.default_rng(seed)
+    img = rng.integers(0, 256, (n, 3), dtype=np.uint8)
+    if kind == "dark":
+        img[:, 0] &= 0x7F
+    elif kind == "bright":
+        img[:, 0] |= 0x80
+    elif kind == "mostly_dark":
+        img[rng.random(n) < 0.9, 0] &= 0x7F
+    elif kind == "runs":                       # runs of ~200 pixels alternating between the halves
+        img[(np.arange(n) // 200) % 2 == 0, 0] &= 0x7F
+        img[(np.arange(n) // 200) % 2 == 1, 0] |= 0x80
+    return img, off
+
+
+@settings(max_examples=200, deadline=None, suppress_health_check=list(HealthCheck))
+@given(view=device_views(), grid=st.sampled_from([17, 33, 33]),
+       method=st.sampled_from(["trilinear", "prism", "pyramidal", "tetrahedral"]),
+       layout=st.sampled_from(["interleaved", "planar"]))
+def test_lut_device_views_random(M, view, grid, method, layout):
+    """The streaming / split LUT kernels on device buffers of arbitrary size and alignment: every
+    combination matches the oracle within the tolerance."""
+    img, off = view
+    n = img.shape[0]
+    buf = torch.zeros(3 * n + 16, dtype=torch.uint8, device="cuda")
+    buf[off:off + 3 * n] = torch.from_numpy(img.reshape(-1)).cuda()
+    x = buf[off:off + 3 * n].view(n, 3)
+    L = M["lut"].build_lut("lab", grid)
+    got = M["lut"].interpolate(L, x, method, layout=layout).cpu().numpy()
+    if layout == "planar":
+        got = got.T
+    vals = O.build_lut_values("lab", grid).astype(np.float32).astype(np.float64)
+    check_lab(got, O.interpolate(vals, img, method))
