@@ -40,6 +40,15 @@
 #ifndef MACT_LUT_SIN
 #define MACT_LUT_SIN 3
 #endif
+// 17^3 tile shape (R02 sweep on C3, tri / prism / pyr / tet): G = 2 groups of 128 pixels per warp and tile
+// 162 / 174 / 196 / 226 against 156 / 176 / 199 / 230 for G = 1, so trilinear (one CTA per SM) takes 2 and the
+// others 1; two output staging buffers per warp (NOB = 2) 171 / 192 / 222: slower; SIN = 2 with NOB = 2 the same.
+#ifndef MACT_LUT_G
+#define MACT_LUT_G 1
+#endif
+#ifndef MACT_LUT_NOB
+#define MACT_LUT_NOB 1
+#endif
 #ifndef MACT_LUT33_TRI_PB
 #define MACT_LUT33_TRI_PB 1
 #endif
@@ -1713,7 +1722,7 @@ static int launch_interp(const float* lat, const uint8_t* rgb, float* out, int64
                              : launch_lut33_split<METHOD>(lat, rgb, out, n, planar, st);
   } else
     return launch_stream_t<OpLut<N, METHOD>, (OpLut<N, METHOD>::PAIR ? MACT_LUT_NW_TRI17 : MACT_LUT_NW),
-                           (N <= 9 ? 2 : 1), MACT_LUT_SIN, 1>(
+                           (N <= 9 || OpLut<N, METHOD>::PAIR ? 2 : MACT_LUT_G), MACT_LUT_SIN, MACT_LUT_NOB>(
         rgb, outs, n, planar, p, st, "lut_interp");
 }
 
